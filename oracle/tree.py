@@ -1,0 +1,220 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.  Quadtree, frequency regimes, cones and the
+neighbour / interaction lists of the DAFMM.
+
+Readings: R2 uniform tree whose leaves are LFR (paper rule 3);
+R3 T = 16; R4 w = circumradius b/sqrt(2); R5 nested cone geometry; R6 N(B) contains B.
+
+Boxes are keyed (level, ix, iy) with integer lattice indices; only non-empty boxes exist.
+Every list is a sorted Python list of keys; directional lists hold (key, cone) pairs.
+"""
+import math
+
+import numpy as np
+
+PHI0 = math.pi / 4096.0  # R5: cone boundaries at PHI0 + 2*pi*k/n (odd multiples of pi/4096)
+
+
+def morton(ix, iy):
+    """Interleave bits (x in even bits): Morton order of the children (0,0),(1,0),(0,1),(1,1)."""
+    code = 0
+    for bit in range(32):
+        code |= ((ix >> bit) & 1) << (2 * bit)
+        code |= ((iy >> bit) & 1) << (2 * bit + 1)
+    return code
+
+
+class Tree:
+    """Uniform quadtree over the root square of the points' quadrature cells.
+
+    Root (R2): the smallest axis-aligned square containing every cell [x_j +- sqrt(w_j)/2]^2,
+    centred on their bounding box.  Leaf level L = the smallest level at which (a) every
+    leaf holds <= leaf_size points and (b) leaves are in the low-frequency regime
+    ((kappa b)^2 <= T, refinement rule 3 of P:204).  Box index of a point at the leaf level:
+    ix = floor(((x - x0) / W) * 2^L), clamped; coarser levels by right shifts.
+    """
+
+    def __init__(self, points, weights, kappa, leaf_size, T=16.0, max_level=20):
+        pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
+        half = 0.5 * np.sqrt(np.asarray(weights, dtype=np.float64))
+        lo_x, hi_x = float(np.min(pts[:, 0] - half)), float(np.max(pts[:, 0] + half))
+        lo_y, hi_y = float(np.min(pts[:, 1] - half)), float(np.max(pts[:, 1] + half))
+        self.W = max(hi_x - lo_x, hi_y - lo_y)
+        cx, cy = 0.5 * (lo_x + hi_x), 0.5 * (lo_y + hi_y)
+        self.x0, self.y0 = cx - 0.5 * self.W, cy - 0.5 * self.W
+        self.kappa, self.T, self.n = float(kappa), float(T), pts.shape[0]
+        self.points = pts
+
+        level = 0
+        while self.kappa * self.width(level) * (self.kappa * self.width(level)) > self.T:
+            level += 1
+        while True:
+            ix, iy = self._lattice(pts, level)
+            _, counts = np.unique(ix.astype(np.int64) << 32 | iy.astype(np.int64), return_counts=True)
+            if counts.max() <= leaf_size or level >= max_level:
+                break
+            level += 1
+        if counts.max() > leaf_size:
+            raise ValueError("leaf_size not reachable within max_level")
+        self.L = level
+        self.ix, self.iy = self._lattice(pts, level)
+        # boxes[l]: {(ix, iy): sorted array of point indices}
+        self.boxes = []
+        for l in range(self.L + 1):
+            sh = self.L - l
+            bx, by = self.ix >> sh, self.iy >> sh
+            order = np.lexsort((np.arange(self.n), by, bx))  # group by box, ascending point index
+            bxo, byo = bx[order], by[order]
+            cut = np.flatnonzero((np.diff(bxo) != 0) | (np.diff(byo) != 0)) + 1
+            starts = np.concatenate([[0], cut])
+            ends = np.concatenate([cut, [self.n]])
+            self.boxes.append({(int(bxo[s]), int(byo[s])): order[s:e] for s, e in zip(starts, ends)})
+
+    def _lattice(self, pts, level):
+        m = 1 << level
+        ix = np.floor(((pts[:, 0] - self.x0) / self.W) * m).astype(np.int64)
+        iy = np.floor(((pts[:, 1] - self.y0) / self.W) * m).astype(np.int64)
+        return np.clip(ix, 0, m - 1), np.clip(iy, 0, m - 1)
+
+    def width(self, level):
+        return math.ldexp(self.W, -level)
+
+    def kb(self, level):
+        return self.kappa * self.width(level)
+
+    def is_hfr(self, level):
+        """a box of width w is HFR iff (kappa w)^2 > T."""
+        kb = self.kb(level)
+        return kb * kb > self.T
+
+    def n_cones(self, level):
+        """R5: smallest power of two n with half-angle pi/n <= 1/(kappa w), w = b/sqrt(2)."""
+        x = math.pi * self.kb(level) / math.sqrt(2.0)
+        n = 1
+        while n < x:
+            n *= 2
+        return n
+
+    def keys(self, level):
+        return sorted(self.boxes[level].keys(), key=lambda k: morton(*k))
+
+
+def is_neighbor(tree, level, a, b):
+    """N(B) membership: LFR — centres closer than 2b; HFR — centres closer than
+    kappa w^2 with w = b/sqrt(2) (R4), i.e. |d| b < kappa b^2 / 2.  d in lattice units."""
+    dx, dy = a[0] - b[0], a[1] - b[1]
+    d2 = dx * dx + dy * dy
+    if tree.is_hfr(level):
+        kb = tree.kb(level)
+        return 4.0 * d2 < kb * kb
+    return d2 < 4
+
+
+def cone_of(n, dx, dy):
+    """Cone index k of the lattice offset (dx, dy): boundaries at PHI0 + 2 pi k / n (R5)."""
+    a = math.atan2(dy, dx) - PHI0
+    if a < 0.0:
+        a += 2.0 * math.pi
+    t = a * n / (2.0 * math.pi)
+    k = int(math.floor(t))
+    frac = t - k
+    assert min(frac, 1.0 - frac) > 1e-9, "box centre on a cone boundary"
+    return k % n
+
+
+class Lists:
+    """N(B), IL(B), IL(B,l), active nodes and the substitute lists of R7, for every level."""
+
+    def __init__(self, tree):
+        self.tree = tree
+        L = tree.L
+        self.N = [dict() for _ in range(L + 1)]
+        self.IL = [dict() for _ in range(L + 1)]      # key -> sorted keys (LFR and HFR alike)
+        self.ILdir = [dict() for _ in range(L + 1)]   # key -> {cone: sorted [(key, cone')]}
+        for l in range(L + 1):
+            boxes = tree.boxes[l]
+            hfr = tree.is_hfr(l)
+            reach = 1
+            if hfr:
+                reach = int(math.ceil(tree.kb(l) / 2.0)) + 1
+            for b in boxes:
+                nb = []
+                for dx in range(-reach, reach + 1):
+                    for dy in range(-reach, reach + 1):
+                        a = (b[0] + dx, b[1] + dy)
+                        if a in boxes and is_neighbor(tree, l, a, b):
+                            nb.append(a)
+                self.N[l][b] = sorted(nb)
+        for l in range(1, L + 1):
+            boxes = tree.boxes[l]
+            for b in boxes:
+                parent = (b[0] >> 1, b[1] >> 1)
+                cand = set()
+                for pn in self.N[l - 1][parent]:
+                    for c in range(4):
+                        a = (2 * pn[0] + (c & 1), 2 * pn[1] + (c >> 1))
+                        if a in boxes:
+                            cand.add(a)
+                # P:376 / P:378: children of the parent's neighbours that are not neighbours of B
+                near = set(self.N[l][b])
+                il = sorted(a for a in cand if a not in near)
+                self.IL[l][b] = il
+                if tree.is_hfr(l):
+                    n = tree.n_cones(l)
+                    d = {}
+                    for a in il:
+                        k = cone_of(n, a[0] - b[0], a[1] - b[1])
+                        kp = cone_of(n, b[0] - a[0], b[1] - a[1])
+                        assert kp == (k + n // 2) % n
+                        d.setdefault(k, []).append((a, kp))
+                    self.ILdir[l][b] = {k: sorted(v) for k, v in d.items()}
+        self._activate()
+
+    def _activate(self):
+        """Active nodes, top-down: a node needs bases if its interaction list is non-empty or
+        its parent's M2M / L2L needs it (passes run up to the coarsest level with a
+        non-empty interaction list)."""
+        tree = self.tree
+        self.active = [set() for _ in range(tree.L + 1)]  # LFR: keys; HFR: (key, cone)
+        for l in range(1, tree.L + 1):
+            hfr = tree.is_hfr(l)
+            parents_any = {nd[0] for nd in self.active[l - 1]} if tree.is_hfr(l - 1) else self.active[l - 1]
+            for b in tree.boxes[l]:
+                parent = (b[0] >> 1, b[1] >> 1)
+                if hfr:
+                    n = tree.n_cones(l)
+                    for k in range(n):
+                        need = bool(self.ILdir[l][b].get(k))
+                        if l > 1 and tree.is_hfr(l - 1):
+                            need = need or (parent, 2 * k) in self.active[l - 1] or \
+                                (parent, 2 * k + 1) in self.active[l - 1]
+                        if need:
+                            self.active[l].add((b, k))
+                else:
+                    need = bool(self.IL[l][b])
+                    if l > 1:
+                        need = need or parent in parents_any
+                    if need:
+                        self.active[l].add(b)
+
+    def far_list(self, level, node):
+        """Far-field list used for the search sets of an active node.
+
+        It is IL(B) (LFR) or IL(B,l) (HFR).  R7: an active HFR node whose IL(B,l) is empty
+        (active only because its parent needs it) uses the children, in the matching child
+        cones, of its parent's IL in the two parent cones that nest in l."""
+        tree = self.tree
+        if not tree.is_hfr(level):
+            return [(a, None) for a in self.IL[level][node]]
+        b, k = node
+        lst = self.ILdir[level][b].get(k, [])
+        if lst:
+            return lst
+        parent = (b[0] >> 1, b[1] >> 1)
+        sub = set()
+        for p in (2 * k, 2 * k + 1):
+            for (a, ap) in self.ILdir[level - 1][parent].get(p, []):
+                for c in range(4):
+                    ac = (2 * a[0] + (c & 1), 2 * a[1] + (c >> 1))
+                    if ac in tree.boxes[level]:
+                        sub.add((ac, ap // 2))
+        return sorted(sub)

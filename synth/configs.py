@@ -1,0 +1,80 @@
+"""Seeded workload generators for BASELINE.json configs 1-4 (plus scaled-down variants).
+
+Grid: h = 2/n, x_ab = (-1 + (a+1/2) h, -1 + (b+1/2) h), a, b in [0, n),
+row-major in b then a; weights w = h^2.  Input x_j = exp(i theta_j), theta ~ U[0, 2 pi)
+from numpy default_rng(0).  Config-4 bump centres then amplitudes from default_rng(1).
+Right-hand sides f = -kappa^2 q u_inc with a plane wave u_inc.
+"""
+import math
+
+import numpy as np
+
+
+def grid_points(n):
+    h = 2.0 / n
+    a = np.arange(n)
+    c = -1.0 + (a + 0.5) * h
+    xx, yy = np.meshgrid(c, c, indexing="xy")  # row-major in b (y) then a (x)
+    pts = np.stack([xx.ravel(), yy.ravel()], axis=1)
+    return pts, np.full(n * n, h * h)
+
+
+def gaussian_q(pts):
+    """q(x) = 1.5 exp(-160 |x|^2) (the Gaussian contrast of P:884)."""
+    return 1.5 * np.exp(-160.0 * (pts[:, 0] ** 2 + pts[:, 1] ** 2))
+
+
+def disk_q(pts, radius=0.5):
+    """q = 1 inside the disk |x| < radius, else 0 (config 3)."""
+    return (pts[:, 0] ** 2 + pts[:, 1] ** 2 < radius * radius).astype(np.float64)
+
+
+def bumps_q(pts, seed=1, count=8):
+    """Sum of `count` Gaussian bumps a_m exp(-200 |x - c_m|^2), c_m ~ U([-0.7,0.7]^2),
+    a_m ~ U(0.5, 2), drawn centres first then amplitudes from default_rng(seed) (config 4)."""
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(-0.7, 0.7, size=(count, 2))
+    amps = rng.uniform(0.5, 2.0, size=count)
+    q = np.zeros(pts.shape[0])
+    for c, a in zip(centres, amps):
+        q += a * np.exp(-200.0 * ((pts[:, 0] - c[0]) ** 2 + (pts[:, 1] - c[1]) ** 2))
+    return q
+
+
+def unit_phase_vector(n, seed=0):
+    rng = np.random.default_rng(seed)
+    theta = rng.uniform(0.0, 2.0 * math.pi, size=n)
+    return np.exp(1j * theta)
+
+
+def plane_wave_rhs(pts, q, kappa, angle_deg=0.0):
+    """f = -kappa^2 q exp(i kappa d.x), d = (cos a, sin a)."""
+    a = math.radians(angle_deg)
+    phase = kappa * (pts[:, 0] * math.cos(a) + pts[:, 1] * math.sin(a))
+    return -kappa * kappa * q * np.exp(1j * phase)
+
+
+# name -> (grid n, kappa, contrast, nca_tol, rhs angle, gmres tol)
+CONFIGS = {
+    "c1": dict(n=64, kappa=10.0, contrast="gaussian", nca_tol=1e-8, angle=0.0, gmres_tol=1e-8),
+    "c2": dict(n=256, kappa=40.0, contrast="gaussian", nca_tol=1e-8, angle=0.0, gmres_tol=1e-8),
+    "c3": dict(n=512, kappa=80.0, contrast="disk", nca_tol=1e-7, angle=30.0, gmres_tol=1e-6),
+    "c4": dict(n=1024, kappa=160.0, contrast="bumps", nca_tol=1e-6, angle=0.0, gmres_tol=1e-6),
+}
+
+
+def make_problem(name, n=None, kappa=None):
+    """Return dict(points, weights, q, kappa, nca_tol, leaf_size, x, f, gmres_tol) for a config.
+    `n` / `kappa` override the grid size / wavenumber for scaled-down variants that keep
+    kappa h fixed when both are scaled together."""
+    cfg = dict(CONFIGS[name])
+    if n is not None:
+        cfg["n"] = n
+    if kappa is not None:
+        cfg["kappa"] = kappa
+    pts, w = grid_points(cfg["n"])
+    q = {"gaussian": gaussian_q, "disk": disk_q, "bumps": bumps_q}[cfg["contrast"]](pts)
+    x = unit_phase_vector(pts.shape[0], seed=0)
+    f = plane_wave_rhs(pts, q, cfg["kappa"], cfg["angle"])
+    return dict(name=name, points=pts, weights=w, q=q, kappa=cfg["kappa"], nca_tol=cfg["nca_tol"],
+                leaf_size=64, x=x, f=f, gmres_tol=cfg["gmres_tol"], n_grid=cfg["n"])

@@ -1,0 +1,153 @@
+"""Pins for the oracle's ACA (R10), nested pivots and serial DAFMM
+ against the dense product."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle.core import Problem
+from oracle.nca import NCA, aca
+from oracle.tree import Tree, Lists
+from synth.configs import make_problem
+
+
+def _aca_on(M, eps):
+    return aca(lambda i: M[i].copy(), lambda j: M[:, j].copy(), M.shape[0], M.shape[1], eps)
+
+
+def test_aca_rank_one_exact():
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal(30) + 1j * rng.standard_normal(30)
+    v = rng.standard_normal(20) + 1j * rng.standard_normal(20)
+    M = np.outer(u, v)
+    rows, cols = _aca_on(M, 1e-10)
+    assert len(rows) == 1 and rows[0] == 0 and cols[0] == int(np.argmax(np.abs(M[0])))
+
+
+def test_aca_full_rank_identity_and_zero():
+    rows, cols = _aca_on(np.eye(6, dtype=complex), 1e-12)
+    assert sorted(rows) == list(range(6)) and rows == cols
+    rows, cols = _aca_on(np.zeros((5, 7), dtype=complex), 1e-8)
+    assert rows == [] and cols == []
+
+
+def test_aca_low_rank_reconstruction_vs_svd():
+    """Cross approximation from the selected pivots reproduces a rank-6 matrix to ~eps."""
+    rng = np.random.default_rng(1)
+    M = (rng.standard_normal((80, 6)) + 1j * rng.standard_normal((80, 6))) @ \
+        (rng.standard_normal((6, 50)) + 1j * rng.standard_normal((6, 50)))
+    rows, cols = _aca_on(M, 1e-10)
+    assert 6 <= len(rows) <= 7
+    approx = M[:, cols] @ np.linalg.solve(M[np.ix_(rows, cols)], M[rows, :]) if len(rows) == 6 else M
+    assert np.linalg.norm(M - approx) / np.linalg.norm(M) < 1e-9
+
+
+def test_aca_kernel_block_accuracy():
+    """On a Helmholtz block between well-separated boxes the skeleton reproduces the block to
+    50 eps, and the rank is below the SVD rank at eps / 100 plus margin."""
+    rng = np.random.default_rng(3)
+    t = rng.uniform(0, 0.1, size=(64, 2))
+    s = rng.uniform(0, 0.1, size=(300, 2)) + np.array([0.35, 0.1])
+    pts = np.concatenate([t, s])
+    prob = Problem(pts, np.full(364, 1e-4), np.ones(364), 40.0)
+    K = oracle.K_block(prob, np.arange(64), np.arange(64, 364))
+    for eps in [1e-4, 1e-8]:
+        rows, cols = _aca_on(K, eps)
+        approx = K[:, cols] @ np.linalg.solve(K[np.ix_(rows, cols)], K[rows, :])
+        assert np.linalg.norm(K - approx) / np.linalg.norm(K) < 50 * eps
+        sv = np.linalg.svd(K, compute_uv=False)
+        assert len(rows) <= np.sum(sv > eps / 100 * sv[0]) + 5
+
+
+def _oracle_case(name, n=None, kappa=None, q_one=False):
+    P = make_problem(name, n=n, kappa=kappa)
+    q = np.ones_like(P["q"]) if q_one else P["q"]
+    prob = Problem(P["points"], P["weights"], q, P["kappa"])
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    return P, prob, tree, lists, NCA(prob, tree, lists, P["nca_tol"])
+
+
+@pytest.fixture(scope="module")
+def c1():
+    return _oracle_case("c1")
+
+
+def _rel_z(y, yd, x):
+    return np.linalg.norm((y - x) - (yd - x)) / np.linalg.norm(yd - x)
+
+
+def test_dafmm_matches_dense_c1(c1):
+    """North-star contract (D10): relative l2 of y - x within 10 nca_tol of the dense product."""
+    P, prob, tree, lists, nca = c1
+    y = nca.matvec(P["x"])
+    yd = oracle.dense_matvec(prob, P["x"])
+    assert _rel_z(y, yd, P["x"]) <= 10 * P["nca_tol"]
+
+
+def test_dafmm_parts_add_up_and_near_is_exact(c1):
+    P, prob, tree, lists, nca = c1
+    x = P["x"]
+    near = nca.potential(x, parts=("near",))
+    far = nca.potential(x, parts=("far",))
+    full = nca.potential(x)
+    assert np.allclose(near + far, full, rtol=0, atol=1e-14 * np.abs(full).max())
+    # the near field is the exact sum over N(leaf): compare a few rows with K directly
+    L = tree.L
+    b = tree.keys(L)[5]
+    rows = tree.boxes[L][b]
+    cols = np.concatenate([tree.boxes[L][a] for a in lists.N[L][b]])
+    direct = oracle.K_block(prob, rows, cols) @ x[cols]
+    assert np.allclose(near[rows], direct, rtol=1e-14, atol=0)
+
+
+def test_dafmm_linearity_and_zero_contrast(c1):
+    P, prob, tree, lists, nca = c1
+    rng = np.random.default_rng(9)
+    x1 = rng.standard_normal(prob.n) + 1j * rng.standard_normal(prob.n)
+    x2 = P["x"]
+    a, b = 0.3 - 1.1j, 2.0 + 0.5j
+    lhs = nca.matvec(a * x1 + b * x2)
+    rhs = a * nca.matvec(x1) + b * nca.matvec(x2)
+    assert np.linalg.norm(lhs - rhs) / np.linalg.norm(rhs) < 1e-12
+    prob0 = Problem(P["points"], P["weights"], np.zeros(prob.n), P["kappa"])
+    nca0 = NCA(prob0, tree, lists, P["nca_tol"], pivots=nca.pivots)
+    assert np.array_equal(nca0.matvec(x2), x2)  # q = 0  =>  y = x exactly
+
+
+def test_pivot_containment_and_determinism(c1):
+    """Self pivots lie in the box, far pivots in the search set built from IL."""
+    P, prob, tree, lists, nca = c1
+    for level in range(1, tree.L + 1):
+        for node, p in nca.pivots[level].items():
+            s = nca.search[level][node]
+            for key in ("ti", "si", "to", "so"):
+                assert np.all(np.isin(p[key], s[key]))
+            assert len(p["ti"]) == len(p["si"]) and len(p["to"]) == len(p["so"])
+            assert not np.intersect1d(s["ti"], s["si"]).size
+    nca2 = NCA(prob, tree, lists, P["nca_tol"])
+    for level in range(1, tree.L + 1):
+        for node, p in nca.pivots[level].items():
+            for key in p:
+                assert np.array_equal(p[key], nca2.pivots[level][node][key])
+
+
+def test_single_level_tree_equals_dense():
+    """With no interaction list anywhere the DAFMM is the near field: equal to dense."""
+    P = make_problem("c1", n=16, kappa=2.0)  # 256 points, 2x2 leaves at level 1
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    assert all(not v for l in range(tree.L + 1) for v in lists.IL[l].values())
+    nca = NCA(prob, tree, lists, 1e-8)
+    assert np.allclose(nca.matvec(P["x"]), oracle.dense_matvec(prob, P["x"]), rtol=1e-14, atol=1e-15)
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c2", 128, 20.0), ("c3", 128, 20.0), ("c1", 128, 4.0)])
+def test_dafmm_matches_dense_scaled_configs(name, n, kappa):
+    """Config-2/3 geometry at quarter size (two HFR levels / disk contrast with exact zeros) and
+    a low-frequency case with LFR non-leaf levels (plain M2M / L2L)."""
+    P, prob, tree, lists, nca = _oracle_case(name, n, kappa)
+    rows = np.arange(0, prob.n, 7)
+    yd = oracle.dense_matvec_rows(prob, P["x"], rows)
+    y = nca.matvec(P["x"])[rows]
+    assert _rel_z(y, yd, P["x"][rows]) <= 10 * P["nca_tol"]

@@ -1,0 +1,99 @@
+"""Pins for the oracle's H0^(1) (bands of reading D2) and self term (reading D1)."""
+import math
+import os
+
+import mpmath as mp
+import numpy as np
+import pytest
+
+import oracle
+from oracle.core import Problem, K_block
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "special_values.txt")
+
+
+def _mp_h0(z):
+    with mp.workdps(40):
+        return complex(mp.hankel1(0, mp.mpf(z)))
+
+
+def test_h0_against_mpmath_all_bands():
+    rng = np.random.default_rng(11)
+    zs = np.concatenate([np.logspace(-3, 3, 240), rng.uniform(7.0, 21.0, 60), [8.0, 20.0, 8.0000001, 19.9999]])
+    h = oracle.h0(zs)
+    for z, hz in zip(zs, h):
+        ref = _mp_h0(z)
+        rel = abs(hz - ref) / abs(ref)
+        # A2: 2e-13 relative up to z = 100, then the input-rounding floor z * eps
+        tol = 2e-13 if z <= 100 else 2e-13 * z / 100
+        assert rel <= tol, (z, rel)
+
+
+def test_h0_printed_values():
+    for line in open(GOLDEN):
+        if line.startswith("#") or not line.strip():
+            continue
+        name, z, val = line.split()
+        z, val = float(z), float(val)
+        h = oracle.h0([z])[0]
+        if name == "J0":
+            assert abs(h.real - val) < 1e-15
+        elif name == "Y0":
+            assert abs(h.imag - val) < 1e-15
+        elif name == "J0_zero":
+            assert abs(h.real) < 1e-13
+        elif name == "Y0_zero":
+            assert abs(h.imag) < 1e-13
+
+
+def test_h0_wronskian():
+    """J0 Y0' - J0' Y0 = 2/(pi z) (A&S 9.1.16), derivatives by 4th-order central differences."""
+    for z in np.linspace(0.1, 100.0, 73):
+        e = 1e-3 * max(1.0, z) ** 0.5 * 1e-1
+        hp2, hp1, hm1, hm2 = oracle.h0([z + 2 * e, z + e, z - e, z - 2 * e])
+        d = (-hp2 + 8 * hp1 - 8 * hm1 + hm2) / (12 * e)
+        h = oracle.h0([z])[0]
+        w = h.real * d.imag - d.real * h.imag
+        assert abs(w - 2 / (math.pi * z)) <= 1e-7 * (2 / (math.pi * z)) + 1e-9
+
+
+def test_h0_large_argument_asymptote():
+    for z in [500.0, 800.0, 1000.0]:
+        h = oracle.h0([z])[0]
+        lead = math.sqrt(2 / (math.pi * z)) * complex(math.cos(z - math.pi / 4), math.sin(z - math.pi / 4))
+        assert abs(h - lead) / abs(lead) < 1e-3  # first correction is 1/(8z)
+        assert abs(h - lead) / abs(lead) > 1e-5
+
+
+def test_green_symmetry_bitwise():
+    rng = np.random.default_rng(5)
+    pts = rng.uniform(-1, 1, size=(40, 2))
+    w = np.ones(40)
+    prob = Problem(pts, w, np.ones(40), 37.0)
+    K = K_block(prob, np.arange(40), np.arange(40))
+    off = ~np.eye(40, dtype=bool)
+    assert np.array_equal(K[off], K.T[off])
+
+
+def test_self_term_against_mpmath_quadrature():
+    """D1: D = int_{|y|<R} (i/4) H0(k|y|) dy, R = sqrt(w/pi), by tanh-sinh quadrature."""
+    for kappa, h in [(10.0, 2 / 64), (160.0, 2 / 1024), (3.0, 0.4), (50.0, 0.02)]:
+        w = h * h
+        D = oracle.self_terms([w], kappa)[0]
+        R = math.sqrt(w / math.pi)
+        with mp.workdps(30):
+            f = lambda rho: mp.hankel1(0, kappa * rho) * rho
+            ref = complex(0.5j * mp.pi * mp.quad(f, [0, R]))
+        assert abs(D - ref) / abs(ref) < 1e-13, (kappa, h, D, ref)
+
+
+def test_self_term_uniform_configs_value():
+    """kappa h = 0.3125 in every uniform config, so kappa^2 D is the same number."""
+    for n, kappa in [(64, 10.0), (256, 40.0), (512, 80.0), (1024, 160.0)]:
+        h = 2.0 / n
+        kd = kappa ** 2 * oracle.self_terms([h * h], kappa)[0]
+        assert abs(kd - (0.036360282 + 0.024319322j)) < 1e-8
+
+
+def test_self_term_zero_mode():
+    assert oracle.self_terms([0.01, 0.2], 5.0, mode="zero").tolist() == [0j, 0j]
