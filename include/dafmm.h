@@ -1,0 +1,142 @@
+/*
+ * dafmm.h — C-ABI of the B200-native DAFMM matvec and GMRES for the discretised 2D
+ * Lippmann-Schwinger equation of arxiv 2204.00326 ("PAPER.md", cited P:<line>).
+ *
+ * Operation (the boundary semantics).  For points x_i, quadrature weights w_i > 0 and a
+ * real contrast q_i, the library applies the discrete operator of Eq. 12a/13
+ * in point (Nystrom) form:
+ *
+ *     y = A x,   (A x)_i = x_i + kappa^2 q_i [ sum_{j != i} G(x_i, x_j) w_j x_j + D_i x_i ]
+ *
+ * with the Helmholtz Green's function G(x,y) = (i/4) H0^(1)(kappa |x - y|) and the
+ * self term D_i = integral of G over the equal-area disk of area w_i (reading D1).
+ * The sum is evaluated by the Directional Algebraic FMM whose low-rank bases
+ * come from the nested cross approximation at tolerance nca_tol; the result
+ * matches the dense product within about 10 x nca_tol (relative l2 of y - x).
+ *
+ * Memory and ownership.  Host arrays passed to dafmm_create are copied; the caller keeps
+ * them.  Vectors passed to dafmm_matvec / ls_gmres_solve are DEVICE pointers to N complex128
+ * values stored interleaved (re, im) in the caller's point order, 16-byte aligned; they must
+ * not alias each other.  The handle owns all device memory of the plan (freed by
+ * dafmm_destroy).  Device work is enqueued on the handle's CUDA stream (default: the legacy
+ * default stream; set with dafmm_set_stream) and is asynchronous to the host unless stated.
+ *
+ * Threading.  A handle is immutable after creation apart from its scratch workspace, so calls
+ * on one handle must be serialised (same stream, one host thread at a time).  Distinct
+ * handles are independent.
+ *
+ * Errors.  Every int-returning call returns DAFMM_OK (0) on success and a negative code on
+ * error; dafmm_last_error() returns a thread-local message for the last failure.
+ * ls_gmres_solve returns DAFMM_NOT_CONVERGED (> 0) when maxit is reached — a status, not an
+ * error; psi then holds the last iterate.
+ */
+#ifndef DAFMM_H
+#define DAFMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dafmm_plan* dafmm_handle;
+
+enum {
+  DAFMM_OK = 0,
+  DAFMM_NOT_CONVERGED = 1, /* ls_gmres_solve: maxit reached before tol (not an error) */
+  DAFMM_EINVAL = -1,       /* bad argument: n <= 0, kappa <= 0 or non-finite, nca_tol not in
+                              (0,1), leaf_size < 1, NaN/Inf input, weight <= 0, duplicate
+                              points, null pointer, unsupported option */
+  DAFMM_ECUDA = -2,        /* a CUDA runtime call failed (message has the CUDA error) */
+  DAFMM_ENOMEM = -3,       /* host or device allocation failed */
+  DAFMM_ESETUP = -4        /* NCA setup failed (singular cross matrix) */
+};
+
+/* Options of dafmm_create_ex; initialise with dafmm_default_options(). */
+typedef struct {
+  double T;            /* regime threshold: a box of width b is HFR iff (kappa b)^2 > T
+                          (reading R3; default 16) */
+  int self_term;       /* 1: disk self term D1 (default); 0: D_i = 0 (point kernel) */
+  int kernel_mode;     /* 0: Lippmann-Schwinger y = x + kappa^2 q o (K x) (default);
+                          1: potential y = K x (the N-body sum of Experiment 1) */
+  int max_level;       /* deepest tree level allowed (default 16) */
+  int num_threads;     /* host threads for setup; 0 = OpenMP default */
+  int host_only;       /* 1: build the host plan only (no device upload; for inspection and
+                          dafmm_export_plan on machines without a GPU); matvec / GMRES then
+                          return DAFMM_EINVAL.  Default 0. */
+} dafmm_options;
+
+/* Statistics of a plan (sizes, ranks, setup times). */
+typedef struct {
+  int64_t n;
+  int32_t levels;            /* leaf level L */
+  int32_t n_nodes;           /* nodes with bases (LFR boxes + HFR (box, cone) pairs) */
+  int64_t p2p_pairs;         /* near-field point pairs (i, j), j != i */
+  int64_t m2l_entries;       /* kernel entries evaluated by M2L per matvec */
+  int64_t m2l_pairs;         /* node pairs in interaction lists */
+  int64_t operator_bytes;    /* bytes of stored translation operators */
+  int64_t device_bytes;      /* total device bytes owned by the handle */
+  double mean_rank_leaf_in, mean_rank_leaf_out;
+  int32_t max_rank;
+  double setup_tree_s, setup_lists_s, setup_nca_s, setup_ops_s, setup_pack_s, setup_upload_s;
+  int64_t aca_entries;       /* kernel entries evaluated by ACA during setup */
+} dafmm_stats_t;
+
+void dafmm_default_options(dafmm_options* opt);
+
+/* Build the plan on the host (tree, lists, cones, NCA pivots, operators) and
+ * upload it to the current CUDA device.
+ *   points  host, n x 2 row-major (x1, x2), fp64
+ *   weights host, n quadrature weights w_j > 0
+ *   q       host, n real contrast values q(x_i)
+ *   n, kappa > 0, leaf_size >= 1 (max points per leaf), nca_tol in (0, 1)
+ *   out     receives the handle.
+ * Synchronous.  Errors: DAFMM_EINVAL, DAFMM_ENOMEM, DAFMM_ECUDA, DAFMM_ESETUP. */
+int dafmm_create(const double* points, const double* weights, const double* q, int64_t n, double kappa,
+                 int leaf_size, double nca_tol, dafmm_handle* out);
+int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
+                    int leaf_size, double nca_tol, const dafmm_options* opt, dafmm_handle* out);
+
+/* y = A x (see the top of this file).  x, y: DEVICE pointers, n complex128 each, caller order,
+ * no aliasing.  Enqueued on the handle's stream; returns immediately. */
+int dafmm_matvec(dafmm_handle h, const void* x, void* y);
+
+/* As dafmm_matvec with only some passes: mask bit 0 = near field (P2P, including
+ * the identity and self term), bit 1 = far field (upward, transverse and downward passes,
+ * P:667-748).  mask 3 equals dafmm_matvec.  For mask 2 the identity term is omitted. */
+#define DAFMM_PART_NEAR 1u
+#define DAFMM_PART_FAR 2u
+int dafmm_matvec_parts(dafmm_handle h, const void* x, void* y, unsigned mask);
+
+/* As dafmm_matvec with HOST buffers: copies x to the device, applies A, copies y back, and
+ * synchronises the handle's stream before returning (the end-to-end path of bench.py). */
+int dafmm_matvec_host(dafmm_handle h, const void* x_host, void* y_host);
+
+/* Restarted GMRES(m) (reading R14: zero initial guess, m = restart (<= 0: 50),
+ * classical Gram-Schmidt with re-orthogonalisation on the device) for A psi = f with the
+ * DAFMM product.  f, psi: DEVICE pointers (n complex128, caller order; psi is overwritten).
+ * Stops when the implicit relative residual <= tol or after maxit inner iterations, then
+ * recomputes the true relative residual ||f - A psi|| / ||f|| into *relres_out.
+ * history (nullable, host, maxit + 1 doubles) receives the implicit residual per iteration.
+ * Synchronous.  Returns DAFMM_OK, DAFMM_NOT_CONVERGED, or an error code. */
+int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int maxit, int restart, int* iters_out,
+                   double* relres_out, double* history);
+
+/* Use stream s (a cudaStream_t) for all later device work of the handle. */
+int dafmm_set_stream(dafmm_handle h, void* stream);
+
+int dafmm_stats(dafmm_handle h, dafmm_stats_t* out);
+
+/* Write the tree, lists, cones and pivot index sets as .npy files into directory `path`
+ * (created if missing) for the independent CPU oracle.  Synchronous, host only. */
+int dafmm_export_plan(dafmm_handle h, const char* path);
+
+void dafmm_destroy(dafmm_handle h);
+
+/* Thread-local message of the last failed call on this thread ("" if none). */
+const char* dafmm_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAFMM_H */

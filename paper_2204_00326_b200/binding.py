@@ -1,0 +1,221 @@
+"""ctypes binding of include/dafmm.h (argument marshalling only).
+
+Device vectors are torch CUDA tensors of dtype complex128 (or raw integer device pointers);
+host arrays are numpy.  Functions mirror the C names; ``DAFMM`` is a small owning wrapper.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_lib", "libdafmm.so")
+_lib = None
+
+EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_matvec", "dafmm_matvec_parts",
+            "dafmm_matvec_host", "ls_gmres_solve", "dafmm_set_stream", "dafmm_stats", "dafmm_export_plan",
+            "dafmm_destroy", "dafmm_last_error"]
+
+DAFMM_OK, DAFMM_NOT_CONVERGED = 0, 1
+ERRORS = {-1: "DAFMM_EINVAL", -2: "DAFMM_ECUDA", -3: "DAFMM_ENOMEM", -4: "DAFMM_ESETUP"}
+
+
+class DAFMMError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("%s: %s" % (ERRORS.get(code, code), msg))
+        self.code = code
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_double), ("self_term", ctypes.c_int), ("kernel_mode", ctypes.c_int),
+                ("max_level", ctypes.c_int), ("num_threads", ctypes.c_int), ("host_only", ctypes.c_int)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("levels", ctypes.c_int32), ("n_nodes", ctypes.c_int32),
+                ("p2p_pairs", ctypes.c_int64), ("m2l_entries", ctypes.c_int64), ("m2l_pairs", ctypes.c_int64),
+                ("operator_bytes", ctypes.c_int64), ("device_bytes", ctypes.c_int64),
+                ("mean_rank_leaf_in", ctypes.c_double), ("mean_rank_leaf_out", ctypes.c_double),
+                ("max_rank", ctypes.c_int32),
+                ("setup_tree_s", ctypes.c_double), ("setup_lists_s", ctypes.c_double),
+                ("setup_nca_s", ctypes.c_double), ("setup_ops_s", ctypes.c_double),
+                ("setup_pack_s", ctypes.c_double), ("setup_upload_s", ctypes.c_double),
+                ("aca_entries", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def library_path():
+    return _LIB_PATH
+
+
+def load():
+    """Load the C-ABI library; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError("libdafmm.so not built: run `python -m paper_2204_00326_b200.build`")
+    lib = ctypes.CDLL(_LIB_PATH)
+    vp, i64, dbl, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+    lib.dafmm_default_options.argtypes = [ctypes.POINTER(Options)]
+    lib.dafmm_create.argtypes = [vp, vp, vp, i64, dbl, i32, dbl, ctypes.POINTER(vp)]
+    lib.dafmm_create_ex.argtypes = [vp, vp, vp, i64, dbl, i32, dbl, ctypes.POINTER(Options), ctypes.POINTER(vp)]
+    lib.dafmm_matvec.argtypes = [vp, vp, vp]
+    lib.dafmm_matvec_parts.argtypes = [vp, vp, vp, ctypes.c_uint]
+    lib.dafmm_matvec_host.argtypes = [vp, vp, vp]
+    lib.ls_gmres_solve.argtypes = [vp, vp, vp, dbl, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(dbl), vp]
+    lib.dafmm_set_stream.argtypes = [vp, vp]
+    lib.dafmm_stats.argtypes = [vp, ctypes.POINTER(Stats)]
+    lib.dafmm_export_plan.argtypes = [vp, ctypes.c_char_p]
+    lib.dafmm_destroy.argtypes = [vp]
+    lib.dafmm_destroy.restype = None
+    lib.dafmm_last_error.restype = ctypes.c_char_p
+    lib.dafmm_last_error.argtypes = []
+    _lib = lib
+    return lib
+
+
+def dafmm_last_error():
+    return load().dafmm_last_error().decode()
+
+
+def _check(rc):
+    if rc < 0:
+        raise DAFMMError(rc, dafmm_last_error())
+    return rc
+
+
+def _host(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a, a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _dev(t):
+    """Device pointer of a torch CUDA complex128 tensor (or an int pointer)."""
+    if isinstance(t, int):
+        return ctypes.c_void_p(t)
+    if not (t.is_cuda and t.is_contiguous() and str(t.dtype) == "torch.complex128"):
+        raise ValueError("expected a contiguous CUDA complex128 tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def default_options():
+    o = Options()
+    load().dafmm_default_options(ctypes.byref(o))
+    return o
+
+
+def dafmm_create_ex(points, weights, q, kappa, leaf_size, nca_tol, options=None):
+    pts, pp = _host(points, np.float64)
+    w, wp = _host(weights, np.float64)
+    qq, qp = _host(q, np.float64)
+    n = w.size
+    if pts.size != 2 * n or qq.size != n:
+        raise ValueError("points must be (n, 2) and weights, q length n")
+    h = ctypes.c_void_p()
+    opt = options if options is not None else default_options()
+    _check(load().dafmm_create_ex(pp, wp, qp, n, float(kappa), int(leaf_size), float(nca_tol), ctypes.byref(opt),
+                                  ctypes.byref(h)))
+    return h
+
+
+def dafmm_create(points, weights, q, kappa, leaf_size, nca_tol):
+    return dafmm_create_ex(points, weights, q, kappa, leaf_size, nca_tol, None)
+
+
+def dafmm_matvec(h, x, y):
+    return _check(load().dafmm_matvec(h, _dev(x), _dev(y)))
+
+
+def dafmm_matvec_parts(h, x, y, mask):
+    return _check(load().dafmm_matvec_parts(h, _dev(x), _dev(y), int(mask)))
+
+
+def dafmm_matvec_host(h, x_host, y_host):
+    """x_host, y_host: numpy complex128 arrays (pinned torch tensors also accepted via .numpy())."""
+    if x_host.dtype != np.complex128 or y_host.dtype != np.complex128:
+        raise ValueError("host vectors must be complex128")
+    return _check(load().dafmm_matvec_host(h, x_host.ctypes.data_as(ctypes.c_void_p),
+                                           y_host.ctypes.data_as(ctypes.c_void_p)))
+
+
+def ls_gmres_solve(h, f, psi, tol, maxit, restart=50, history=None):
+    """Returns (status, iterations, true relative residual); history: numpy float64 (maxit+1) or None."""
+    it = ctypes.c_int()
+    rr = ctypes.c_double()
+    hp = None
+    if history is not None:
+        if history.dtype != np.float64 or history.size < maxit + 1:
+            raise ValueError("history must be float64 with maxit + 1 entries")
+        hp = history.ctypes.data_as(ctypes.c_void_p)
+    rc = _check(load().ls_gmres_solve(h, _dev(f), _dev(psi), float(tol), int(maxit), int(restart), ctypes.byref(it),
+                                      ctypes.byref(rr), hp))
+    return rc, it.value, rr.value
+
+
+def dafmm_set_stream(h, stream):
+    """stream: a torch.cuda.Stream or a raw cudaStream_t integer."""
+    ptr = stream if isinstance(stream, int) else stream.cuda_stream
+    return _check(load().dafmm_set_stream(h, ctypes.c_void_p(ptr)))
+
+
+def dafmm_stats(h):
+    s = Stats()
+    _check(load().dafmm_stats(h, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def dafmm_export_plan(h, path):
+    return _check(load().dafmm_export_plan(h, str(path).encode()))
+
+
+def dafmm_destroy(h):
+    if h:
+        load().dafmm_destroy(h)
+
+
+class DAFMM:
+    """Owning wrapper: ``op = DAFMM(points, w, q, kappa, leaf_size, nca_tol); op.matvec(x, y)``."""
+
+    def __init__(self, points, weights, q, kappa, leaf_size=64, nca_tol=1e-8, **opts):
+        o = default_options()
+        for k, v in opts.items():
+            setattr(o, k, v)
+        self.h = dafmm_create_ex(points, weights, q, kappa, leaf_size, nca_tol, o)
+        self.n = int(np.asarray(weights).size)
+
+    def set_stream(self, stream):
+        dafmm_set_stream(self.h, stream)
+
+    def matvec(self, x, y, mask=3):
+        if mask == 3:
+            dafmm_matvec(self.h, x, y)
+        else:
+            dafmm_matvec_parts(self.h, x, y, mask)
+        return y
+
+    def matvec_host(self, x_host, y_host):
+        dafmm_matvec_host(self.h, x_host, y_host)
+        return y_host
+
+    def gmres(self, f, psi, tol, maxit, restart=50, history=None):
+        return ls_gmres_solve(self.h, f, psi, tol, maxit, restart, history)
+
+    def stats(self):
+        return dafmm_stats(self.h)
+
+    def export_plan(self, path):
+        dafmm_export_plan(self.h, path)
+
+    def close(self):
+        if self.h:
+            dafmm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

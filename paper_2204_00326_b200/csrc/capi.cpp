@@ -1,0 +1,210 @@
+// C-ABI of include/dafmm.h: argument checking, error plumbing, handle lifetime.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "dafmm.h"
+#include "device.h"
+#include "plan.h"
+
+struct dafmm_plan {
+  dafmm::Plan plan;
+  dafmm::DevPlan dev;
+  int64_t operator_bytes = 0;
+  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
+extern "C" {
+
+void dafmm_default_options(dafmm_options* opt) {
+  if (!opt) return;
+  dafmm::Options o;
+  opt->T = o.T;
+  opt->self_term = o.self_term;
+  opt->kernel_mode = o.kernel_mode;
+  opt->max_level = o.max_level;
+  opt->num_threads = o.num_threads;
+  opt->host_only = o.host_only;
+}
+
+int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
+                    int leaf_size, double nca_tol, const dafmm_options* opt, dafmm_handle* out) {
+  if (!out) return fail(DAFMM_EINVAL, "out is null");
+  *out = nullptr;
+  dafmm::Options o;
+  if (opt) {
+    o.T = opt->T;
+    o.self_term = opt->self_term;
+    o.kernel_mode = opt->kernel_mode;
+    o.max_level = opt->max_level;
+    o.num_threads = opt->num_threads;
+    o.host_only = opt->host_only;
+  }
+  std::unique_ptr<dafmm_plan> h;
+  try {
+    h.reset(new dafmm_plan());
+  } catch (const std::bad_alloc&) {
+    return fail(DAFMM_ENOMEM, "host allocation failed");
+  }
+  std::string err;
+  int rc;
+  try {
+    rc = dafmm::build_plan(h->plan, points, weights, q, n, kappa, leaf_size, nca_tol, o, err);
+    if (rc != DAFMM_OK) return fail(rc, err);
+    double t0 = now_s();
+    dafmm::Packed pk;
+    rc = dafmm::pack_plan(h->plan, pk, err);
+    if (rc != DAFMM_OK) return fail(rc, err);
+    double t1 = now_s();
+    h->plan.t_ops = t1 - t0;
+    if (!o.host_only) {
+      rc = dafmm::upload_plan(pk, h->plan, h->dev, err);
+      if (rc != DAFMM_OK) {
+        dafmm::free_plan(h->dev);
+        return fail(rc, err);
+      }
+      h->plan.t_upload = now_s() - t1;
+    }
+    h->operator_bytes = (int64_t)pk.ops.size() * 16;
+    h->p2p_pairs = pk.p2p_pairs;
+    h->m2l_entries = pk.m2l_entries;
+    h->m2l_pairs = pk.m2l_pairs;
+  } catch (const std::bad_alloc&) {
+    dafmm::free_plan(h->dev);
+    return fail(DAFMM_ENOMEM, "host allocation failed during setup");
+  }
+  *out = h.release();
+  g_last_error.clear();
+  return DAFMM_OK;
+}
+
+int dafmm_create(const double* points, const double* weights, const double* q, int64_t n, double kappa, int leaf_size,
+                 double nca_tol, dafmm_handle* out) {
+  return dafmm_create_ex(points, weights, q, n, kappa, leaf_size, nca_tol, nullptr, out);
+}
+
+int dafmm_matvec_parts(dafmm_handle h, const void* x, void* y, unsigned mask) {
+  if (!h || !x || !y) return fail(DAFMM_EINVAL, "null handle or vector");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  if (x == y) return fail(DAFMM_EINVAL, "x and y must not alias");
+  if ((mask & 3u) == 0 || (mask & ~3u)) return fail(DAFMM_EINVAL, "mask must be a non-empty subset of {1, 2}");
+  std::string err;
+  int rc = dafmm::run_matvec(h->dev, (const double2*)x, (double2*)y, mask, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
+
+int dafmm_matvec(dafmm_handle h, const void* x, void* y) { return dafmm_matvec_parts(h, x, y, 3u); }
+
+int dafmm_matvec_host(dafmm_handle h, const void* x_host, void* y_host) {
+  if (!h || !x_host || !y_host) return fail(DAFMM_EINVAL, "null handle or vector");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  size_t bytes = sizeof(double2) * (size_t)h->dev.n;
+  double2* xd = h->dev.host_stage;
+  double2* yd = h->dev.host_stage + h->dev.n;
+  cudaStream_t s = h->dev.stream;
+  cudaError_t e = cudaMemcpyAsync(xd, x_host, bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(DAFMM_ECUDA, std::string("H2D: ") + cudaGetErrorString(e));
+  std::string err;
+  int rc = dafmm::run_matvec(h->dev, xd, yd, 3u, err);
+  if (rc != DAFMM_OK) return fail(rc, err);
+  e = cudaMemcpyAsync(y_host, yd, bytes, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(DAFMM_ECUDA, std::string("D2H: ") + cudaGetErrorString(e));
+  return DAFMM_OK;
+}
+
+int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int maxit, int restart, int* iters_out,
+                   double* relres_out, double* history) {
+  if (!h || !f || !psi || !iters_out || !relres_out) return fail(DAFMM_EINVAL, "null argument");
+  if (f == psi) return fail(DAFMM_EINVAL, "f and psi must not alias");
+  if (!(tol > 0.0) || maxit < 1) return fail(DAFMM_EINVAL, "tol must be > 0 and maxit >= 1");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  std::string err;
+  int rc = dafmm::run_gmres(h->dev, (const double2*)f, (double2*)psi, tol, maxit, restart, iters_out, relres_out,
+                            history, err);
+  if (rc < 0) return fail(rc, err);
+  return rc;
+}
+
+int dafmm_set_stream(dafmm_handle h, void* stream) {
+  if (!h) return fail(DAFMM_EINVAL, "null handle");
+  h->dev.stream = (cudaStream_t)stream;
+  return DAFMM_OK;
+}
+
+int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
+  if (!h || !out) return fail(DAFMM_EINVAL, "null argument");
+  std::memset(out, 0, sizeof(*out));
+  const dafmm::Plan& P = h->plan;
+  out->n = P.n;
+  out->levels = P.L;
+  int nodes = 0, maxr = 0;
+  double rin = 0, rout = 0;
+  int leafnodes = 0;
+  for (int l = 1; l <= P.L; ++l) {
+    nodes += (int)P.levels[l].nodes.size();
+    for (auto& np : P.piv[l]) {
+      maxr = std::max(maxr, (int)std::max(np.ti.size(), np.so.size()));
+      if (l == P.L) {
+        rin += (double)np.ti.size();
+        rout += (double)np.so.size();
+        ++leafnodes;
+      }
+    }
+  }
+  out->n_nodes = nodes;
+  out->max_rank = maxr;
+  out->mean_rank_leaf_in = leafnodes ? rin / leafnodes : 0.0;
+  out->mean_rank_leaf_out = leafnodes ? rout / leafnodes : 0.0;
+  out->p2p_pairs = h->p2p_pairs;
+  out->m2l_entries = h->m2l_entries;
+  out->m2l_pairs = h->m2l_pairs;
+  out->operator_bytes = h->operator_bytes;
+  out->device_bytes = (int64_t)h->dev.device_bytes;
+  out->setup_tree_s = P.t_tree;
+  out->setup_lists_s = P.t_lists;
+  out->setup_nca_s = P.t_nca;
+  out->setup_ops_s = P.t_ops;
+  out->setup_pack_s = P.t_pack;
+  out->setup_upload_s = P.t_upload;
+  out->aca_entries = P.aca_entries;
+  return DAFMM_OK;
+}
+
+int dafmm_export_plan(dafmm_handle h, const char* path) {
+  if (!h || !path) return fail(DAFMM_EINVAL, "null argument");
+  std::string err;
+  int rc = dafmm::export_plan(h->plan, path, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
+
+void dafmm_destroy(dafmm_handle h) {
+  if (!h) return;
+  if (!h->plan.opt.host_only) {
+    if (h->dev.stream) cudaStreamSynchronize(h->dev.stream);
+    else cudaDeviceSynchronize();
+  }
+  dafmm::free_plan(h->dev);
+  delete h;
+}
+
+const char* dafmm_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

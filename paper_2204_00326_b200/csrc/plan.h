@@ -1,0 +1,116 @@
+// Host-side plan: tree, lists, NCA pivots and operators of one dafmm handle, plus the
+// packed flat arrays that are uploaded once to HBM.
+#pragma once
+#include <array>
+#include <complex>
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.h"
+#include "hankel.cuh"
+
+namespace dafmm {
+
+using zd = std::complex<double>;
+
+struct Options {
+  double T = 16.0;         // regime threshold (reading R3)
+  int self_term = 1;       // 0 zero (point kernel, E1), 1 disk (reading D1)
+  int kernel_mode = 0;     // 0 Lippmann-Schwinger y = x + k^2 q (K x); 1 potential y = K x
+  int max_level = 16;
+  int num_threads = 0;     // host setup threads (0: OpenMP default)
+  int host_only = 0;       // skip the device upload
+};
+
+struct Box {
+  int64_t ix, iy;
+  int32_t begin, end;  // tree-order point range
+};
+
+struct Level {
+  int level = 0;
+  double b = 0, kb = 0;
+  bool hfr = false;
+  int ncones = 1;
+  std::vector<Box> boxes;                      // non-empty boxes in Morton order
+  std::unordered_map<uint64_t, int> index;     // packed (ix, iy) -> box
+  std::vector<std::vector<int>> N, IL;         // per box, box indices at this level
+  // ILdir[box] = sorted list of (cone, src box, src cone)
+  std::vector<std::vector<std::array<int, 3>>> ILdir;
+  // nodes: LFR -> one per active box (cone = -1); HFR -> one per active (box, cone)
+  std::vector<std::pair<int, int>> nodes;
+  std::vector<int> node_of;                    // box * ncones + cone (cone = 0 for LFR) -> node or -1
+  int node_id(int box, int cone) const { return node_of[(size_t)box * ncones + (hfr ? cone : 0)]; }
+};
+
+struct NodePivots {
+  std::vector<int32_t> ti, si, to, so;  // original point indices, in ACA selection order
+};
+
+struct Plan {
+  Options opt;
+  int64_t n = 0;
+  double kappa = 0, nca_tol = 0;
+  double W = 0, x0 = 0, y0 = 0;
+  int L = 0;
+  // input copies (original order)
+  std::vector<double> pts, w, q;
+  std::vector<zd> D;                 // self terms D_i (original order)
+  std::vector<int32_t> perm;         // tree index -> original index
+  std::vector<Level> levels;
+  std::vector<std::vector<NodePivots>> piv;  // [level][node]
+  // statistics
+  double t_tree = 0, t_lists = 0, t_nca = 0, t_ops = 0, t_pack = 0, t_upload = 0;
+  int64_t aca_entries = 0;
+};
+
+// Packed device-layout arrays (host copies before upload).
+struct Packed {
+  // per tree point
+  std::vector<double> pts_t;        // 2 per point
+  std::vector<double> w_t, qk2_t;   // weights, kappa^2 q
+  std::vector<cplx> D_t;            // self term
+  std::vector<int32_t> perm;
+  // expansion buffers
+  int64_t n_mult = 0, n_loc = 0;
+  std::vector<double> so_xy, ti_xy;  // 2 per multipole / local slot
+  std::vector<cplx> ops;             // all operator blocks, column-major
+  // generic translation batches: item -> [term_ptr[i], term_ptr[i+1]) terms
+  struct Batch {
+    std::vector<int64_t> dst_off;     // per item
+    std::vector<int32_t> dst_rows;    // per item
+    std::vector<int32_t> term_ptr;    // items + 1
+    std::vector<int64_t> mat_off;     // per term (into ops)
+    std::vector<int64_t> src_off;     // per term
+    std::vector<int32_t> src_cols;    // per term
+  };
+  Batch p2m;                         // leaf: dst multipole, src tree points (v), 1 term
+  std::vector<Batch> m2m;            // per parent level, processed from fine to coarse
+  std::vector<Batch> l2l;            // per parent level, processed from coarse to fine
+  // M2L: target nodes with source node CSR
+  std::vector<int64_t> m2l_loc_off;  // per target
+  std::vector<int32_t> m2l_rows;     // r_i per target
+  std::vector<int32_t> m2l_src_ptr;  // targets + 1
+  std::vector<int64_t> m2l_src_off;  // per source entry: multipole offset
+  std::vector<int32_t> m2l_src_cnt;  // per source entry: r_o
+  // leaves: near field + L2P + combine
+  std::vector<int32_t> leaf_begin, leaf_end;  // tree ranges
+  std::vector<int32_t> near_ptr;              // leaves + 1
+  std::vector<int32_t> near_begin, near_end;  // per near entry: tree range of the source leaf
+  std::vector<int64_t> leaf_loc_off;          // -1: no far field
+  std::vector<int32_t> leaf_rank;             // r_i
+  std::vector<int64_t> leaf_U_off;
+  int max_leaf = 0;
+  // statistics
+  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;
+};
+
+// setup.cpp
+int build_plan(Plan& plan, const double* points, const double* weights, const double* q, int64_t n,
+               double kappa, int leaf_size, double nca_tol, const Options& opt, std::string& err);
+int pack_plan(const Plan& plan, Packed& pk, std::string& err);
+int export_plan(const Plan& plan, const std::string& dir, std::string& err);
+
+}  // namespace dafmm

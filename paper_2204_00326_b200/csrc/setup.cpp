@@ -1,0 +1,915 @@
+// Host setup of the DAFMM plan: quadtree, regimes, cones, neighbour and
+// interaction lists, nested cross approximation pivots and the
+// translation operators in the form the device passes consume.
+//
+// Product code: shares nothing with oracle/.  Readings of silent passages are the
+// R-numbers of DESIGN.md.  Everything here runs once per handle and is timed separately
+// from the matvec (dafmm_stats).
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <sys/stat.h>
+
+#include "dafmm.h"
+#include "plan.h"
+
+namespace dafmm {
+
+namespace {
+
+constexpr double kPhi0 = kPi / 4096.0;  // R5: cone boundaries at odd multiples of pi/4096
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+uint64_t pack_key(int64_t ix, int64_t iy) { return ((uint64_t)ix << 32) | (uint64_t)(uint32_t)iy; }
+
+uint64_t spread_bits(uint64_t v) {
+  uint64_t r = 0;
+  for (int b = 0; b < 32; ++b) r |= ((v >> b) & 1ull) << (2 * b);
+  return r;
+}
+uint64_t morton(int64_t ix, int64_t iy) { return spread_bits((uint64_t)ix) | (spread_bits((uint64_t)iy) << 1); }
+
+// ---- self term (reading D1): D = (i pi R / (2 kappa)) H1(kappa R) - 1/kappa^2, R = sqrt(w/pi) ----
+// H1^(1)(z) for small z from the power series of J1 and Y1 (Bessel's series; z <= 8 here).
+zd hankel1_small(double z) {
+  const double g = 0.57721566490153286061;
+  double h = 0.25 * z * z;
+  double c = 1.0;          // (-h)^k / (k! (k+1)!)
+  double sj = 0.0, sy = 0.0;
+  double psi_k = -g, psi_k1 = 1.0 - g;  // psi(k+1), psi(k+2)
+  for (int k = 0; k < 300; ++k) {
+    if (k > 0) {
+      c *= -h / (double(k) * double(k + 1));
+      psi_k += 1.0 / k;
+      psi_k1 += 1.0 / (k + 1);
+    }
+    sj += c;
+    sy += (psi_k + psi_k1) * c;
+    if (k > h && std::fabs(c) < 1e-24) break;
+  }
+  double j1 = 0.5 * z * sj;
+  double y1 = -2.0 / (kPi * z) + (2.0 / kPi) * std::log(0.5 * z) * j1 - (0.5 * z / kPi) * sy;
+  return zd(j1, y1);
+}
+
+zd self_term_disk(double kappa, double w) {
+  double R = std::sqrt(w / kPi);
+  return zd(0.0, kPi * R / (2.0 * kappa)) * hankel1_small(kappa * R) - 1.0 / (kappa * kappa);
+}
+
+// ---- complex LU with partial pivoting (reading R12: solves, never explicit inverses) ----
+struct LU {
+  int r = 0;
+  std::vector<zd> a;  // row-major, factors in place
+  std::vector<int> p;
+  bool factor(const std::vector<zd>& m, int n) {
+    r = n;
+    a = m;
+    p.resize(n);
+    for (int k = 0; k < n; ++k) {
+      int piv = k;
+      double best = std::abs(a[(size_t)k * n + k]);
+      for (int i = k + 1; i < n; ++i) {
+        double v = std::abs(a[(size_t)i * n + k]);
+        if (v > best) { best = v; piv = i; }
+      }
+      if (!(best > 0.0)) return false;
+      p[k] = piv;
+      if (piv != k)
+        for (int j = 0; j < n; ++j) std::swap(a[(size_t)k * n + j], a[(size_t)piv * n + j]);
+      zd inv = 1.0 / a[(size_t)k * n + k];
+      for (int i = k + 1; i < n; ++i) {
+        zd f = a[(size_t)i * n + k] * inv;
+        a[(size_t)i * n + k] = f;
+        if (f != 0.0)
+          for (int j = k + 1; j < n; ++j) a[(size_t)i * n + j] -= f * a[(size_t)k * n + j];
+      }
+    }
+    return true;
+  }
+  // Solve A x = b in place (b length r).
+  void solve(zd* b) const {
+    int n = r;
+    for (int k = 0; k < n; ++k)
+      if (p[k] != k) std::swap(b[k], b[p[k]]);
+    for (int i = 0; i < n; ++i) {
+      zd s = b[i];
+      for (int j = 0; j < i; ++j) s -= a[(size_t)i * n + j] * b[j];
+      b[i] = s;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      zd s = b[i];
+      for (int j = i + 1; j < n; ++j) s -= a[(size_t)i * n + j] * b[j];
+      b[i] = s / a[(size_t)i * n + i];
+    }
+  }
+};
+
+struct Ctx {
+  const Plan& p;
+  KernelConsts kc;
+  explicit Ctx(const Plan& plan) : p(plan), kc(make_kernel_consts(plan.kappa)) {}
+  // H0^(1)(kappa |x_i - x_j|), i != j (original indices)
+  zd H(int32_t i, int32_t j) const {
+    double dx = p.pts[2 * (size_t)i] - p.pts[2 * (size_t)j];
+    double dy = p.pts[2 * (size_t)i + 1] - p.pts[2 * (size_t)j + 1];
+    cplx h = h0(dx * dx + dy * dy, kc);
+    return zd(h.re, h.im);
+  }
+  // K_ij = G(x_i, x_j) w_j: the discretised volume potential compressed by the NCA (reading R9)
+  zd K(int32_t i, int32_t j) const { return zd(0.0, 0.25) * H(i, j) * p.w[j]; }
+};
+
+// ---- partially pivoted ACA on K[rows, cols] (stopping rule of Rjasanow 2002
+// cited at P:816; tie-breaking and termination of reading R10) ----
+void aca(const Ctx& cx, const std::vector<int32_t>& rows, const std::vector<int32_t>& cols, double eps,
+         std::vector<int32_t>& prow, std::vector<int32_t>& pcol, int64_t& entries) {
+  prow.clear();
+  pcol.clear();
+  const int m = (int)rows.size(), n = (int)cols.size();
+  if (m == 0 || n == 0) return;
+  const int cap = std::min(std::min(m, n), 200);
+  std::vector<zd> U, V;  // k x m, k x n
+  U.reserve((size_t)cap * m);
+  V.reserve((size_t)cap * n);
+  std::vector<char> used_r(m, 0), used_c(n, 0);
+  std::vector<zd> r(n), u(m);
+  double norm2 = 0.0;
+  int i = 0, k = 0;
+  while (k < cap) {
+    for (int j = 0; j < n; ++j) r[j] = cx.K(rows[i], cols[j]);
+    entries += n;
+    for (int l = 0; l < k; ++l) {
+      zd ul = U[(size_t)l * m + i];
+      const zd* vl = &V[(size_t)l * n];
+      for (int j = 0; j < n; ++j) r[j] -= ul * vl[j];
+    }
+    used_r[i] = 1;
+    int jm = -1;
+    double best = -1.0;
+    for (int j = 0; j < n; ++j) {
+      if (used_c[j]) continue;
+      double a = std::abs(r[j]);
+      if (a > best) { best = a; jm = j; }
+    }
+    if (!(best > 0.0)) {
+      int nxt = -1;
+      for (int t = 0; t < m; ++t)
+        if (!used_r[t]) { nxt = t; break; }
+      if (nxt < 0) break;
+      i = nxt;
+      continue;
+    }
+    zd inv = 1.0 / r[jm];
+    for (int j = 0; j < n; ++j) r[j] *= inv;  // v
+    for (int t = 0; t < m; ++t) u[t] = cx.K(rows[t], cols[jm]);
+    entries += m;
+    for (int l = 0; l < k; ++l) {
+      zd vl = V[(size_t)l * n + jm];
+      const zd* ul = &U[(size_t)l * m];
+      for (int t = 0; t < m; ++t) u[t] -= vl * ul[t];
+    }
+    double cross = 0.0;
+    for (int l = 0; l < k; ++l) {
+      zd du = 0.0, dv = 0.0;
+      const zd* ul = &U[(size_t)l * m];
+      const zd* vl = &V[(size_t)l * n];
+      for (int t = 0; t < m; ++t) du += std::conj(ul[t]) * u[t];
+      for (int j = 0; j < n; ++j) dv += std::conj(vl[j]) * r[j];
+      cross += 2.0 * std::real(du * dv);
+    }
+    double nu2 = 0.0, nv2 = 0.0;
+    for (int t = 0; t < m; ++t) nu2 += std::norm(u[t]);
+    for (int j = 0; j < n; ++j) nv2 += std::norm(r[j]);
+    norm2 += cross + nu2 * nv2;
+    if (k > 0 && std::sqrt(nu2 * nv2) <= eps * std::sqrt(norm2)) break;
+    U.insert(U.end(), u.begin(), u.end());
+    V.insert(V.end(), r.begin(), r.end());
+    prow.push_back(rows[i]);
+    pcol.push_back(cols[jm]);
+    used_c[jm] = 1;
+    ++k;
+    bool all = true;
+    int im = -1;
+    double bu = -1.0;
+    for (int t = 0; t < m; ++t) {
+      if (used_r[t]) continue;
+      all = false;
+      double a = std::abs(u[t]);
+      if (a > bu) { bu = a; im = t; }
+    }
+    if (all) break;
+    i = im;
+  }
+}
+
+int cone_of(int n, int64_t dx, int64_t dy, bool& ok) {
+  double a = std::atan2((double)dy, (double)dx) - kPhi0;
+  if (a < 0.0) a += 2.0 * kPi;
+  double t = a * n / (2.0 * kPi);
+  double fl = std::floor(t);
+  double frac = t - fl;
+  ok = std::min(frac, 1.0 - frac) > 1e-9;
+  return ((int)fl) % n;
+}
+
+void sorted_union(std::vector<int32_t>& v) {
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+}
+
+}  // namespace
+
+// ============================================================================================
+int build_plan(Plan& P, const double* points, const double* weights, const double* q, int64_t n, double kappa,
+               int leaf_size, double nca_tol, const Options& opt, std::string& err) {
+  double t0 = now_s();
+  if (!points || !weights || !q) { err = "null input pointer"; return DAFMM_EINVAL; }
+  if (n <= 0 || n > (int64_t)1 << 30) { err = "n must be in [1, 2^30]"; return DAFMM_EINVAL; }
+  if (!(kappa > 0.0) || !std::isfinite(kappa)) { err = "kappa must be positive and finite"; return DAFMM_EINVAL; }
+  if (!(nca_tol > 0.0 && nca_tol < 1.0)) { err = "nca_tol must be in (0, 1)"; return DAFMM_EINVAL; }
+  if (leaf_size < 1) { err = "leaf_size must be >= 1"; return DAFMM_EINVAL; }
+  if (!(opt.T > 0.0) || opt.self_term < 0 || opt.self_term > 1 || opt.kernel_mode < 0 || opt.kernel_mode > 1 ||
+      opt.max_level < 0 || opt.max_level > 24) {
+    err = "invalid options";
+    return DAFMM_EINVAL;
+  }
+  if (opt.num_threads > 0) omp_set_num_threads(opt.num_threads);
+  P.opt = opt;
+  P.n = n;
+  P.kappa = kappa;
+  P.nca_tol = nca_tol;
+  P.pts.assign(points, points + 2 * n);
+  P.w.assign(weights, weights + n);
+  P.q.assign(q, q + n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(P.pts[2 * i]) || !std::isfinite(P.pts[2 * i + 1]) || !std::isfinite(P.q[i]) ||
+        !std::isfinite(P.w[i])) {
+      err = "non-finite input at index " + std::to_string(i);
+      return DAFMM_EINVAL;
+    }
+    if (!(P.w[i] > 0.0)) { err = "weights must be > 0"; return DAFMM_EINVAL; }
+    if (opt.self_term == 1 && kappa * std::sqrt(P.w[i] / kPi) > 8.0) {
+      err = "self-term disk too large (kappa sqrt(w/pi) > 8)";
+      return DAFMM_EINVAL;
+    }
+  }
+  // ---- root square of the quadrature cells (reading R2) ----
+  double lox = INFINITY, hix = -INFINITY, loy = INFINITY, hiy = -INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    double h = 0.5 * std::sqrt(P.w[i]);
+    lox = std::min(lox, P.pts[2 * i] - h);
+    hix = std::max(hix, P.pts[2 * i] + h);
+    loy = std::min(loy, P.pts[2 * i + 1] - h);
+    hiy = std::max(hiy, P.pts[2 * i + 1] + h);
+  }
+  P.W = std::max(hix - lox, hiy - loy);
+  double cxr = 0.5 * (lox + hix), cyr = 0.5 * (loy + hiy);
+  P.x0 = cxr - 0.5 * P.W;
+  P.y0 = cyr - 0.5 * P.W;
+  auto width = [&](int l) { return std::ldexp(P.W, -l); };
+  // ---- leaf level: leaves LFR (rule 3) and <= leaf_size points ----
+  int L = 0;
+  while (kappa * width(L) * (kappa * width(L)) > opt.T) ++L;
+  std::vector<int64_t> ix(n), iy(n);
+  auto lattice = [&](int l) {
+    double m = std::ldexp(1.0, l);
+    int64_t mx = ((int64_t)1 << l) - 1;
+    for (int64_t i = 0; i < n; ++i) {
+      int64_t a = (int64_t)std::floor(((P.pts[2 * i] - P.x0) / P.W) * m);
+      int64_t b = (int64_t)std::floor(((P.pts[2 * i + 1] - P.y0) / P.W) * m);
+      ix[i] = std::min<int64_t>(std::max<int64_t>(a, 0), mx);
+      iy[i] = std::min<int64_t>(std::max<int64_t>(b, 0), mx);
+    }
+  };
+  std::vector<uint64_t> keys(n);
+  while (true) {
+    if (L > opt.max_level) {
+      err = "leaf_size not reachable within max_level (adaptive trees are not supported yet)";
+      return DAFMM_EINVAL;
+    }
+    lattice(L);
+    for (int64_t i = 0; i < n; ++i) keys[i] = pack_key(ix[i], iy[i]);
+    std::vector<uint64_t> s = keys;
+    std::sort(s.begin(), s.end());
+    int64_t run = 1, mx = 1;
+    for (int64_t i = 1; i < n; ++i) {
+      run = (s[i] == s[i - 1]) ? run + 1 : 1;
+      mx = std::max(mx, run);
+    }
+    if (mx <= leaf_size) break;
+    ++L;
+  }
+  P.L = L;
+  // ---- tree order: Morton code of the leaf, then original index ----
+  std::vector<uint64_t> mcode(n);
+  for (int64_t i = 0; i < n; ++i) mcode[i] = morton(ix[i], iy[i]);
+  P.perm.resize(n);
+  std::iota(P.perm.begin(), P.perm.end(), 0);
+  std::sort(P.perm.begin(), P.perm.end(), [&](int32_t a, int32_t b) {
+    return mcode[a] != mcode[b] ? mcode[a] < mcode[b] : a < b;
+  });
+  // duplicate points (G is singular off the diagonal): compare within each leaf
+  {
+    int64_t s = 0;
+    while (s < n) {
+      int64_t e = s + 1;
+      while (e < n && mcode[P.perm[e]] == mcode[P.perm[s]]) ++e;
+      std::vector<std::pair<double, double>> xy;
+      for (int64_t t = s; t < e; ++t) xy.emplace_back(P.pts[2 * (size_t)P.perm[t]], P.pts[2 * (size_t)P.perm[t] + 1]);
+      std::sort(xy.begin(), xy.end());
+      for (size_t t = 1; t < xy.size(); ++t)
+        if (xy[t] == xy[t - 1]) { err = "duplicate points"; return DAFMM_EINVAL; }
+      s = e;
+    }
+  }
+  P.levels.assign(L + 1, Level());
+  for (int l = 0; l <= L; ++l) {
+    Level& lv = P.levels[l];
+    lv.level = l;
+    lv.b = width(l);
+    lv.kb = kappa * lv.b;
+    lv.hfr = lv.kb * lv.kb > opt.T;
+    if (lv.hfr) {
+      double x = kPi * lv.kb / std::sqrt(2.0);
+      int nc = 1;
+      while (nc < x) nc *= 2;
+      lv.ncones = nc;
+    }
+    int sh = L - l;
+    int64_t t = 0;
+    while (t < n) {
+      int32_t o = P.perm[t];
+      int64_t bx = ix[o] >> sh, by = iy[o] >> sh;
+      int64_t e = t + 1;
+      while (e < n && (ix[P.perm[e]] >> sh) == bx && (iy[P.perm[e]] >> sh) == by) ++e;
+      lv.index[pack_key(bx, by)] = (int)lv.boxes.size();
+      lv.boxes.push_back({bx, by, (int32_t)t, (int32_t)e});
+      t = e;
+    }
+  }
+  P.D.assign(n, zd(0.0, 0.0));
+  if (opt.self_term == 1)
+    for (int64_t i = 0; i < n; ++i) P.D[i] = self_term_disk(kappa, P.w[i]);
+  double t1 = now_s();
+  P.t_tree = t1 - t0;
+
+  // ---- lists ----
+  for (int l = 0; l <= L; ++l) {
+    Level& lv = P.levels[l];
+    int nb = (int)lv.boxes.size();
+    lv.N.assign(nb, {});
+    int64_t reach = lv.hfr ? (int64_t)std::ceil(lv.kb / 2.0) + 1 : 1;
+    const double kb2 = lv.kb * lv.kb;
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int b = 0; b < nb; ++b) {
+      const Box& B = lv.boxes[b];
+      for (int64_t dx = -reach; dx <= reach; ++dx)
+        for (int64_t dy = -reach; dy <= reach; ++dy) {
+          auto it = lv.index.find(pack_key(B.ix + dx, B.iy + dy));
+          if (B.ix + dx < 0 || B.iy + dy < 0 || it == lv.index.end()) continue;
+          int64_t d2 = dx * dx + dy * dy;
+          bool nbr = lv.hfr ? (4.0 * (double)d2 < kb2) : (d2 < 4);  // P:286 / P:302 (R4)
+          if (nbr) lv.N[b].push_back(it->second);
+        }
+      std::sort(lv.N[b].begin(), lv.N[b].end());
+    }
+  }
+  bool cone_ok = true;
+  for (int l = 1; l <= L; ++l) {
+    Level& lv = P.levels[l];
+    const Level& pv = P.levels[l - 1];
+    int nb = (int)lv.boxes.size();
+    lv.IL.assign(nb, {});
+    lv.ILdir.assign(nb, {});
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int b = 0; b < nb; ++b) {
+      const Box& B = lv.boxes[b];
+      int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+      std::vector<int> il;
+      for (int pn : pv.N[pb]) {
+        const Box& PB = pv.boxes[pn];
+        for (int c = 0; c < 4; ++c) {
+          auto it = lv.index.find(pack_key(2 * PB.ix + (c & 1), 2 * PB.iy + (c >> 1)));
+          if (it == lv.index.end()) continue;
+          if (!std::binary_search(lv.N[b].begin(), lv.N[b].end(), it->second)) il.push_back(it->second);
+        }
+      }
+      std::sort(il.begin(), il.end());
+      lv.IL[b] = il;
+      if (lv.hfr) {
+        for (int a : il) {
+          bool ok1, ok2;
+          int k = cone_of(lv.ncones, lv.boxes[a].ix - B.ix, lv.boxes[a].iy - B.iy, ok1);
+          int kp = cone_of(lv.ncones, B.ix - lv.boxes[a].ix, B.iy - lv.boxes[a].iy, ok2);
+          if (!ok1 || !ok2 || kp != (k + lv.ncones / 2) % lv.ncones) {
+#pragma omp atomic write
+            cone_ok = false;
+          }
+          lv.ILdir[b].push_back({k, a, kp});
+        }
+        std::sort(lv.ILdir[b].begin(), lv.ILdir[b].end());
+      }
+    }
+  }
+  if (!cone_ok) { err = "box centre on a cone boundary"; return DAFMM_ESETUP; }
+  // ---- active nodes, top-down ----
+  for (int l = 0; l <= L; ++l) {
+    Level& lv = P.levels[l];
+    lv.node_of.assign(lv.boxes.size() * (size_t)lv.ncones, -1);
+    if (l == 0) continue;
+    const Level& pv = P.levels[l - 1];
+    std::vector<char> parent_any(pv.boxes.size(), 0);
+    for (auto& nd : pv.nodes) parent_any[nd.first] = 1;
+    for (int b = 0; b < (int)lv.boxes.size(); ++b) {
+      const Box& B = lv.boxes[b];
+      int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+      if (lv.hfr) {
+        std::vector<char> has(lv.ncones, 0);
+        for (auto& e : lv.ILdir[b]) has[e[0]] = 1;
+        for (int k = 0; k < lv.ncones; ++k) {
+          bool need = has[k];
+          if (l > 1 && pv.hfr)
+            need = need || pv.node_id(pb, 2 * k) >= 0 || pv.node_id(pb, 2 * k + 1) >= 0;
+          if (need) {
+            lv.node_of[(size_t)b * lv.ncones + k] = (int)lv.nodes.size();
+            lv.nodes.push_back({b, k});
+          }
+        }
+      } else {
+        bool need = !lv.IL[b].empty() || (l > 1 && parent_any[pb]);
+        if (need) {
+          lv.node_of[b] = (int)lv.nodes.size();
+          lv.nodes.push_back({b, -1});
+        }
+      }
+    }
+  }
+  double t2 = now_s();
+  P.t_lists = t2 - t1;
+
+  // ---- NCA pivots, bottom-up ----
+  Ctx cx(P);
+  P.piv.assign(L + 1, {});
+  int64_t total_entries = 0;
+  for (int l = L; l >= 1; --l) {
+    Level& lv = P.levels[l];
+    P.piv[l].assign(lv.nodes.size(), NodePivots());
+    const bool leaf = (l == L);
+    const Level* cv = leaf ? nullptr : &P.levels[l + 1];
+    const Level& pv = P.levels[l - 1];
+    // child node ids of (box, cone) at level l+1 (C(B) / C(B, k))
+    auto children = [&](const Level& at, int lvl, int box, int cone, std::vector<int>& out) {
+      out.clear();
+      const Level& ch = P.levels[lvl + 1];
+      const Box& B = at.boxes[box];
+      for (int c = 0; c < 4; ++c) {
+        auto it = ch.index.find(pack_key(2 * B.ix + (c & 1), 2 * B.iy + (c >> 1)));
+        if (it == ch.index.end()) continue;
+        int nd = ch.node_id(it->second, ch.hfr ? cone / 2 : 0);
+        if (nd >= 0) out.push_back(nd);
+      }
+    };
+    int64_t level_entries = 0;
+    int fail = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : level_entries)
+    for (int nd = 0; nd < (int)lv.nodes.size(); ++nd) {
+      int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
+      // far list: IL(B) / IL(B,k); R7 substitute for an active HFR node with empty IL(B,k)
+      std::vector<std::pair<int, int>> far;
+      if (!lv.hfr) {
+        for (int a : lv.IL[b]) far.push_back({a, -1});
+      } else {
+        for (auto& e : lv.ILdir[b])
+          if (e[0] == k) far.push_back({e[1], e[2]});
+        if (far.empty()) {
+          const Box& B = lv.boxes[b];
+          int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+          for (auto& e : pv.ILdir[pb]) {
+            if (e[0] != 2 * k && e[0] != 2 * k + 1) continue;
+            const Box& A = pv.boxes[e[1]];
+            for (int c = 0; c < 4; ++c) {
+              auto it = lv.index.find(pack_key(2 * A.ix + (c & 1), 2 * A.iy + (c >> 1)));
+              if (it != lv.index.end()) far.push_back({it->second, e[2] / 2});
+            }
+          }
+          std::sort(far.begin(), far.end());
+          far.erase(std::unique(far.begin(), far.end()), far.end());
+        }
+      }
+      std::vector<int32_t> ti, si, to, so;
+      if (leaf) {
+        const Box& B = lv.boxes[b];
+        for (int32_t t = B.begin; t < B.end; ++t) ti.push_back(P.perm[t]);
+        so = ti;
+        for (auto& f : far) {
+          const Box& A = lv.boxes[f.first];
+          for (int32_t t = A.begin; t < A.end; ++t) si.push_back(P.perm[t]);
+        }
+        sorted_union(ti);
+        sorted_union(so);
+        sorted_union(si);
+        to = si;
+      } else {
+        std::vector<int> kids;
+        children(lv, l, b, k, kids);
+        for (int c : kids) {
+          const NodePivots& pc = P.piv[l + 1][c];
+          ti.insert(ti.end(), pc.ti.begin(), pc.ti.end());
+          so.insert(so.end(), pc.so.begin(), pc.so.end());
+        }
+        for (auto& f : far) {
+          children(lv, l, f.first, f.second, kids);
+          for (int c : kids) {
+            const NodePivots& pc = P.piv[l + 1][c];
+            si.insert(si.end(), pc.so.begin(), pc.so.end());
+            to.insert(to.end(), pc.ti.begin(), pc.ti.end());
+          }
+        }
+        sorted_union(ti);
+        sorted_union(so);
+        sorted_union(si);
+        sorted_union(to);
+      }
+      (void)cv;
+      NodePivots& np = P.piv[l][nd];
+      int64_t ent = 0;
+      aca(cx, ti, si, nca_tol, np.ti, np.si, ent);
+      aca(cx, to, so, nca_tol, np.to, np.so, ent);
+      level_entries += ent;
+    }
+    (void)fail;
+    total_entries += level_entries;
+  }
+  P.aca_entries = total_entries;
+  double t3 = now_s();
+  P.t_nca = t3 - t2;
+  return DAFMM_OK;
+}
+
+// ============================================================================================
+// Packing: node offsets, pivot coordinates, operator blocks (P:427-562 in the G-only form of
+// DESIGN.md §Operators), and the per-pass work lists.
+int pack_plan(const Plan& P, Packed& pk, std::string& err) {
+  double t0 = now_s();
+  const int L = P.L;
+  const int64_t n = P.n;
+  Ctx cx(P);
+  pk.perm = P.perm;
+  pk.pts_t.resize(2 * n);
+  pk.w_t.resize(n);
+  pk.qk2_t.resize(n);
+  pk.D_t.resize(n);
+  for (int64_t t = 0; t < n; ++t) {
+    int32_t o = P.perm[t];
+    pk.pts_t[2 * t] = P.pts[2 * (size_t)o];
+    pk.pts_t[2 * t + 1] = P.pts[2 * (size_t)o + 1];
+    pk.w_t[t] = P.w[o];
+    pk.qk2_t[t] = P.kappa * P.kappa * P.q[o];
+    pk.D_t[t] = {P.D[o].real(), P.D[o].imag()};
+  }
+  // ---- node offsets ----
+  std::vector<std::vector<int64_t>> moff(L + 1), loff(L + 1);
+  int64_t nm = 0, nl = 0;
+  for (int l = 1; l <= L; ++l) {
+    size_t nn = P.levels[l].nodes.size();
+    moff[l].resize(nn);
+    loff[l].resize(nn);
+    for (size_t nd = 0; nd < nn; ++nd) {
+      moff[l][nd] = nm;
+      loff[l][nd] = nl;
+      nm += (int64_t)P.piv[l][nd].so.size();
+      nl += (int64_t)P.piv[l][nd].ti.size();
+    }
+  }
+  pk.n_mult = nm;
+  pk.n_loc = nl;
+  pk.so_xy.resize(2 * nm);
+  pk.ti_xy.resize(2 * nl);
+  for (int l = 1; l <= L; ++l)
+    for (size_t nd = 0; nd < P.levels[l].nodes.size(); ++nd) {
+      const NodePivots& np = P.piv[l][nd];
+      for (size_t k = 0; k < np.so.size(); ++k) {
+        pk.so_xy[2 * (moff[l][nd] + k)] = P.pts[2 * (size_t)np.so[k]];
+        pk.so_xy[2 * (moff[l][nd] + k) + 1] = P.pts[2 * (size_t)np.so[k] + 1];
+      }
+      for (size_t k = 0; k < np.ti.size(); ++k) {
+        pk.ti_xy[2 * (loff[l][nd] + k)] = P.pts[2 * (size_t)np.ti[k]];
+        pk.ti_xy[2 * (loff[l][nd] + k) + 1] = P.pts[2 * (size_t)np.ti[k] + 1];
+      }
+    }
+  // ---- operator block descriptors; blocks are filled in parallel afterwards ----
+  struct Job {
+    int kind;  // 0: V (P2M), 1: T (M2M), 2: C (L2L), 3: U (L2P)
+    int level, node, child;  // node at `level`, child node at level + 1
+    int64_t off;
+  };
+  std::vector<Job> jobs;
+  int64_t ops_len = 0;
+  auto add_job = [&](int kind, int l, int nd, int ch, int64_t len) {
+    jobs.push_back({kind, l, nd, ch, ops_len});
+    ops_len += len;
+    return jobs.back().off;
+  };
+  const Level& leaf = P.levels[L];
+  auto child_nodes = [&](int l, int nd, std::vector<int>& out) {
+    out.clear();
+    const Level& lv = P.levels[l];
+    const Level& ch = P.levels[l + 1];
+    const Box& B = lv.boxes[lv.nodes[nd].first];
+    int cone = lv.nodes[nd].second;
+    for (int c = 0; c < 4; ++c) {
+      auto it = ch.index.find(pack_key(2 * B.ix + (c & 1), 2 * B.iy + (c >> 1)));
+      if (it == ch.index.end()) continue;
+      int cn = ch.node_id(it->second, ch.hfr ? cone / 2 : 0);
+      if (cn >= 0) out.push_back(cn);
+    }
+  };
+  // P2M
+  for (size_t nd = 0; nd < leaf.nodes.size(); ++nd) {
+    const Box& B = leaf.boxes[leaf.nodes[nd].first];
+    int ro = (int)P.piv[L][nd].so.size();
+    int m = B.end - B.begin;
+    if (ro == 0) continue;
+    int64_t off = add_job(0, L, (int)nd, -1, (int64_t)ro * m);
+    pk.p2m.dst_off.push_back(moff[L][nd]);
+    pk.p2m.dst_rows.push_back(ro);
+    pk.p2m.term_ptr.push_back((int32_t)pk.p2m.mat_off.size());
+    pk.p2m.mat_off.push_back(off);
+    pk.p2m.src_off.push_back(B.begin);
+    pk.p2m.src_cols.push_back(m);
+  }
+  pk.p2m.term_ptr.push_back((int32_t)pk.p2m.mat_off.size());
+  // M2M, fine to coarse
+  std::vector<int> kids;
+  pk.m2m.clear();
+  for (int l = L - 1; l >= 1; --l) {
+    Packed::Batch bt;
+    const Level& lv = P.levels[l];
+    for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
+      int ro = (int)P.piv[l][nd].so.size();
+      if (ro == 0) continue;
+      child_nodes(l, (int)nd, kids);
+      bool any = false;
+      for (int c : kids) {
+        int rc = (int)P.piv[l + 1][c].so.size();
+        if (rc == 0) continue;
+        if (!any) {
+          bt.dst_off.push_back(moff[l][nd]);
+          bt.dst_rows.push_back(ro);
+          bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+          any = true;
+        }
+        bt.mat_off.push_back(add_job(1, l, (int)nd, c, (int64_t)ro * rc));
+        bt.src_off.push_back(moff[l + 1][c]);
+        bt.src_cols.push_back(rc);
+      }
+    }
+    bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+    pk.m2m.push_back(std::move(bt));
+  }
+  // L2L, coarse to fine: items are the child nodes, terms the parent nodes listing them
+  pk.l2l.clear();
+  for (int l = 1; l <= L - 1; ++l) {
+    const Level& lv = P.levels[l];
+    const Level& ch = P.levels[l + 1];
+    std::vector<std::vector<std::pair<int, int>>> incoming(ch.nodes.size());  // child -> (parent node)
+    for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
+      if (P.piv[l][nd].ti.empty()) continue;
+      child_nodes(l, (int)nd, kids);
+      for (int c : kids) incoming[c].push_back({(int)nd, c});
+    }
+    Packed::Batch bt;
+    for (size_t c = 0; c < ch.nodes.size(); ++c) {
+      int rc = (int)P.piv[l + 1][c].ti.size();
+      if (rc == 0 || incoming[c].empty()) continue;
+      bt.dst_off.push_back(loff[l + 1][c]);
+      bt.dst_rows.push_back(rc);
+      bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+      for (auto& pr : incoming[c]) {
+        int rp = (int)P.piv[l][pr.first].ti.size();
+        bt.mat_off.push_back(add_job(2, l, pr.first, (int)c, (int64_t)rc * rp));
+        bt.src_off.push_back(loff[l][pr.first]);
+        bt.src_cols.push_back(rp);
+      }
+    }
+    bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+    pk.l2l.push_back(std::move(bt));
+  }
+  // M2L targets (all levels, one launch)
+  pk.m2l_src_ptr.push_back(0);
+  for (int l = 1; l <= L; ++l) {
+    const Level& lv = P.levels[l];
+    for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
+      int ri = (int)P.piv[l][nd].ti.size();
+      if (ri == 0) continue;
+      int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
+      int cnt = 0;
+      auto add_src = [&](int sn) {
+        int ro = (int)P.piv[l][sn].so.size();
+        if (ro == 0) return;
+        pk.m2l_src_off.push_back(moff[l][sn]);
+        pk.m2l_src_cnt.push_back(ro);
+        pk.m2l_entries += (int64_t)ri * ro;
+        ++pk.m2l_pairs;
+        ++cnt;
+      };
+      if (lv.hfr) {
+        for (auto& e : lv.ILdir[b])
+          if (e[0] == k) add_src(lv.node_id(e[1], e[2]));
+      } else {
+        for (int a : lv.IL[b]) add_src(lv.node_id(a, 0));
+      }
+      if (cnt == 0) continue;
+      pk.m2l_loc_off.push_back(loff[l][nd]);
+      pk.m2l_rows.push_back(ri);
+      pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
+    }
+  }
+  // leaves: near field, L2P
+  pk.near_ptr.push_back(0);
+  pk.max_leaf = 0;
+  for (size_t b = 0; b < leaf.boxes.size(); ++b) {
+    const Box& B = leaf.boxes[b];
+    pk.leaf_begin.push_back(B.begin);
+    pk.leaf_end.push_back(B.end);
+    pk.max_leaf = std::max(pk.max_leaf, B.end - B.begin);
+    for (int a : leaf.N[b]) {
+      pk.near_begin.push_back(leaf.boxes[a].begin);
+      pk.near_end.push_back(leaf.boxes[a].end);
+      pk.p2p_pairs += (int64_t)(B.end - B.begin) * (leaf.boxes[a].end - leaf.boxes[a].begin);
+    }
+    pk.p2p_pairs -= (B.end - B.begin);
+    pk.near_ptr.push_back((int32_t)pk.near_begin.size());
+    int nd = leaf.node_of[b];
+    int ri = nd >= 0 ? (int)P.piv[L][nd].ti.size() : 0;
+    if (ri > 0) {
+      pk.leaf_loc_off.push_back(loff[L][nd]);
+      pk.leaf_rank.push_back(ri);
+      pk.leaf_U_off.push_back(add_job(3, L, nd, (int)b, (int64_t)(B.end - B.begin) * ri));
+    } else {
+      pk.leaf_loc_off.push_back(-1);
+      pk.leaf_rank.push_back(0);
+      pk.leaf_U_off.push_back(0);
+    }
+  }
+  // ---- operator blocks (column-major), in parallel ----
+  try {
+    pk.ops.assign((size_t)ops_len, cplx{0.0, 0.0});
+  } catch (...) {
+    err = "host allocation of operator blocks failed";
+    return DAFMM_ENOMEM;
+  }
+  int fail = 0;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (size_t jb = 0; jb < jobs.size(); ++jb) {
+    const Job& J = jobs[jb];
+    const NodePivots& np = P.piv[J.level][J.node];
+    cplx* out = pk.ops.data() + J.off;
+    if (J.kind == 0 || J.kind == 1) {
+      // V~ = H(to, so)^{-1} H(to, s) : rows = so, cols = s (leaf points or child's so)
+      int r = (int)np.so.size();
+      std::vector<int32_t> cols;
+      if (J.kind == 0) {
+        const Box& B = leaf.boxes[P.levels[L].nodes[J.node].first];
+        for (int32_t t = B.begin; t < B.end; ++t) cols.push_back(P.perm[t]);
+      } else {
+        cols = P.piv[J.level + 1][J.child].so;
+      }
+      std::vector<zd> M((size_t)r * r);
+      for (int a = 0; a < r; ++a)
+        for (int c = 0; c < r; ++c) M[(size_t)a * r + c] = cx.H(np.to[a], np.so[c]);
+      LU lu;
+      if (!lu.factor(M, r)) {
+#pragma omp atomic write
+        fail = 1;
+        continue;
+      }
+      std::vector<zd> rhs(r);
+      for (size_t c = 0; c < cols.size(); ++c) {
+        for (int a = 0; a < r; ++a) rhs[a] = cx.H(np.to[a], cols[c]);
+        lu.solve(rhs.data());
+        for (int a = 0; a < r; ++a) out[(size_t)c * r + a] = {rhs[a].real(), rhs[a].imag()};
+      }
+    } else {
+      // U~ = H(t, si) H(ti, si)^{-1}: rows = t (leaf points or child's ti), cols = ti.
+      // X M = B  <=>  M^T X^T = B^T : factor M^T, solve one row of X per right-hand side.
+      int r = (int)np.ti.size();
+      std::vector<int32_t> rows;
+      if (J.kind == 3) {
+        const Box& B = leaf.boxes[J.child];
+        for (int32_t t = B.begin; t < B.end; ++t) rows.push_back(P.perm[t]);
+      } else {
+        rows = P.piv[J.level + 1][J.child].ti;
+      }
+      std::vector<zd> MT((size_t)r * r);
+      for (int a = 0; a < r; ++a)
+        for (int c = 0; c < r; ++c) MT[(size_t)c * r + a] = cx.H(np.ti[a], np.si[c]);
+      LU lu;
+      if (!lu.factor(MT, r)) {
+#pragma omp atomic write
+        fail = 1;
+        continue;
+      }
+      std::vector<zd> rhs(r);
+      int nr = (int)rows.size();
+      for (int a = 0; a < nr; ++a) {
+        for (int c = 0; c < r; ++c) rhs[c] = cx.H(rows[a], np.si[c]);
+        lu.solve(rhs.data());
+        for (int c = 0; c < r; ++c) out[(size_t)c * nr + a] = {rhs[c].real(), rhs[c].imag()};
+      }
+    }
+  }
+  if (fail) {
+    err = "singular NCA cross matrix";
+    return DAFMM_ESETUP;
+  }
+  (void)t0;
+  return DAFMM_OK;
+}
+
+// ============================================================================================
+// Plan export (.npy files) for the oracle.
+namespace {
+template <typename T>
+bool write_npy(const std::string& path, const char* descr, const std::vector<T>& data, std::vector<int64_t> shape) {
+  FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) return false;
+  std::string sh = "(";
+  for (size_t i = 0; i < shape.size(); ++i) sh += std::to_string(shape[i]) + (shape.size() == 1 ? "," : (i + 1 < shape.size() ? ", " : ""));
+  sh += ")";
+  std::string hdr = std::string("{'descr': '") + descr + "', 'fortran_order': False, 'shape': " + sh + ", }";
+  size_t total = 10 + hdr.size() + 1;
+  size_t pad = (64 - total % 64) % 64;
+  hdr += std::string(pad, ' ') + "\n";
+  unsigned char magic[8] = {0x93, 'N', 'U', 'M', 'P', 'Y', 1, 0};
+  uint16_t hl = (uint16_t)hdr.size();
+  std::fwrite(magic, 1, 8, f);
+  std::fwrite(&hl, 2, 1, f);
+  std::fwrite(hdr.data(), 1, hdr.size(), f);
+  if (!data.empty()) std::fwrite(data.data(), sizeof(T), data.size(), f);
+  std::fclose(f);
+  return true;
+}
+}  // namespace
+
+int export_plan(const Plan& P, const std::string& dir, std::string& err) {
+  mkdir(dir.c_str(), 0755);
+  bool ok = true;
+  std::vector<double> meta = {(double)P.n, (double)P.L, P.W, P.x0, P.y0, P.kappa, P.opt.T, P.nca_tol};
+  ok &= write_npy(dir + "/meta.npy", "<f8", meta, {(int64_t)meta.size()});
+  std::vector<int64_t> perm(P.perm.begin(), P.perm.end());
+  ok &= write_npy(dir + "/perm.npy", "<i8", perm, {(int64_t)perm.size()});
+  for (int l = 0; l <= P.L; ++l) {
+    const Level& lv = P.levels[l];
+    std::string pre = dir + "/l" + std::to_string(l) + "_";
+    std::vector<int64_t> boxes;
+    for (auto& b : lv.boxes) { boxes.push_back(b.ix); boxes.push_back(b.iy); }
+    ok &= write_npy(pre + "boxes.npy", "<i8", boxes, {(int64_t)lv.boxes.size(), 2});
+    std::vector<int64_t> info = {lv.hfr ? 1 : 0, lv.ncones};
+    ok &= write_npy(pre + "info.npy", "<i8", info, {2});
+    auto csr = [&](const std::vector<std::vector<int>>& lists, const std::string& name) {
+      std::vector<int64_t> ptr = {0}, idx;
+      for (auto& v : lists) {
+        for (int a : v) idx.push_back(a);
+        ptr.push_back((int64_t)idx.size());
+      }
+      ok &= write_npy(pre + name + "_ptr.npy", "<i8", ptr, {(int64_t)ptr.size()});
+      ok &= write_npy(pre + name + "_idx.npy", "<i8", idx, {(int64_t)idx.size()});
+    };
+    csr(lv.N, "N");
+    if (l >= 1) {
+      csr(lv.IL, "IL");
+      std::vector<int64_t> dir4;
+      for (size_t b = 0; b < lv.ILdir.size(); ++b)
+        for (auto& e : lv.ILdir[b]) { dir4.push_back((int64_t)b); dir4.push_back(e[0]); dir4.push_back(e[1]); dir4.push_back(e[2]); }
+      ok &= write_npy(pre + "ILdir.npy", "<i8", dir4, {(int64_t)dir4.size() / 4, 4});
+      std::vector<int64_t> nodes;
+      for (auto& nd : lv.nodes) { nodes.push_back(nd.first); nodes.push_back(nd.second); }
+      ok &= write_npy(pre + "nodes.npy", "<i8", nodes, {(int64_t)lv.nodes.size(), 2});
+      const char* names[4] = {"ti", "si", "to", "so"};
+      for (int s = 0; s < 4; ++s) {
+        std::vector<int64_t> ptr = {0}, idx;
+        for (auto& np : P.piv[l]) {
+          const std::vector<int32_t>& v = s == 0 ? np.ti : s == 1 ? np.si : s == 2 ? np.to : np.so;
+          for (int32_t a : v) idx.push_back(a);
+          ptr.push_back((int64_t)idx.size());
+        }
+        ok &= write_npy(pre + names[s] + "_ptr.npy", "<i8", ptr, {(int64_t)ptr.size()});
+        ok &= write_npy(pre + names[s] + "_idx.npy", "<i8", idx, {(int64_t)idx.size()});
+      }
+    }
+  }
+  if (!ok) { err = "could not write plan files to " + dir; return DAFMM_EINVAL; }
+  return DAFMM_OK;
+}
+
+}  // namespace dafmm

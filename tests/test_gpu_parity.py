@@ -1,0 +1,125 @@
+"""GPU parity: the CUDA DAFMM (through the C-ABI) against the oracle's serial DAFMM on the
+product's validated pivots (<= 1e-11 relative l2 on y - x, D10) and against the dense
+product (<= 10 nca_tol); edge cases; sampled rows at full config-4 size."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle
+from oracle.core import Problem
+from oracle.nca import NCA
+from oracle.plan_io import compare_lists, load_plan, validate_pivots
+from oracle.tree import Lists, Tree
+from synth.configs import make_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _prod():
+    import paper_2204_00326_b200 as prod
+    return prod
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _gpu_matvec(op, x, mask=3):
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    yd = torch.empty_like(xd)
+    op.matvec(xd, yd, mask)
+    torch.cuda.synchronize()
+    return yd.cpu().numpy()
+
+
+def _oracle_on_product_plan(P, op, tmp_path):
+    op.export_plan(tmp_path / "plan")
+    plan = load_plan(tmp_path / "plan")
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    compare_lists(plan, tree, lists)
+    piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv)
+    validate_pivots(nca, piv)
+    return prob, nca
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0),
+                                          ("c1", 128, 4.0), ("c1", 40, 7.0)])
+def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
+    P = make_problem(name, n=n, kappa=kappa)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path)
+    x = P["x"]
+    y_gpu = _gpu_matvec(op, x)
+    y_cpu = nca.matvec(x)
+    assert _rel(y_gpu - x, y_cpu - x) <= 1e-11
+    rows = np.arange(0, prob.n, 3)
+    yd = oracle.dense_matvec_rows(prob, x, rows)
+    assert _rel(y_gpu[rows] - x[rows], yd - x[rows]) <= 10 * P["nca_tol"]
+    # pass accounting: near + far = full (far omits the identity)
+    near = _gpu_matvec(op, x, 1)
+    far = _gpu_matvec(op, x, 2)
+    assert _rel(near + far, y_gpu) <= 1e-14
+    assert _rel(near - x, nca.matvec(x, parts=("near",)) - x) <= 1e-12
+
+
+def test_gpu_zero_contrast_identity_and_linearity():
+    P = make_problem("c1")
+    op = _prod().DAFMM(P["points"], P["weights"], np.zeros(4096), P["kappa"], 64, P["nca_tol"])
+    assert np.array_equal(_gpu_matvec(op, P["x"]), P["x"])
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    rng = np.random.default_rng(1)
+    x1 = rng.standard_normal(4096) + 1j * rng.standard_normal(4096)
+    a, b = 0.7 - 0.2j, -1.5 + 2j
+    lhs = _gpu_matvec(op, a * x1 + b * P["x"])
+    rhs = a * _gpu_matvec(op, x1) + b * _gpu_matvec(op, P["x"])
+    assert _rel(lhs, rhs) <= 1e-13
+
+
+def test_gpu_single_level_equals_dense():
+    P = make_problem("c1", n=16, kappa=2.0)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, 1e-8)
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    assert _rel(_gpu_matvec(op, P["x"]), oracle.dense_matvec(prob, P["x"])) <= 1e-14
+
+
+def test_gpu_ragged_points_and_potential_mode(tmp_path):
+    """Random (non-lattice) points, ragged leaves, and the E1-style potential mode y = K x."""
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(-1, 1, size=(3000, 2))
+    w = np.full(3000, 4.0 / 3000)
+    q = 1.0 + 0.5 * np.cos(3 * pts[:, 0])
+    P = dict(points=pts, weights=w, q=q, kappa=12.0, nca_tol=1e-8, x=np.exp(1j * rng.uniform(0, 6.3, 3000)))
+    op = _prod().DAFMM(pts, w, q, 12.0, 64, 1e-8)
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path)
+    y = _gpu_matvec(op, P["x"])
+    assert _rel(y - P["x"], nca.matvec(P["x"]) - P["x"]) <= 1e-11
+    op2 = _prod().DAFMM(pts, w, q, 12.0, 64, 1e-8, kernel_mode=1, self_term=0)
+    y2 = _gpu_matvec(op2, P["x"])
+    prob0 = Problem(pts, w, q, 12.0, self_term="zero")
+    ref = oracle.K_block(prob0, np.arange(0, 3000, 5), np.arange(3000)) @ P["x"]
+    assert _rel(y2[::5], ref) <= 10 * 1e-8
+
+
+def test_gpu_host_path_matches_device_path():
+    P = make_problem("c1")
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    yh = np.empty(4096, dtype=np.complex128)
+    op.matvec_host(np.ascontiguousarray(P["x"]), yh)
+    assert np.array_equal(yh, _gpu_matvec(op, P["x"]))
+
+
+def test_gpu_invalid_inputs():
+    prod = _prod()
+    P = make_problem("c1", n=16)
+    with pytest.raises(prod.DAFMMError):
+        prod.DAFMM(P["points"], P["weights"], P["q"], -1.0, 64, 1e-8)
+    bad = P["points"].copy()
+    bad[3] = bad[2]
+    with pytest.raises(prod.DAFMMError):
+        prod.DAFMM(bad, P["weights"], P["q"], 5.0, 64, 1e-8)
+    with pytest.raises(prod.DAFMMError):
+        prod.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1.5)
