@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the B200 DAFMM matvec y = x + kappa^2 q o V[x] (arxiv 2204.00326).
+
+Metric (BASELINE.json): DAFMM matvec unknowns/s at N = 1M, kappa = 160 (complex fp64), the
+fraction of the fp64 roofline, and the GMRES solve time.  One "step" is one full matvec
+(gather, P2M, M2M, M2L, L2L, near field + L2P + combine: every §8(a) row a1-a12) through the
+C-ABI ``dafmm_matvec`` on device-resident vectors.  Setup (host tree / lists / NCA / operators
+and upload) is timed separately and reported as ``setup_s``.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank runs an independent replica of the workload on its own GPU
+("replicas only"; the north star is single-GPU), timing is the max over
+ranks, and value = N x unknowns / max time ("scaling": "weak").
+
+Timing: W untimed warm-up matvecs; then K timed matvecs, each bracketed by CUDA events on the
+handle's stream; L2 is flushed (512 MiB memset) between timed steps, outside the events; the
+whole region is bracketed by barrier + synchronize.  Clocks are sampled with nvidia-smi during
+the timed region.  ``e2e`` repeats the measurement through ``dafmm_matvec_host`` (pinned host
+x -> device, matvec, device -> pinned host y; copies inside the events).
+
+The ``cpu_baseline`` leg (rank 0, N = 1 only) and ``--impl reference`` time the CPU oracle
+(oracle/, test infrastructure) as it stands: the dense definition of the product on a bounded
+sample of rows of the same workload, on all host cores (OpenMP).  Its rows are also compared
+with the GPU result of the same x (``sampled_rel_err``).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from synth.configs import CONFIGS, make_problem  # noqa: E402
+
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "roofline_inputs.json")
+MEASURED_PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+# fp64 peak when profiles/roofline_inputs.json has no measured value: 148 SMs x 64 DFMA/clk x
+# 2 flop x 1.965 GHz (unit counts and the max SM clock)
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+BAD_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown")
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args(argv)
+
+
+# ---------------------------------------------------------------------------------------------
+# distributed plumbing (pure functions are unit-tested on CPU with gloo, tests/test_bench_host.py)
+# ---------------------------------------------------------------------------------------------
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def max_over_ranks(value, device=None):
+    """Max of a float over all ranks (identity without an initialised process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(device=None):
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        if device is not None and str(device).startswith("cuda"):
+            dist.barrier(device_ids=[int(str(device).split(":")[1])])
+        else:
+            dist.barrier()
+
+
+def whole_job_value(n_unknowns, world, ms_per_step_max):
+    """Aggregate unknowns/s over all replicas (weak scaling)."""
+    return n_unknowns * world / (ms_per_step_max * 1e-3)
+
+
+def roofline_entry(pass_ms, matvecs, stats, inputs):
+    """Roofline object for the dominant far/near kernel.
+
+    achieved = kernel entries per launch x fp64 flops per entry (counted by ncu on the shipped
+    evaluator, profiles/roofline_inputs.json) / average launch duration (CUDA events)."""
+    entries = {"near": stats["p2p_pairs"], "m2l": stats["m2l_entries"]}
+    dom = max(("near", "m2l"), key=lambda k: pass_ms.get(k, 0.0))
+    avg_ms = pass_ms[dom] / max(matvecs, 1)
+    kin = inputs.get("kernels", {}).get(dom, {})
+    fpe = kin.get("fp64_flops_per_entry")
+    peak = inputs.get("fp64_tflops_measured")
+    peak_src = "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/)"
+    if not peak:
+        peak, peak_src = FP64_NOMINAL_TFLOPS, "nominal 148 SM x 64 DFMA/clk x 1.965 GHz"
+    achieved = entries[dom] * fpe / (avg_ms * 1e-3) / 1e12 if fpe else None
+    return {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": kin.get("dram_bytes_per_launch"),
+            "avg_launch_ms": avg_ms, "entries_per_launch": entries[dom],
+            "entries_per_s": entries[dom] / (avg_ms * 1e-3), "fp64_flops_per_entry": fpe,
+            "peak_source": peak_src, "ncu_source": inputs.get("source")}
+
+
+def summarize_clocks(rows):
+    """rows: list of dicts from nvidia-smi csv (sm, max, reasons...) -> clocks object."""
+    if not rows:
+        return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+    sms = [r["sm"] for r in rows]
+    reasons = set()
+    for r in rows:
+        for k in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"):
+            if r.get(k) == "Active":
+                reasons.add(k)
+    return {"sm_mhz": statistics.median(sms), "sm_max_mhz": max(r["max"] for r in rows),
+            "reasons": sorted(reasons), "samples": len(rows)}
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + self.FIELDS,
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [v.strip() for v in line.split(",")]
+            try:
+                self.rows.append(dict(sm=float(p[0]), max=float(p[1]), hw_slowdown=p[2], hw_thermal_slowdown=p[3],
+                                      sw_thermal_slowdown=p[4], sw_power_cap=p[5]))
+            except (ValueError, IndexError):
+                pass
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=5)
+        return summarize_clocks(self.rows)
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def workload_name(P):
+    cfg = CONFIGS[P["name"]]
+    return ("%s: %dx%d cell-centred grid on [-1,1]^2, N=%d, kappa=%g, q=%s, x=unit-modulus seeded phases, "
+            "leaf 64, nca_tol %g" % (P["name"], cfg["n"], cfg["n"], P["points"].shape[0], P["kappa"],
+                                      cfg["contrast"], P["nca_tol"]))
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------------------------
+def oracle_rows_sample(P, target_s, max_rows=4096):
+    """Time the oracle's dense product (plain definition, oracle/src/oracle_core.c, OpenMP over
+    rows) on a seeded sample of rows sized for about target_s seconds.  Returns
+    (rows/s, rows, seconds, y_rows)."""
+    import oracle
+    prob = oracle.Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    n = prob.n
+    rng = np.random.default_rng(12345)
+    probe = np.sort(rng.choice(n, size=min(16, n), replace=False))
+    t0 = time.perf_counter()
+    oracle.dense_matvec_rows(prob, P["x"], probe)
+    dt = time.perf_counter() - t0
+    rows_n = int(min(max_rows, n, max(16, target_s / max(dt, 1e-9) * probe.size)))
+    rows = np.sort(rng.choice(n, size=rows_n, replace=False))
+    t0 = time.perf_counter()
+    y_rows = oracle.dense_matvec_rows(prob, P["x"], rows)
+    secs = time.perf_counter() - t0
+    return rows_n / secs, rows, secs, y_rows
+
+
+def host_cores():
+    v = os.environ.get("OMP_NUM_THREADS")
+    return int(v) if v and v.isdigit() else os.cpu_count()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    P = make_problem(args.config)
+    n_steps = args.steps + args.warmup
+    per_step = max(1.0, min(10.0, 150.0 / max(n_steps, 1)))
+    vals, secs_all, rows_total = [], 0.0, 0
+    for i in range(n_steps):
+        rate, rows, secs, _ = oracle_rows_sample(P, per_step)
+        if i >= args.warmup:
+            vals.append(rate)
+            secs_all += secs
+            rows_total += rows.size
+    value = rows_total / secs_all
+    sample = "dense product rows (oracle_core.c, all N columns) on %d seeded rows per step" % (rows_total // max(
+        args.steps, 1))
+    line = {"impl": "reference", "metric": "DAFMM matvec unknowns/s", "value": value, "unit": "unknowns/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs_all * 1e3 / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(P), "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "unknowns/s", "cores": host_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "unknowns/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------------------------
+def time_matvecs(op, stream, x, y, steps, flush, host=None):
+    """Per-step CUDA-event times (ms) of `steps` matvecs on `stream`, L2 flushed in between."""
+    import torch
+    times = []
+    for _ in range(steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        if host is None:
+            op.matvec(x, y)
+        else:
+            op.matvec_host(host[0], host[1])
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return times
+
+
+def gmres_case(name, prod, torch):
+    P = make_problem(name)
+    t0 = time.perf_counter()
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    setup = time.perf_counter() - t0
+    f = torch.from_numpy(P["f"]).cuda()
+    psi = torch.empty_like(f)
+    maxit = 3000
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rc, iters, relres = op.gmres(f, psi, P["gmres_tol"], maxit, 50)
+    solve = time.perf_counter() - t0
+    op.close()
+    return {"config": name, "N": int(P["points"].shape[0]), "kappa": P["kappa"], "tol": P["gmres_tol"],
+            "restart": 50, "status": "converged" if rc == 0 else "not_converged", "iterations": iters,
+            "true_relres": relres, "solve_s": solve, "setup_s": setup}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2204_00326_b200 as prod
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P = make_problem(args.config)
+    N = int(P["points"].shape[0])
+    t0 = time.perf_counter()
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    setup_s = time.perf_counter() - t0
+    stats = op.stats()
+    stream = torch.cuda.Stream(device=dev)
+    op.set_stream(stream)
+    x = torch.from_numpy(P["x"]).to(dev)
+    y = torch.empty_like(x)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    time_matvecs(op, stream, x, y, args.warmup, flush)
+    op.set_profiling(True)
+    torch.cuda.synchronize()
+    barrier(dev)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local).start()
+    time.sleep(0.3)  # let the sampler start before the timed region
+    times = time_matvecs(op, stream, x, y, args.steps, flush)
+    torch.cuda.synchronize()
+    barrier(dev)
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    pass_ms, matvecs, launches = op.pass_times()
+    op.set_profiling(False)
+    ms_local = sum(times) / len(times)
+    ms_max = max_over_ranks(ms_local, dev)
+    value = whole_job_value(N, world, ms_max)
+
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+        yh = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+        xh.copy_(torch.from_numpy(P["x"]))
+        host = (xh.numpy(), yh.numpy())
+        time_matvecs(op, stream, None, None, max(1, args.warmup), flush, host)
+        barrier(dev)
+        et = time_matvecs(op, stream, None, None, args.steps, flush, host)
+        e_ms = max_over_ranks(sum(et) / len(et), dev)
+        e2e = {"value": whole_job_value(N, world, e_ms), "unit": "unknowns/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": int(xh.numel() * xh.element_size()),
+               "d2h_bytes_per_step": int(yh.numel() * yh.element_size()),
+               "path": "dafmm_matvec_host (pinned host buffers)"}
+
+    line = None
+    if rank == 0:
+        inputs = load_json(PROFILE_SUMMARY)
+        roof = roofline_entry(pass_ms, matvecs, stats, inputs)
+        line = {"metric": "DAFMM matvec unknowns/s", "value": value, "unit": "unknowns/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+                "ms_per_step_min": min(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": workload_name(P), "N": N, "kappa": P["kappa"], "nca_tol": P["nca_tol"],
+                           "leaf_size": 64, "complex": True, "parallelism": "replicas" if world > 1 else "1 GPU",
+                           "l2": "flushed between steps (512 MiB memset outside the events)"},
+                "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
+                "gpu_launches_per_step": launches / max(matvecs, 1),
+                "roofline": roof,
+                "pass_ms_per_step": {k: v / max(matvecs, 1) for k, v in pass_ms.items()},
+                "setup_s": setup_s,
+                "setup_breakdown_s": {k: stats[k] for k in ("setup_tree_s", "setup_lists_s", "setup_nca_s",
+                                                           "setup_ops_s", "setup_upload_s")},
+                "plan": {k: stats[k] for k in ("levels", "n_nodes", "p2p_pairs", "m2l_entries", "m2l_pairs",
+                                               "operator_bytes", "device_bytes", "mean_rank_leaf_in",
+                                               "mean_rank_leaf_out", "max_rank")}}
+        if world == 1 and not args.no_cpu_baseline:
+            rate, rows, secs, y_rows = oracle_rows_sample(P, 15.0)
+            op.matvec(x, y)
+            torch.cuda.synchronize()
+            yg = y.cpu().numpy()[rows]
+            xs = P["x"][rows]
+            line["cpu_baseline"] = {"value": rate, "unit": "unknowns/s", "cores": host_cores(), "kind": "oracle",
+                                    "sample": "dense definition of A x (oracle_core.c, OpenMP) on %d seeded rows "
+                                              "x all %d columns of the same workload, %.1f s" % (rows.size, N, secs),
+                                    "sampled_rel_err": float(np.linalg.norm((yg - xs) - (y_rows - xs)) /
+                                                             np.linalg.norm(y_rows - xs))}
+        if world == 1 and not args.no_gmres:
+            op.close()
+            line["gmres"] = [gmres_case(c, prod, torch) for c in ("c2", "c3")]
+        print(json.dumps(line), flush=True)
+    op.close()
+    if world > 1:
+        barrier(dev)
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -80,6 +80,8 @@ typedef struct {
   int32_t max_rank;
   double setup_tree_s, setup_lists_s, setup_nca_s, setup_ops_s, setup_pack_s, setup_upload_s;
   int64_t aca_entries;       /* kernel entries evaluated by ACA during setup */
+  int64_t m2l_band_entries[16]; /* M2L entries per H0 band code (0 generic, 1 near, 2+b far band b) */
+  int64_t p2p_band_entries[16]; /* P2P point pairs per band code */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);
@@ -125,7 +127,24 @@ int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int max
 /* Use stream s (a cudaStream_t) for all later device work of the handle. */
 int dafmm_set_stream(dafmm_handle h, void* stream);
 
+/* Statistics of the plan (sizes, ranks, setup wall times).  Host only; never fails on a
+ * valid handle. */
 int dafmm_stats(dafmm_handle h, dafmm_stats_t* out);
+
+/* Per-pass profiling (SURVEY §5 "CUDA events per pass").  dafmm_set_profiling(h, 1) creates
+ * CUDA events on the handle's stream around each pass of every later matvec and resets the
+ * accumulators and the kernel-launch counter; 0 switches event recording off (the counter
+ * keeps counting).  dafmm_pass_times synchronises on the last profiled matvec and writes the
+ * accumulated milliseconds per pass into ms_out[DAFMM_NUM_PASSES], in the order
+ *   0 gather (caller order -> tree order, w scaling)
+ *   1 P2M     2 M2M, all levels     3 M2L, all levels
+ *   4 L2L, all levels     5 near field P2P + L2P + combine + scatter
+ * plus the number of profiled matvecs and the number of kernels launched by the library since
+ * the last reset (either pointer may be NULL).  The memsets of the expansion buffers fall in
+ * pass 0.  Errors: DAFMM_EINVAL (null handle / host-only plan), DAFMM_ECUDA. */
+#define DAFMM_NUM_PASSES 6
+int dafmm_set_profiling(dafmm_handle h, int enable);
+int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64_t* launches_out);
 
 /* Write the tree, lists, cones and pivot index sets as .npy files into directory `path`
  * (created if missing) for the independent CPU oracle.  Synchronous, host only. */

@@ -14,7 +14,10 @@ _lib = None
 
 EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_matvec", "dafmm_matvec_parts",
             "dafmm_matvec_host", "ls_gmres_solve", "dafmm_set_stream", "dafmm_stats", "dafmm_export_plan",
-            "dafmm_destroy", "dafmm_last_error"]
+            "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times"]
+
+NUM_PASSES = 6
+PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near"]
 
 DAFMM_OK, DAFMM_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "DAFMM_EINVAL", -2: "DAFMM_ECUDA", -3: "DAFMM_ENOMEM", -4: "DAFMM_ESETUP"}
@@ -40,10 +43,14 @@ class Stats(ctypes.Structure):
                 ("setup_tree_s", ctypes.c_double), ("setup_lists_s", ctypes.c_double),
                 ("setup_nca_s", ctypes.c_double), ("setup_ops_s", ctypes.c_double),
                 ("setup_pack_s", ctypes.c_double), ("setup_upload_s", ctypes.c_double),
-                ("aca_entries", ctypes.c_int64)]
+                ("aca_entries", ctypes.c_int64), ("m2l_band_entries", ctypes.c_int64 * 16),
+                ("p2p_band_entries", ctypes.c_int64 * 16)]
 
     def as_dict(self):
-        return {f: getattr(self, f) for f, _ in self._fields_}
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        for k in ("m2l_band_entries", "p2p_band_entries"):
+            d[k] = list(d[k])
+        return d
 
 
 def library_path():
@@ -69,6 +76,8 @@ def load():
     lib.dafmm_set_stream.argtypes = [vp, vp]
     lib.dafmm_stats.argtypes = [vp, ctypes.POINTER(Stats)]
     lib.dafmm_export_plan.argtypes = [vp, ctypes.c_char_p]
+    lib.dafmm_set_profiling.argtypes = [vp, i32]
+    lib.dafmm_pass_times.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.dafmm_destroy.argtypes = [vp]
     lib.dafmm_destroy.restype = None
     lib.dafmm_last_error.restype = ctypes.c_char_p
@@ -167,6 +176,18 @@ def dafmm_stats(h):
     return s.as_dict()
 
 
+def dafmm_set_profiling(h, enable):
+    return _check(load().dafmm_set_profiling(h, int(bool(enable))))
+
+
+def dafmm_pass_times(h):
+    """Returns ({pass name: accumulated ms}, profiled matvecs, kernel launches since reset)."""
+    ms = (ctypes.c_double * NUM_PASSES)()
+    cnt, launches = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().dafmm_pass_times(h, ms, ctypes.byref(cnt), ctypes.byref(launches)))
+    return dict(zip(PASS_NAMES, list(ms))), cnt.value, launches.value
+
+
 def dafmm_export_plan(h, path):
     return _check(load().dafmm_export_plan(h, str(path).encode()))
 
@@ -205,6 +226,12 @@ class DAFMM:
 
     def stats(self):
         return dafmm_stats(self.h)
+
+    def set_profiling(self, enable=True):
+        dafmm_set_profiling(self.h, enable)
+
+    def pass_times(self):
+        return dafmm_pass_times(self.h)
 
     def export_plan(self, path):
         dafmm_export_plan(self.h, path)

@@ -16,6 +16,7 @@ struct dafmm_plan {
   dafmm::DevPlan dev;
   int64_t operator_bytes = 0;
   int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;
+  std::vector<int64_t> m2l_band, p2p_band;
 };
 
 namespace {
@@ -86,6 +87,8 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     h->p2p_pairs = pk.p2p_pairs;
     h->m2l_entries = pk.m2l_entries;
     h->m2l_pairs = pk.m2l_pairs;
+    h->m2l_band = pk.m2l_band_entries;
+    h->p2p_band = pk.p2p_band_entries;
   } catch (const std::bad_alloc&) {
     dafmm::free_plan(h->dev);
     return fail(DAFMM_ENOMEM, "host allocation failed during setup");
@@ -149,6 +152,26 @@ int dafmm_set_stream(dafmm_handle h, void* stream) {
   return DAFMM_OK;
 }
 
+int dafmm_set_profiling(dafmm_handle h, int enable) {
+  if (!h) return fail(DAFMM_EINVAL, "null handle");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  std::string err;
+  int rc = dafmm::set_profiling(h->dev, enable != 0, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
+
+int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64_t* launches_out) {
+  if (!h || !ms_out) return fail(DAFMM_EINVAL, "null argument");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  std::string err;
+  int rc = dafmm::harvest_profile(h->dev, err);
+  if (rc != DAFMM_OK) return fail(rc, err);
+  for (int p = 0; p < dafmm::kNumPasses; ++p) ms_out[p] = h->dev.prof_ms[p];
+  if (matvecs_out) *matvecs_out = h->dev.prof_count;
+  if (launches_out) *launches_out = h->dev.launches;
+  return DAFMM_OK;
+}
+
 int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   if (!h || !out) return fail(DAFMM_EINVAL, "null argument");
   std::memset(out, 0, sizeof(*out));
@@ -185,6 +208,8 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->setup_pack_s = P.t_pack;
   out->setup_upload_s = P.t_upload;
   out->aca_entries = P.aca_entries;
+  for (size_t b = 0; b < h->m2l_band.size() && b < 16; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
+  for (size_t b = 0; b < h->p2p_band.size() && b < 16; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
   return DAFMM_OK;
 }
 

@@ -9,6 +9,9 @@
 
 namespace dafmm {
 
+// Passes timed by the profiler, in launch order (DAFMM_PASS_* of dafmm.h).
+constexpr int kNumPasses = 6;  // gather, p2m, m2m, m2l, l2l, near (P2P + L2P + combine)
+
 struct DevBatch {
   int items = 0;
   int64_t* dst_off = nullptr;
@@ -45,6 +48,10 @@ struct DevPlan {
   int32_t* m2l_src_ptr = nullptr;
   int64_t* m2l_src_off = nullptr;
   int32_t* m2l_src_cnt = nullptr;
+  int32_t* m2l_item_ptr = nullptr;
+  int32_t* m2l_item_code = nullptr;
+  int32_t* m2l_item_begin = nullptr;
+  int32_t* m2l_item_end = nullptr;
   // leaves
   int nleaves = 0, max_leaf = 0;
   int32_t* leaf_begin = nullptr;
@@ -55,6 +62,7 @@ struct DevPlan {
   int64_t* leaf_loc_off = nullptr;
   int32_t* leaf_rank = nullptr;
   int64_t* leaf_U_off = nullptr;
+  int32_t* leaf_band = nullptr;
   // scratch
   double2* x_t = nullptr;
   double2* v_t = nullptr;
@@ -72,7 +80,19 @@ struct DevPlan {
   int gm_part_blocks = 0;
   size_t device_bytes = 0;
   std::vector<void*> allocations;
+  // per-pass CUDA-event profiling (dafmm_set_profiling / dafmm_pass_times)
+  int64_t launches = 0;          // kernels launched by run_matvec / run_gmres since the last reset
+  bool prof = false;
+  bool prof_pending = false;     // events of the last profiled matvec not yet harvested
+  cudaEvent_t prof_ev[kNumPasses + 1] = {};
+  double prof_ms[kNumPasses] = {};
+  int64_t prof_count = 0;        // profiled matvecs harvested
 };
+
+// Enable / disable per-pass event timing; resets the accumulators and the launch counter.
+int set_profiling(DevPlan& d, bool on, std::string& err);
+// Harvest the events of the last profiled matvec into prof_ms (synchronises on them).
+int harvest_profile(DevPlan& d, std::string& err);
 
 int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err);
 void free_plan(DevPlan& d);

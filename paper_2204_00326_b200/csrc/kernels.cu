@@ -24,6 +24,7 @@ namespace {
 constexpr int kNearThreads = 256;
 constexpr int kM2LThreads = 128;
 constexpr int kStage = 512;  // staged source pivots / points per chunk (32 B each)
+constexpr int kTB = 4;       // kernel entries evaluated in lockstep per thread (shared coefficients)
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
@@ -90,18 +91,115 @@ __device__ __forceinline__ void stage_sources(double4* sbuf, int fill, const dou
   }
 }
 
+// Source lists as CSR entries e -> (first source, count).
+struct M2LSources {
+  const int64_t* off;
+  const int32_t* cnt;
+  __device__ __forceinline__ int64_t first(int e) const { return off[e]; }
+  __device__ __forceinline__ int count(int e) const { return cnt[e]; }
+};
+struct NearSources {
+  const int32_t* begin;
+  const int32_t* end;
+  __device__ __forceinline__ int64_t first(int e) const { return begin[e]; }
+  __device__ __forceinline__ int count(int e) const { return end[e] - begin[e]; }
+};
+
+// acc += sum over the source entries [e, pe) of H0_band(kappa |xt - s_j|) v_j.  Sources are
+// staged through shared memory in chunks of kStage; thread (t, slice) takes every nsl-th
+// staged source.  CTA-uniform (contains barriers): every thread calls it with the same
+// arguments apart from xt / active / slice.  GUARD: the segment may contain the pair i == j
+// (the own leaf of the near field), whose entry is excluded (its value is the self term D_i).
+template <int CODE, bool GUARD, class Src>
+__device__ __forceinline__ void accumulate(double4* sbuf, const Src& src, int e, int pe, const double2* __restrict__ xy,
+                                           const double2* __restrict__ val, double2 xt, bool active, int slice,
+                                           int nsl, double& ar, double& ai, const KernelConsts& kc,
+                                           const Pair* logtab) {
+  int kin = 0;
+  while (e < pe) {
+    int fill = 0;
+    while (e < pe && fill < kStage) {
+      int cnt = src.count(e);
+      int take = min(cnt - kin, kStage - fill);
+      stage_sources(sbuf, fill, xy, val, src.first(e) + kin, take);
+      fill += take;
+      kin += take;
+      if (kin == cnt) {
+        ++e;
+        kin = 0;
+      }
+    }
+    __syncthreads();
+    if (active) {
+      // kTB staged sources per step (j, j + nsl, ...), evaluated in lockstep; lanes past the
+      // fill (and the i == j pair under GUARD) get a safe distance and a zero weight
+      for (int j = slice; j < fill; j += kTB * nsl) {
+        double r2[kTB], vr[kTB], vi[kTB], hr[kTB], hi[kTB];
+#pragma unroll
+        for (int b = 0; b < kTB; ++b) {
+          const int jb = j + b * nsl;
+          const bool ok = jb < fill;
+          const double4 sv = sbuf[ok ? jb : j];
+          const double dx = xt.x - sv.x, dy = xt.y - sv.y;
+          const double d2 = fma(dx, dx, dy * dy);
+          const bool use = ok && (!GUARD || d2 > 0.0);
+          r2[b] = use ? d2 : kc.r2_safe;
+          vr[b] = use ? sv.z : 0.0;
+          vi[b] = use ? sv.w : 0.0;
+        }
+        h0_band_vec<CODE, kTB>(r2, hr, hi, kc, logtab);
+#pragma unroll
+        for (int b = 0; b < kTB; ++b) {
+          ar = fma(hr[b], vr[b], fma(-hi[b], vi[b], ar));
+          ai = fma(hr[b], vi[b], fma(hi[b], vr[b], ai));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Dispatch a CTA-uniform band code to its instantiation.
+template <bool GUARD, class Src>
+__device__ __forceinline__ void accumulate_code(int code, double4* sbuf, const Src& src, int e, int pe,
+                                                const double2* __restrict__ xy, const double2* __restrict__ val,
+                                                double2 xt, bool active, int slice, int nsl, double& ar, double& ai,
+                                                const KernelConsts& kc, const Pair* logtab) {
+#define DAFMM_BAND_CASE(C) \
+  case C: accumulate<C, GUARD>(sbuf, src, e, pe, xy, val, xt, active, slice, nsl, ar, ai, kc, logtab); break;
+  switch (code) {
+    DAFMM_BAND_CASE(1)
+    DAFMM_BAND_CASE(2)
+    DAFMM_BAND_CASE(3)
+    DAFMM_BAND_CASE(4)
+    DAFMM_BAND_CASE(5)
+    DAFMM_BAND_CASE(6)
+    DAFMM_BAND_CASE(7)
+    DAFMM_BAND_CASE(8)
+    DAFMM_BAND_CASE(9)
+    default: accumulate<kBandGeneric, GUARD>(sbuf, src, e, pe, xy, val, xt, active, slice, nsl, ar, ai, kc, logtab);
+  }
+#undef DAFMM_BAND_CASE
+}
+static_assert(kNumBandCodes == 10, "accumulate_code lists the band codes 1..9 explicitly");
+
 // ---- M2L: u[t] = sum_{src nodes} sum_k H0(kappa |t - s_k|) m_k --------------------
-// One CTA per target node; thread (t, slice) accumulates over staged source pivots.
+// One CTA per target node; its source nodes come in band-uniform segments (items).
 __global__ void __launch_bounds__(kM2LThreads) m2l_kernel(
-    const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows, const int32_t* __restrict__ src_ptr,
-    const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cnt, const double2* __restrict__ ti_xy,
-    const double2* __restrict__ so_xy, const double2* __restrict__ mult, double2* __restrict__ loc, KernelConsts kc) {
+    const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows, const int32_t* __restrict__ item_ptr,
+    const int32_t* __restrict__ item_code, const int32_t* __restrict__ item_begin,
+    const int32_t* __restrict__ item_end, const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cnt,
+    const double2* __restrict__ ti_xy, const double2* __restrict__ so_xy, const double2* __restrict__ mult,
+    double2* __restrict__ loc, KernelConsts kc) {
   __shared__ double4 sbuf[kStage];
   __shared__ double2 red[kM2LThreads];
+  __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
+  load_log_table(logtab);
   const int tgt = blockIdx.x;
   const int r = rows[tgt];
   const int64_t lo = loc_off[tgt];
-  const int ps = src_ptr[tgt], pe = src_ptr[tgt + 1];
+  const int is = item_ptr[tgt], ie = item_ptr[tgt + 1];
+  const M2LSources src{src_off, src_cnt};
   for (int t0 = 0; t0 < r; t0 += kM2LThreads) {
     const int rc = min(kM2LThreads, r - t0);
     const int nsl = kM2LThreads / rc;
@@ -110,29 +208,9 @@ __global__ void __launch_bounds__(kM2LThreads) m2l_kernel(
     const bool active = slice < nsl;
     double2 xt = ld2(ti_xy + lo + t0 + t);
     double ar = 0.0, ai = 0.0;
-    int e = ps, kin = 0;
-    while (e < pe) {
-      int fill = 0;
-      while (e < pe && fill < kStage) {
-        int cnt = src_cnt[e];
-        int take = min(cnt - kin, kStage - fill);
-        stage_sources(sbuf, fill, so_xy, mult, src_off[e] + kin, take);
-        fill += take;
-        kin += take;
-        if (kin == cnt) { ++e; kin = 0; }
-      }
-      __syncthreads();
-      if (active) {
-        for (int j = slice; j < fill; j += nsl) {
-          double4 s = sbuf[j];
-          double dx = xt.x - s.x, dy = xt.y - s.y;
-          cplx h = h0(fma(dx, dx, dy * dy), kc);
-          ar = fma(h.re, s.z, fma(-h.im, s.w, ar));
-          ai = fma(h.re, s.w, fma(h.im, s.z, ai));
-        }
-      }
-      __syncthreads();
-    }
+    for (int it = is; it < ie; ++it)
+      accumulate_code<false>(item_code[it], sbuf, src, item_begin[it], item_end[it], so_xy, mult, xt, active, slice,
+                             nsl, ar, ai, kc, logtab);
     red[threadIdx.x] = make_double2(ar, ai);
     __syncthreads();
     if (threadIdx.x < rc) {
@@ -151,19 +229,25 @@ __global__ void __launch_bounds__(kM2LThreads) m2l_kernel(
 // ---- near field + L2P + combine ------------------------------------------------
 // phi_t = (i/4) [ sum_{j in N(leaf), j != t} H0 v_j + (U u)_t ] + D_t x_t
 // y[perm[t]] = x_t + kappa^2 q_t phi_t   (kernel_mode 0)   or   phi_t   (kernel_mode 1)
+// The leaf's own block is the first near entry (the only one with i == j pairs).
 __global__ void __launch_bounds__(kNearThreads) near_kernel(
     const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end, const int32_t* __restrict__ near_ptr,
-    const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int64_t* __restrict__ leaf_loc_off,
-    const int32_t* __restrict__ leaf_rank, const int64_t* __restrict__ leaf_U_off, const double2* __restrict__ ops,
-    const double2* __restrict__ loc, const double2* __restrict__ pts_t, const double2* __restrict__ v_t,
-    const double2* __restrict__ x_t, const double* __restrict__ qk2_t, const double2* __restrict__ D_t,
-    const int32_t* __restrict__ perm, double2* __restrict__ y, KernelConsts kc, int kernel_mode, unsigned mask) {
+    const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int32_t* __restrict__ leaf_band,
+    const int64_t* __restrict__ leaf_loc_off, const int32_t* __restrict__ leaf_rank,
+    const int64_t* __restrict__ leaf_U_off, const double2* __restrict__ ops, const double2* __restrict__ loc,
+    const double2* __restrict__ pts_t, const double2* __restrict__ v_t, const double2* __restrict__ x_t,
+    const double* __restrict__ qk2_t, const double2* __restrict__ D_t, const int32_t* __restrict__ perm,
+    double2* __restrict__ y, KernelConsts kc, int kernel_mode, unsigned mask) {
   __shared__ double4 sbuf[kStage];
   __shared__ double2 red[kNearThreads];
+  __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
+  load_log_table(logtab);
   const int leaf = blockIdx.x;
   const int tb = leaf_begin[leaf], m = leaf_end[leaf] - tb;
   const int ps = near_ptr[leaf], pe = near_ptr[leaf + 1];
   const bool do_near = mask & 1u, do_far = (mask & 2u) && leaf_loc_off[leaf] >= 0;
+  const int band = leaf_band[leaf];
+  const NearSources src{near_begin, near_end};
   for (int t0 = 0; t0 < m; t0 += kNearThreads) {
     const int rc = min(kNearThreads, m - t0);
     const int nsl = kNearThreads / rc;
@@ -172,32 +256,13 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(
     const bool active = slice < nsl;
     double2 xt = ld2(pts_t + tb + t0 + t);
     double ar = 0.0, ai = 0.0;
-    if (do_near) {
-      int e = ps, kin = 0;
-      while (e < pe) {
-        int fill = 0;
-        while (e < pe && fill < kStage) {
-          int cnt = near_end[e] - near_begin[e];
-          int take = min(cnt - kin, kStage - fill);
-          stage_sources(sbuf, fill, pts_t, v_t, (int64_t)near_begin[e] + kin, take);
-          fill += take;
-          kin += take;
-          if (kin == cnt) { ++e; kin = 0; }
-        }
-        __syncthreads();
-        if (active) {
-          for (int j = slice; j < fill; j += nsl) {
-            double4 s = sbuf[j];
-            double dx = xt.x - s.x, dy = xt.y - s.y;
-            double r2 = fma(dx, dx, dy * dy);
-            if (r2 > 0.0) {
-              cplx h = h0(r2, kc);
-              ar = fma(h.re, s.z, fma(-h.im, s.w, ar));
-              ai = fma(h.re, s.w, fma(h.im, s.z, ai));
-            }
-          }
-        }
-        __syncthreads();
+    if (do_near && pe > ps) {
+      if (band == kBandNear) {
+        accumulate<kBandNear, true>(sbuf, src, ps, ps + 1, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
+        accumulate<kBandNear, false>(sbuf, src, ps + 1, pe, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
+      } else {
+        accumulate<kBandGeneric, true>(sbuf, src, ps, ps + 1, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
+        accumulate<kBandGeneric, false>(sbuf, src, ps + 1, pe, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
       }
     }
     red[threadIdx.x] = make_double2(ar, ai);
@@ -379,12 +444,13 @@ bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& 
          upload(d, &b.src_off, h.src_off, err) && upload(d, &b.src_cols, h.src_cols, err);
 }
 
-void launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate) {
-  if (b.items == 0) return;
+int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate) {
+  if (b.items == 0) return 0;
   int threads = 256;
   int blocks = (b.items * 32 + threads - 1) / threads;
   translate_kernel<<<blocks, threads, 0, d.stream>>>(b.items, b.dst_off, b.dst_rows, b.term_ptr, b.mat_off, b.src_off,
                                                      b.src_cols, d.ops, src, dst, accumulate);
+  return 1;
 }
 
 }  // namespace
@@ -416,13 +482,16 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   d.m2l_targets = (int)pk.m2l_loc_off.size();
   ok = ok && upload(d, &d.m2l_loc_off, pk.m2l_loc_off, err) && upload(d, &d.m2l_rows, pk.m2l_rows, err) &&
        upload(d, &d.m2l_src_ptr, pk.m2l_src_ptr, err) && upload(d, &d.m2l_src_off, pk.m2l_src_off, err) &&
-       upload(d, &d.m2l_src_cnt, pk.m2l_src_cnt, err);
+       upload(d, &d.m2l_src_cnt, pk.m2l_src_cnt, err) && upload(d, &d.m2l_item_ptr, pk.m2l_item_ptr, err) &&
+       upload(d, &d.m2l_item_code, pk.m2l_item_code, err) && upload(d, &d.m2l_item_begin, pk.m2l_item_begin, err) &&
+       upload(d, &d.m2l_item_end, pk.m2l_item_end, err);
   d.nleaves = (int)pk.leaf_begin.size();
   d.max_leaf = pk.max_leaf;
   ok = ok && upload(d, &d.leaf_begin, pk.leaf_begin, err) && upload(d, &d.leaf_end, pk.leaf_end, err) &&
        upload(d, &d.near_ptr, pk.near_ptr, err) && upload(d, &d.near_begin, pk.near_begin, err) &&
        upload(d, &d.near_end, pk.near_end, err) && upload(d, &d.leaf_loc_off, pk.leaf_loc_off, err) &&
-       upload(d, &d.leaf_rank, pk.leaf_rank, err) && upload(d, &d.leaf_U_off, pk.leaf_U_off, err);
+       upload(d, &d.leaf_rank, pk.leaf_rank, err) && upload(d, &d.leaf_U_off, pk.leaf_U_off, err) &&
+       upload(d, &d.leaf_band, pk.leaf_band, err);
   ok = ok && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
        alloc(d, &d.loc, pk.n_loc, err) && alloc(d, &d.host_stage, 2 * plan.n, err);
   if (!ok) return DAFMM_ECUDA;
@@ -430,29 +499,80 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
 }
 
 void free_plan(DevPlan& d) {
+  for (auto& e : d.prof_ev)
+    if (e) {
+      cudaEventDestroy(e);
+      e = nullptr;
+    }
   for (void* p : d.allocations) cudaFree(p);
   d.allocations.clear();
   if (d.gm_hostbuf) cudaFreeHost(d.gm_hostbuf);
   d.gm_hostbuf = nullptr;
 }
 
+int set_profiling(DevPlan& d, bool on, std::string& err) {
+  if (on && !d.prof_ev[0])
+    for (auto& e : d.prof_ev)
+      if (!ck(cudaEventCreate(&e), err, "cudaEventCreate")) return DAFMM_ECUDA;
+  d.prof = on;
+  d.prof_pending = false;
+  for (double& v : d.prof_ms) v = 0.0;
+  d.prof_count = 0;
+  d.launches = 0;
+  return DAFMM_OK;
+}
+
+int harvest_profile(DevPlan& d, std::string& err) {
+  if (!d.prof_pending) return DAFMM_OK;
+  if (!ck(cudaEventSynchronize(d.prof_ev[kNumPasses]), err, "profile event sync")) return DAFMM_ECUDA;
+  for (int p = 0; p < kNumPasses; ++p) {
+    float ms = 0.f;
+    if (!ck(cudaEventElapsedTime(&ms, d.prof_ev[p], d.prof_ev[p + 1]), err, "profile elapsed")) return DAFMM_ECUDA;
+    d.prof_ms[p] += ms;
+  }
+  ++d.prof_count;
+  d.prof_pending = false;
+  return DAFMM_OK;
+}
+
 int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::string& err) {
   cudaStream_t s = d.stream;
+  if (d.prof && harvest_profile(d, err) != DAFMM_OK) return DAFMM_ECUDA;
+  // profiling marks: event p is recorded before pass p (p = 0..5) and event 6 after the last
+  auto mark = [&](int p) {
+    if (d.prof) cudaEventRecord(d.prof_ev[p], s);
+  };
+  mark(0);
   gather_kernel<<<grid_for(d.n, 256, 148 * 16), 256, 0, s>>>(d.n, d.perm, d.w_t, x, d.x_t, d.v_t);
-  if ((mask & 2u) && d.n_mult > 0) {
+  ++d.launches;
+  const bool far = (mask & 2u) && d.n_mult > 0;
+  if (far) {
     cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, s);
     cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, s);
-    launch_translate(d, d.p2m, d.v_t, d.mult, 0);                 // P2M
-    for (auto& b : d.m2m) launch_translate(d, b, d.mult, d.mult, 0);  // M2M
-    if (d.m2l_targets > 0)                                           // M2L
-      m2l_kernel<<<d.m2l_targets, kM2LThreads, 0, s>>>(d.m2l_loc_off, d.m2l_rows, d.m2l_src_ptr, d.m2l_src_off,
-                                                        d.m2l_src_cnt, d.ti_xy, d.so_xy, d.mult, d.loc, d.kc);
-    for (auto& b : d.l2l) launch_translate(d, b, d.loc, d.loc, 1);    // L2L
   }
+  mark(1);
+  if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0);  // P2M
+  mark(2);
+  if (far)
+    for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0);  // M2M
+  mark(3);
+  if (far && d.m2l_targets > 0) {  // M2L
+    m2l_kernel<<<d.m2l_targets, kM2LThreads, 0, s>>>(d.m2l_loc_off, d.m2l_rows, d.m2l_item_ptr, d.m2l_item_code,
+                                                      d.m2l_item_begin, d.m2l_item_end, d.m2l_src_off,
+                                                      d.m2l_src_cnt, d.ti_xy, d.so_xy, d.mult, d.loc, d.kc);
+    ++d.launches;
+  }
+  mark(4);
+  if (far)
+    for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1);  // L2L
+  mark(5);
   near_kernel<<<d.nleaves, kNearThreads, 0, s>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
-                                                 d.leaf_loc_off, d.leaf_rank, d.leaf_U_off, d.ops, d.loc, d.pts_t,
+                                                 d.leaf_band, d.leaf_loc_off, d.leaf_rank, d.leaf_U_off, d.ops, d.loc, d.pts_t,
                                                  d.v_t, d.x_t, d.qk2_t, d.D_t, d.perm, y, d.kc, d.kernel_mode,
-                                                 (d.n_mult > 0) ? mask : (mask & 1u));
+                                                 far ? mask : (mask & 1u));
+  ++d.launches;
+  mark(6);
+  if (d.prof) d.prof_pending = true;
   return ck(cudaGetLastError(), err, "matvec launch") ? DAFMM_OK : DAFMM_ECUDA;
 }
 
@@ -469,9 +589,9 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
     if (d.gm_V) { err = "GMRES workspace already sized for another restart"; return DAFMM_EINVAL; }
     d.gm_restart = m;
     if (!alloc(d, &d.gm_V, (size_t)(m + 1) * n, err) || !alloc(d, &d.gm_w, n, err) || !alloc(d, &d.gm_r, n, err) ||
-        !alloc(d, &d.gm_h, 2 * (m + 2), err) || !alloc(d, &d.gm_part, (size_t)nb * (m + 2), err))
+        !alloc(d, &d.gm_h, 3 * (m + 2), err) || !alloc(d, &d.gm_part, (size_t)nb * (m + 2), err))
       return DAFMM_ECUDA;
-    if (!ck(cudaMallocHost((void**)&d.gm_hostbuf, sizeof(double) * 4 * (m + 2)), err, "cudaMallocHost"))
+    if (!ck(cudaMallocHost((void**)&d.gm_hostbuf, sizeof(double2) * 3 * (m + 2)), err, "cudaMallocHost"))
       return DAFMM_ECUDA;
     d.gm_part_blocks = nb;
   }

@@ -95,6 +95,12 @@ struct Packed {
   std::vector<int32_t> m2l_src_ptr;  // targets + 1
   std::vector<int64_t> m2l_src_off;  // per source entry: multipole offset
   std::vector<int32_t> m2l_src_cnt;  // per source entry: r_o
+  // band-uniform segments of each target's source list: items of target
+  // t are [m2l_item_ptr[t], m2l_item_ptr[t+1]); item i covers source entries
+  // [m2l_item_begin[i], m2l_item_end[i]) whose point pairs all lie in band m2l_item_code[i]
+  std::vector<int32_t> m2l_item_ptr;   // targets + 1
+  std::vector<int32_t> m2l_item_code, m2l_item_begin, m2l_item_end;
+  std::vector<int64_t> m2l_band_entries = std::vector<int64_t>(kNumBandCodes, 0);
   // leaves: near field + L2P + combine
   std::vector<int32_t> leaf_begin, leaf_end;  // tree ranges
   std::vector<int32_t> near_ptr;              // leaves + 1
@@ -102,6 +108,8 @@ struct Packed {
   std::vector<int64_t> leaf_loc_off;          // -1: no far field
   std::vector<int32_t> leaf_rank;             // r_i
   std::vector<int64_t> leaf_U_off;
+  std::vector<int32_t> leaf_band;             // P2P band code: near if every pair has z <= 8
+  std::vector<int64_t> p2p_band_entries = std::vector<int64_t>(kNumBandCodes, 0);
   int max_leaf = 0;
   // statistics
   int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;

@@ -704,23 +704,23 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     bt.term_ptr.push_back((int32_t)bt.mat_off.size());
     pk.l2l.push_back(std::move(bt));
   }
-  // M2L targets (all levels, one launch)
-  pk.m2l_src_ptr.push_back(0);
+  // M2L targets (all levels, one launch).  Each target's source nodes are
+  // classified by the exact z-range of their pivot-point pairs and grouped into band-uniform
+  // segments.
+  struct M2LTarget {
+    int level, node;
+    std::vector<int> src;  // source node ids at `level`
+  };
+  std::vector<M2LTarget> tg;
   for (int l = 1; l <= L; ++l) {
     const Level& lv = P.levels[l];
     for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
       int ri = (int)P.piv[l][nd].ti.size();
       if (ri == 0) continue;
       int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
-      int cnt = 0;
+      M2LTarget t{l, (int)nd, {}};
       auto add_src = [&](int sn) {
-        int ro = (int)P.piv[l][sn].so.size();
-        if (ro == 0) return;
-        pk.m2l_src_off.push_back(moff[l][sn]);
-        pk.m2l_src_cnt.push_back(ro);
-        pk.m2l_entries += (int64_t)ri * ro;
-        ++pk.m2l_pairs;
-        ++cnt;
+        if (!P.piv[l][sn].so.empty()) t.src.push_back(sn);
       };
       if (lv.hfr) {
         for (auto& e : lv.ILdir[b])
@@ -728,13 +728,73 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       } else {
         for (int a : lv.IL[b]) add_src(lv.node_id(a, 0));
       }
-      if (cnt == 0) continue;
-      pk.m2l_loc_off.push_back(loff[l][nd]);
-      pk.m2l_rows.push_back(ri);
-      pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
+      if (!t.src.empty()) tg.push_back(std::move(t));
     }
   }
-  // leaves: near field, L2P
+  std::vector<std::vector<int>> codes(tg.size());
+#pragma omp parallel for schedule(dynamic, 16)
+  for (size_t i = 0; i < tg.size(); ++i) {
+    const NodePivots& pt = P.piv[tg[i].level][tg[i].node];
+    codes[i].resize(tg[i].src.size());
+    for (size_t e = 0; e < tg[i].src.size(); ++e) {
+      const NodePivots& ps = P.piv[tg[i].level][tg[i].src[e]];
+      double lo = INFINITY, hi = 0.0;
+      for (int32_t a : pt.ti)
+        for (int32_t c : ps.so) {
+          double dx = P.pts[2 * (size_t)a] - P.pts[2 * (size_t)c];
+          double dy = P.pts[2 * (size_t)a + 1] - P.pts[2 * (size_t)c + 1];
+          double r2 = dx * dx + dy * dy;
+          lo = std::min(lo, r2);
+          hi = std::max(hi, r2);
+        }
+      codes[i][e] = choose_band(P.kappa * std::sqrt(lo), P.kappa * std::sqrt(hi));
+    }
+  }
+  pk.m2l_src_ptr.push_back(0);
+  pk.m2l_item_ptr.push_back(0);
+  for (size_t i = 0; i < tg.size(); ++i) {
+    const int l = tg[i].level;
+    const int ri = (int)P.piv[l][tg[i].node].ti.size();
+    std::vector<int> order(tg[i].src.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return codes[i][a] < codes[i][b]; });
+    int prev = -1;
+    for (int e : order) {
+      int sn = tg[i].src[e];
+      int ro = (int)P.piv[l][sn].so.size();
+      int code = codes[i][e];
+      if (code != prev) {
+        if (prev >= 0) pk.m2l_item_end.push_back((int32_t)pk.m2l_src_off.size());
+        pk.m2l_item_code.push_back(code);
+        pk.m2l_item_begin.push_back((int32_t)pk.m2l_src_off.size());
+        prev = code;
+      }
+      pk.m2l_src_off.push_back(moff[l][sn]);
+      pk.m2l_src_cnt.push_back(ro);
+      pk.m2l_entries += (int64_t)ri * ro;
+      pk.m2l_band_entries[code] += (int64_t)ri * ro;
+      ++pk.m2l_pairs;
+    }
+    pk.m2l_item_end.push_back((int32_t)pk.m2l_src_off.size());
+    pk.m2l_item_ptr.push_back((int32_t)pk.m2l_item_code.size());
+    pk.m2l_loc_off.push_back(loff[l][tg[i].node]);
+    pk.m2l_rows.push_back(ri);
+    pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
+  }
+  // leaves: near field (own leaf first: the only segment with i == j pairs), L2P
+  auto bbox = [&](const Box& B, double* bb) {
+    bb[0] = bb[1] = INFINITY;
+    bb[2] = bb[3] = -INFINITY;
+    for (int32_t t = B.begin; t < B.end; ++t) {
+      int32_t o = P.perm[t];
+      bb[0] = std::min(bb[0], P.pts[2 * (size_t)o]);
+      bb[1] = std::min(bb[1], P.pts[2 * (size_t)o + 1]);
+      bb[2] = std::max(bb[2], P.pts[2 * (size_t)o]);
+      bb[3] = std::max(bb[3], P.pts[2 * (size_t)o + 1]);
+    }
+  };
+  std::vector<double> lbb(4 * leaf.boxes.size());
+  for (size_t b = 0; b < leaf.boxes.size(); ++b) bbox(leaf.boxes[b], &lbb[4 * b]);
   pk.near_ptr.push_back(0);
   pk.max_leaf = 0;
   for (size_t b = 0; b < leaf.boxes.size(); ++b) {
@@ -742,12 +802,25 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     pk.leaf_begin.push_back(B.begin);
     pk.leaf_end.push_back(B.end);
     pk.max_leaf = std::max(pk.max_leaf, B.end - B.begin);
-    for (int a : leaf.N[b]) {
+    std::vector<int> nb = leaf.N[b];
+    std::stable_partition(nb.begin(), nb.end(), [&](int a) { return a == (int)b; });
+    double zmax = 0.0;
+    int64_t pairs = 0;
+    for (int a : nb) {
       pk.near_begin.push_back(leaf.boxes[a].begin);
       pk.near_end.push_back(leaf.boxes[a].end);
-      pk.p2p_pairs += (int64_t)(B.end - B.begin) * (leaf.boxes[a].end - leaf.boxes[a].begin);
+      pairs += (int64_t)(B.end - B.begin) * (leaf.boxes[a].end - leaf.boxes[a].begin);
+      const double* p = &lbb[4 * b];
+      const double* q = &lbb[4 * (size_t)a];
+      double dx = std::max(p[2] - q[0], q[2] - p[0]);
+      double dy = std::max(p[3] - q[1], q[3] - p[1]);
+      zmax = std::max(zmax, P.kappa * std::sqrt(dx * dx + dy * dy));
     }
-    pk.p2p_pairs -= (B.end - B.begin);
+    pairs -= (B.end - B.begin);
+    pk.p2p_pairs += pairs;
+    int band = zmax <= dafmm_fit::Z_NEAR ? kBandNear : kBandGeneric;
+    pk.leaf_band.push_back(band);
+    pk.p2p_band_entries[band] += pairs;
     pk.near_ptr.push_back((int32_t)pk.near_begin.size());
     int nd = leaf.node_of[b];
     int ri = nd >= 0 ? (int)P.piv[L][nd].ti.size() : 0;

@@ -1,0 +1,105 @@
+"""CPU checks of the C-ABI library (no GPU, no compute calls on the device): it loads, exports
+every function include/dafmm.h declares, rejects bad arguments, and its host setup (tree,
+lists, cones, NCA pivots) agrees with the oracle's own construction."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle.core import Problem
+from oracle.nca import NCA
+from oracle.plan_io import compare_lists, load_plan, validate_pivots
+from oracle.tree import Lists, Tree
+from synth.configs import make_problem
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _prod():
+    import paper_2204_00326_b200 as prod
+    return prod
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "dafmm.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(?:int|void|const char\*)\s+(\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    prod = _prod()
+    lib = ctypes.CDLL(prod.library_path())
+    names = _declared()
+    assert "dafmm_create" in names and "ls_gmres_solve" in names and "dafmm_matvec" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    assert sorted(prod.EXPORTED) == names
+
+
+def _host_plan(P, tmp_path, **opts):
+    prod = _prod()
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], host_only=1, **opts)
+    op.export_plan(tmp_path / "plan")
+    stats = op.stats()
+    op.close()
+    return load_plan(tmp_path / "plan"), stats
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0)])
+def test_host_setup_matches_oracle_lists_and_pivots(name, n, kappa, tmp_path):
+    P = make_problem(name, n=n, kappa=kappa)
+    plan, stats = _host_plan(P, tmp_path)
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    compare_lists(plan, tree, lists)
+    piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv)
+    validate_pivots(nca, piv)
+    assert stats["p2p_pairs"] > 0 and stats["levels"] == tree.L
+    assert np.array_equal(np.sort(plan["perm"]), np.arange(P["points"].shape[0]))
+
+
+def test_host_setup_ragged_points(tmp_path):
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(-1, 1, size=(3000, 2))
+    P = dict(points=pts, weights=np.full(3000, 4.0 / 3000), q=np.ones(3000), kappa=12.0, nca_tol=1e-8)
+    plan, _ = _host_plan(P, tmp_path)
+    tree = Tree(pts, P["weights"], 12.0, 64)
+    compare_lists(plan, tree, Lists(tree))
+
+
+@pytest.mark.parametrize("bad", ["kappa", "tol", "dup", "nan", "weight", "leaf"])
+def test_invalid_arguments_rejected(bad):
+    prod = _prod()
+    P = make_problem("c1", n=16)
+    pts, w, q, kappa, tol, leaf = P["points"].copy(), P["weights"].copy(), P["q"].copy(), 5.0, 1e-8, 64
+    if bad == "kappa":
+        kappa = -1.0
+    elif bad == "tol":
+        tol = 1.5
+    elif bad == "dup":
+        pts[3] = pts[2]
+    elif bad == "nan":
+        q[5] = np.nan
+    elif bad == "weight":
+        w[0] = 0.0
+    elif bad == "leaf":
+        leaf = 0
+    with pytest.raises(prod.DAFMMError) as e:
+        prod.DAFMM(pts, w, q, kappa, leaf, tol, host_only=1)
+    assert e.value.code == -1
+    assert prod.dafmm_last_error() != ""
+
+
+def test_host_only_plan_refuses_device_calls():
+    prod = _prod()
+    P = make_problem("c1", n=16)
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1e-8, host_only=1)
+    with pytest.raises(prod.DAFMMError):
+        prod.dafmm_matvec(op.h, 1, 2)
+    with pytest.raises(prod.DAFMMError):
+        op.set_profiling(True)
+    op.close()

@@ -3,32 +3,50 @@
 
 PRODUCT TOOLING (not the oracle; the oracle evaluates H0 by its own series / Miller /
 asymptotic bands and never reads this header).  Fits are Chebyshev interpolants computed in
-40-digit arithmetic with mpmath, converted to monomial form in a scaled variable and checked
-in fp64 Horner arithmetic against mpmath before being written.
+multi-digit arithmetic with mpmath, converted to monomial form and checked in fp64 Horner
+arithmetic against mpmath before being written.
 
-Bands:
-  near  z <  Z_NEAR:  H0 = J0(u) + i [ (1/pi) ln(u) J0(u) + R(u) ],  u = z^2/4,
-        J0 and R (the regular part of Y0) as polynomials in t = u / U_MAX * 2 - 1.
-  far   z >= Z_FAR:   H0 = sqrt(2/(pi z)) (P + i Q) e^{i (z - pi/4)},
-        P(s), Qt(s) polynomials in v = 2 s - 1, s = (Z_FAR / z)^2, Q = Qt * Z_FAR / z.
-  sincos on |rho| <= pi/4: sin(rho)/rho and cos(rho) as polynomials in rho^2.
+All evaluators take z2 = (kappa r)^2 (the kernels store kappa-scaled coordinates).
+
+  near-type band Zn (z <= Zn), code:   H0 = J0 + i [ (1/pi) ln(u) J0 + R ],  u = z2/4,
+        J0 and R (the regular part of Y0) polynomials in t = 2u/U - 1, U = Zn^2/4.
+  far-type band, z in [zlo, zhi]:   H0 = sqrt(2/(pi z)) (P + i Q) e^{i (z - pi/4)},
+        P, Q polynomials in x = A s + B, s = 1/z mapped from [1/zhi, 1/zlo] onto [-1, 1].
+        One band is emitted as code (the generic far band [8, inf)); the rest are a data
+        table the kernels copy into shared memory per work segment.
+  sincos on |rho| <= pi/4: sin(rho)/rho and cos(rho) polynomials in rho^2 (code).
+  ln u = e ln2 + ln c_i + log1p(m/c_i - 1), u = 2^e m, with a 2^7-entry table (rcp_i, ln c_i)
+        indexed by the top mantissa bits (data) and a degree-9 log1p (code).
+
+Polynomials emitted as code are lane-blocked Horner evaluators with literal coefficients: on
+sm_100a each literal is a uniform-register immediate shared by the TB lanes of a block.
 """
+import math
 import os
 import sys
 
 import mpmath as mp
 import numpy as np
 
-mp.mp.dps = 45
-Z_NEAR = 8.0
-U_MAX = Z_NEAR * Z_NEAR / 4.0
-Z_FAR = 8.0
+mp.mp.dps = 32
+NEAR_BANDS = [8.0, 12.0]            # near-type bands z <= Zn (code)
+GENERIC_FAR = (8.0, float("inf"))   # far-type band emitted as code (generic per-lane path)
+TOL_FAR = 3.0e-16                   # max abs error of P, Q (|P| ~ 1)
+TOL_NEAR = 3.2e-15                  # max abs error of J0, R
 
 
-def cheb_coeffs(f, deg, a, b):
+def far_menu():
+    """Far-type data bands: ratio-2 and ratio-4 bands on a sqrt(2) grid from 2.5, and tails."""
+    g = [2.5 * math.sqrt(2.0) ** k for k in range(13)]
+    bands = [(a, 2 * a) for a in g] + [(a, 4 * a) for a in g[:11]]
+    bands += [(a, float("inf")) for a in (16.0, 32.0, 64.0, 128.0, 256.0)]
+    return bands
+
+
+def cheb_coeffs(f, deg):
     n = deg + 1
     nodes = [mp.cos(mp.pi * (k + mp.mpf(1) / 2) / n) for k in range(n)]
-    vals = [f(mp.mpf(a) + (mp.mpf(b) - a) * (x + 1) / 2) for x in nodes]
+    vals = [f(x) for x in nodes]
     c = []
     for j in range(n):
         s = mp.fsum(vals[k] * mp.cos(mp.pi * j * (k + mp.mpf(1) / 2) / n) for k in range(n))
@@ -37,8 +55,8 @@ def cheb_coeffs(f, deg, a, b):
     return c
 
 
-def cheb_to_monomial(c):
-    """Chebyshev series on [-1,1] -> monomial coefficients (ascending)."""
+def cheb_to_monomial(c, a=1, b=0):
+    """Chebyshev series in w on [-1,1] -> monomial coefficients (ascending) in y, w = a y + b."""
     n = len(c)
     T = [[mp.mpf(0)] * n for _ in range(n)]
     T[0][0] = mp.mpf(1)
@@ -47,13 +65,18 @@ def cheb_to_monomial(c):
     for k in range(2, n):
         for j in range(n):
             T[k][j] = (2 * T[k - 1][j - 1] if j > 0 else 0) - T[k - 2][j]
-    return [mp.fsum(c[k] * T[k][j] for k in range(n)) for j in range(n)]
+    mono_w = [mp.fsum(c[k] * T[k][j] for k in range(n)) for j in range(n)]
+    out = [mp.mpf(0)] * n
+    for j, cw in enumerate(mono_w):
+        for i in range(j + 1):
+            out[i] += cw * mp.binomial(j, i) * mp.mpf(a) ** i * mp.mpf(b) ** (j - i)
+    return out
 
 
 def horner(coef, x):
     acc = np.float64(coef[-1])
     for a in reversed(coef[:-1]):
-        acc = acc * x + np.float64(a)
+        acc = np.float64(acc * np.float64(x) + np.float64(a))
     return acc
 
 
@@ -62,8 +85,9 @@ def j0_of_u(u):
 
 
 def r_of_u(u):
+    """Regular part of Y0: Y0 - (1/pi) ln(u) J0 with u = z^2/4 (limit 2 gamma / pi at 0)."""
     if u == 0:
-        return 2 / mp.pi * mp.euler
+        return 2 * mp.euler / mp.pi
     z = 2 * mp.sqrt(u)
     return mp.bessely(0, z) - (1 / mp.pi) * mp.log(u) * mp.besselj(0, z)
 
@@ -73,107 +97,195 @@ def pq(z):
     return h.real, h.imag
 
 
-def fit_near(deg):
-    cj = cheb_to_monomial(cheb_coeffs(lambda t: j0_of_u((t + 1) / 2 * U_MAX), deg, -1, 1))
-    cr = cheb_to_monomial(cheb_coeffs(lambda t: r_of_u((t + 1) / 2 * U_MAX), deg, -1, 1))
-    return cj, cr
+def fit_near(zn):
+    U = zn * zn / 4
+    for deg in range(12, 30):
+        cj = cheb_to_monomial(cheb_coeffs(lambda t: j0_of_u((t + 1) / 2 * U), deg))
+        cr = cheb_to_monomial(cheb_coeffs(lambda t: r_of_u((t + 1) / 2 * U), deg))
+        err = 0.0
+        for u in np.linspace(0, U, 241):
+            t = np.float64(u / U * 2 - 1)
+            err = max(err, abs(horner(cj, t) - float(j0_of_u(mp.mpf(u)))),
+                      abs(horner(cr, t) - float(r_of_u(mp.mpf(u)))))
+        if err < TOL_NEAR:
+            print("near z <= %g: degree %d, max abs err %.2e" % (zn, deg, err), file=sys.stderr)
+            return cj, cr, deg, err
+    raise RuntimeError("near fit failed")
 
 
-def fit_far(deg):
-    def fp(v):
-        s = (v + 1) / 2
-        return pq(Z_FAR / mp.sqrt(s))[0] if s > 0 else mp.mpf(1)
-
-    def fq(v):
-        s = (v + 1) / 2
-        if s == 0:
-            return mp.mpf(-1) / (8 * Z_FAR)
-        z = Z_FAR / mp.sqrt(s)
-        return pq(z)[1] * z / Z_FAR
-
-    return (cheb_to_monomial(cheb_coeffs(fp, deg, -1, 1)), cheb_to_monomial(cheb_coeffs(fq, deg, -1, 1)))
+def band_map(zlo, zhi):
+    slo = mp.mpf(0) if zhi == float("inf") else mp.mpf(1) / zhi
+    shi = mp.mpf(1) / zlo
+    return slo, shi, 2 / (shi - slo), -(shi + slo) / (shi - slo)
 
 
-def fit_sincos(deg):
+def fit_far(zlo, zhi, start=4):
+    slo, shi, A, B = band_map(zlo, zhi)
+
+    def s_of(x):
+        return slo + (shi - slo) * (x + 1) / 2
+
+    def fp(x):
+        return pq(1 / s_of(x))[0] if s_of(x) > 0 else mp.mpf(1)
+
+    def fq(x):
+        return pq(1 / s_of(x))[1] if s_of(x) > 0 else mp.mpf(0)
+
+    checks = [mp.mpf(x) for x in np.linspace(-1, 1, 121)]
+    ref = [pq(1 / s_of(x)) if s_of(x) > 0 else (mp.mpf(1), mp.mpf(0)) for x in checks]
+    for deg in range(start, 34):
+        cp = cheb_to_monomial(cheb_coeffs(fp, deg))
+        cq = cheb_to_monomial(cheb_coeffs(fq, deg))
+        err = 0.0
+        for x, (P, Q) in zip(checks, ref):
+            err = max(err, abs(horner(cp, float(x)) - float(P)), abs(horner(cq, float(x)) - float(Q)))
+        if err < TOL_FAR:
+            print("far band [%g, %g]: degree %d, max abs err %.2e" % (zlo, zhi, deg, err), file=sys.stderr)
+            return cp, cq, deg, err, float(A), float(B)
+    raise RuntimeError("far fit failed for [%g, %g]" % (zlo, zhi))
+
+
+def fit_sincos():
     r2max = (mp.pi / 4) ** 2
-    fs = lambda v: (mp.sin(mp.sqrt((v + 1) / 2 * r2max)) / mp.sqrt((v + 1) / 2 * r2max)) if v > -1 else mp.mpf(1)
-    fc = lambda v: mp.cos(mp.sqrt((v + 1) / 2 * r2max))
-    return cheb_to_monomial(cheb_coeffs(fs, deg, -1, 1)), cheb_to_monomial(cheb_coeffs(fc, deg, -1, 1)), r2max
-
-
-def emit(name, coef):
-    """An inline Horner evaluator with the coefficients as literals (folded into DFMA operands)."""
-    expr = "%.17e" % float(coef[-1])
-    for a in reversed(coef[:-1]):
-        expr = "fma(%s, x, %.17e)" % (expr, float(a))
-    return "DAFMM_HD double %s(double x) {\n  return %s;\n}\n" % (name, expr)
+    for deg in range(5, 14):
+        fs = lambda w: (mp.sin(mp.sqrt((w + 1) / 2 * r2max)) / mp.sqrt((w + 1) / 2 * r2max)) if w > -1 else mp.mpf(1)
+        fc = lambda w: mp.cos(mp.sqrt((w + 1) / 2 * r2max))
+        a, b = 2 / r2max, -1  # w = 2 rho^2 / r2max - 1  ->  monomials in rho^2
+        cs = cheb_to_monomial(cheb_coeffs(fs, deg), a, b)
+        cc = cheb_to_monomial(cheb_coeffs(fc, deg), a, b)
+        err = 0.0
+        for rho in np.linspace(-float(mp.pi / 4), float(mp.pi / 4), 513):
+            r2 = np.float64(rho * rho)
+            err = max(err, abs(rho * horner(cs, r2) - np.sin(rho)), abs(horner(cc, r2) - np.cos(rho)))
+        if err < 2.3e-16:
+            print("sincos: degree %d, max abs err %.2e" % (deg, err), file=sys.stderr)
+            return cs, cc, deg, err
+    raise RuntimeError("sincos fit failed")
 
 
 def cody_waite():
-    """pi/2 split into C1 (33 significant bits), C2 (33 bits), C3 (53 bits)."""
+    """pi/2 = C1 + C2 (+ C3): C1 with 33 significant bits (m C1 exact for m < 2^20), C2 the
+    rounded remainder; C3 (< 1e-20) is below the fp64 resolution of rho for z < 1e4."""
     half_pi = mp.pi / 2
+
     def trunc(x, bits):
         e = int(mp.floor(mp.log(abs(x), 2)))
         scale = mp.mpf(2) ** (bits - 1 - e)
         return mp.floor(x * scale) / scale
     c1 = trunc(half_pi, 33)
-    c2 = trunc(half_pi - c1, 33)
-    c3 = half_pi - c1 - c2
-    return float(c1), float(c2), float(c3)
+    return float(c1), float(half_pi - c1)
+
+
+def log_table(bits=7):
+    """(rcp_i, ln c_i) with rcp_i = fp64(1 / (1 + (i + 1/2) / 2^bits)) and ln c_i = -ln(rcp_i)
+    exactly for the stored rcp_i, so ln(m) = log1p(m rcp_i - 1) + ln c_i is an identity."""
+    out = []
+    for i in range(1 << bits):
+        rcp = float(1 / (1 + (mp.mpf(i) + mp.mpf(1) / 2) / (1 << bits)))
+        out.append((rcp, float(-mp.log(mp.mpf(rcp)))))
+    return out
+
+
+def log1p_coeffs():
+    """log1p(r) = r + r^2 q(r), q(r) = sum_{k>=0} (-1)^(k+1) r^k / (k+2), split into even and odd
+    parts q = qe(r^2) + r qo(r^2) (degree 9 overall: |r| <= 2^-8 leaves a relative tail < 1e-20)."""
+    q = [mp.mpf((-1) ** (k + 1)) / (k + 2) for k in range(8)]
+    return q[0::2], q[1::2]
+
+
+def h2_function(name, ca, cb, doc, template="template <int TB>", prefix="DAFMM_HD void"):
+    """A lane-blocked pair-Horner evaluator with literal coefficients:
+    a[i] = sum_k ca[k] x[i]^k, b[i] = sum_k cb[k] x[i]^k for i < TB."""
+    n = max(len(ca), len(cb))
+    ca = [float(v) for v in ca] + [0.0] * (n - len(ca))
+    cb = [float(v) for v in cb] + [0.0] * (n - len(cb))
+    out = ["// %s" % doc, template, "%s %s(const double* x, double* a, double* b) {" % (prefix, name),
+           "  DAFMM_H2_INIT(%.17e, %.17e)" % (ca[-1], cb[-1])]
+    for k in range(n - 2, -1, -1):
+        out.append("  DAFMM_H2_STEP(%.17e, %.17e)" % (ca[k], cb[k]))
+    out.append("}")
+    return "\n".join(out)
 
 
 def main(out_path):
-    # --- near band ---
-    for deg in range(12, 26):
-        cj, cr = fit_near(deg)
-        err = 0.0
-        for u in np.linspace(0, U_MAX, 257):
-            t = np.float64(u / U_MAX * 2 - 1)
-            ej = abs(horner(cj, t) - float(j0_of_u(mp.mpf(u))))
-            er = abs(horner(cr, t) - float(r_of_u(mp.mpf(u))))
-            err = max(err, ej, er)
-        print("near deg", deg, "max abs err", err, file=sys.stderr)
-        if err < 4e-16 * 8:
-            break
-    near_deg, near_err = deg, err
-    # --- far band ---
-    for deg in range(8, 30):
-        cp, cq = fit_far(deg)
-        err = 0.0
-        for s in np.linspace(0, 1, 257):
-            v = np.float64(2 * s - 1)
-            if s == 0:
-                continue
-            z = Z_FAR / mp.sqrt(mp.mpf(s))
-            P, Q = pq(z)
-            err = max(err, abs(horner(cp, v) - float(P)), abs(horner(cq, v) - float(Q * z / Z_FAR)))
-        print("far deg", deg, "max abs err", err, file=sys.stderr)
-        if err < 3e-16:
-            break
-    far_deg, far_err = deg, err
-    for deg in range(5, 14):
-        cs, cc, r2max = fit_sincos(deg)
-        err = 0.0
-        for rho in np.linspace(-float(mp.pi / 4), float(mp.pi / 4), 513):
-            v = np.float64(rho * rho / float(r2max) * 2 - 1)
-            err = max(err, abs(rho * horner(cs, v) - np.sin(rho)), abs(horner(cc, v) - np.cos(rho)))
-        print("sincos deg", deg, "max abs err", err, file=sys.stderr)
-        if err < 2.3e-16:
-            break
+    nears = [fit_near(zn) for zn in NEAR_BANDS]
+    gfar = fit_far(*GENERIC_FAR)
+    menu = far_menu()
+    fars = [fit_far(zlo, zhi) for zlo, zhi in menu]
+    cs, cc, sc_deg, sc_err = fit_sincos()
+    c1, c2 = cody_waite()
+    qe, qo = log1p_coeffs()
+    lt = log_table()
+    maxn = max(f[2] for f in fars) + 1
+    L = []
+    w = L.append
+    w("// GENERATED by tools/fit_hankel.py — do not edit.  Product-side H0^(1) fits (DESIGN.md §6).")
+    for zn, f in zip(NEAR_BANDS, nears):
+        w("// near band z <= %g: degree %d, fp64 Horner max abs err %.2e" % (zn, f[2], f[3]))
+    w("// generic far band [%g, inf): degree %d, %.2e;  sincos degree %d, %.2e" % (GENERIC_FAR[0], gfar[2], gfar[3],
+                                                                                  sc_deg, sc_err))
+    w("// %d far-type data bands, degrees %d..%d, max abs err <= %.1e" % (len(fars), min(f[2] for f in fars),
+                                                                         max(f[2] for f in fars), TOL_FAR))
+    w("#pragma once")
+    w('#include "common.h"')
+    w("#define DAFMM_H2_INIT(ca, cb)                 \\")
+    w("  _Pragma(\"unroll\") for (int i = 0; i < TB; ++i) { \\")
+    w("    a[i] = ca;                                \\")
+    w("    b[i] = cb;                                \\")
+    w("  }")
+    w("#define DAFMM_H2_STEP(ca, cb)                 \\")
+    w("  _Pragma(\"unroll\") for (int i = 0; i < TB; ++i) { \\")
+    w("    a[i] = fma(a[i], x[i], ca);               \\")
+    w("    b[i] = fma(b[i], x[i], cb);               \\")
+    w("  }")
+    w("namespace dafmm_fit {")
+    w("constexpr double INV_PI = %.17e;" % float(1 / mp.pi))
+    w("constexpr double TWO_OVER_PI = %.17e;" % float(2 / mp.pi))
+    w("constexpr double SQRT_2_OVER_PI = %.17e;" % float(mp.sqrt(2 / mp.pi)))
+    w("constexpr double LN2 = %.17e;" % float(mp.log(2)))
+    w("constexpr double PIO2_1 = %.17e;\nconstexpr double PIO2_2 = %.17e;" % (c1, c2))
+    w("constexpr int LOG_BITS = 7;")
+    w("struct alignas(16) Pair {\n  double a, b;\n};")
+    w("// near-type bands: NearJR<Zn>::eval evaluates (J0, R) at t = z2 * T_SCALE - 1")
+    w("template <int ZN>\nstruct NearJR;")
+    for zn, f in zip(NEAR_BANDS, nears):
+        U = zn * zn / 4
+        body = h2_function("eval", f[0], f[1], "(J0, R) in t = 2u/U - 1, U = %g (degree %d)" % (U, f[2]),
+                           template="template <int TB>", prefix="static DAFMM_HD void")
+        w("template <>\nstruct NearJR<%d> {\n  static constexpr double Z2_MAX = %.17g;  // z^2 <= Z2_MAX\n"
+          "  static constexpr double T_SCALE = %.17g;  // t = z2 * T_SCALE - 1 = 2 (z2/4) / U - 1\n%s\n};"
+          % (int(zn), zn * zn, 0.5 / U, body))
+    w(h2_function("generic_far_pq", gfar[0], gfar[1],
+                  "(P, Q) of the generic far band [%g, inf) in x = A/z + B (degree %d)" % (GENERIC_FAR[0], gfar[2])))
+    w("constexpr double GENERIC_FAR_ZLO = %.17g;" % GENERIC_FAR[0])
+    w("constexpr double GENERIC_FAR_A = %.17e, GENERIC_FAR_B = %.17e;" % (gfar[4], gfar[5]))
+    w(h2_function("sincos_poly", cs, cc, "(sin(rho)/rho, cos(rho)) in rho^2 (degree %d)" % sc_deg))
+    w(h2_function("log1p_poly", qe, qo, "(qe, qo) in r^2: log1p(r) = r + r^2 (qe + r qo)"))
+    w("// far-type data bands: x = A / z + B; pq[k] = (P_k, Q_k), k < n")
+    w("constexpr int NUM_FAR = %d;" % len(fars))
+    w("constexpr int FAR_MAXN = %d;" % maxn)
+    w("struct FarBand {\n  double zlo, zhi, A, B;\n  int n, pad;\n  Pair pq[FAR_MAXN];\n};")
+    rows = []
+    for (zlo, zhi), f in zip(menu, fars):
+        n = f[2] + 1
+        pqs = ", ".join("{%.17e, %.17e}" % (float(a), float(b)) for a, b in zip(f[0], f[1]))
+        pqs += "".join(", {0.0, 0.0}" for _ in range(maxn - n))
+        rows.append("{%.17g, %s, %.17e, %.17e, %d, 0, {%s}}" % (zlo, "1e308" if zhi == float("inf") else
+                                                                "%.17g" % zhi, f[4], f[5], n, pqs))
+    init = "{\n" + ",\n".join(rows) + "}"
+    w("#if defined(__CUDACC__)")
+    w("static __constant__ FarBand kFarBandsDev[NUM_FAR] = %s;" % init)
+    w("#endif")
+    w("static const FarBand kFarBandsHost[NUM_FAR] = %s;" % init)
+    w("// log table (rcp_i, ln c_i), i = top LOG_BITS mantissa bits")
+    init = "{" + ", ".join("{%.17e, %.17e}" % t for t in lt) + "}"
+    w("#if defined(__CUDACC__)")
+    w("static __constant__ Pair kLogTabDev[1 << LOG_BITS] = %s;" % init)
+    w("#endif")
+    w("static const Pair kLogTabHost[1 << LOG_BITS] = %s;" % init)
+    w("}  // namespace dafmm_fit")
     with open(out_path, "w") as f:
-        f.write("// GENERATED by tools/fit_hankel.py — do not edit.  Product-side H0^(1) fits\n")
-        f.write("// (near band: fp64 Horner max abs err %.2e at degree %d; far band %.2e at degree %d).\n"
-                % (near_err, near_deg, far_err, far_deg))
-        f.write("#pragma once\n#include \"common.h\"\nnamespace dafmm_fit {\n")
-        f.write("static constexpr double Z_NEAR = %.17g;\nstatic constexpr double U_MAX = %.17g;\n" % (Z_NEAR, U_MAX))
-        f.write("static constexpr double Z_FAR = %.17g;\nstatic constexpr double SC_R2MAX = %.17e;\n"
-                % (Z_FAR, float(r2max)))
-        c1, c2, c3 = cody_waite()
-        f.write("static constexpr double PIO2_1 = %.17e;\nstatic constexpr double PIO2_2 = %.17e;\n"
-                "static constexpr double PIO2_3 = %.17e;\n" % (c1, c2, c3))
-        f.write(emit("near_j0", cj) + emit("near_r", cr) + emit("far_p", cp) + emit("far_q", cq))
-        f.write(emit("sin_over_x", cs) + emit("cos_poly", cc))
-        f.write("}  // namespace dafmm_fit\n")
+        f.write("\n".join(L) + "\n")
 
 
 if __name__ == "__main__":
