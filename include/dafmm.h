@@ -80,8 +80,8 @@ typedef struct {
   int32_t max_rank;
   double setup_tree_s, setup_lists_s, setup_nca_s, setup_ops_s, setup_pack_s, setup_upload_s;
   int64_t aca_entries;       /* kernel entries evaluated by ACA during setup */
-  int64_t m2l_band_entries[16]; /* M2L entries per H0 band code (0 generic, 1 near, 2+b far band b) */
-  int64_t p2p_band_entries[16]; /* P2P point pairs per band code */
+  int64_t m2l_band_entries[48]; /* M2L entries per H0 band code (hankel.cuh: 0 generic, 1 near z<=8, 2 near z<=12, 3+b data band b) */
+  int64_t p2p_band_entries[48]; /* P2P point pairs per band code */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);
@@ -132,17 +132,21 @@ int dafmm_set_stream(dafmm_handle h, void* stream);
 int dafmm_stats(dafmm_handle h, dafmm_stats_t* out);
 
 /* Per-pass profiling (SURVEY §5 "CUDA events per pass").  dafmm_set_profiling(h, 1) creates
- * CUDA events on the handle's stream around each pass of every later matvec and resets the
- * accumulators and the kernel-launch counter; 0 switches event recording off (the counter
- * keeps counting).  dafmm_pass_times synchronises on the last profiled matvec and writes the
- * accumulated milliseconds per pass into ms_out[DAFMM_NUM_PASSES], in the order
+ * CUDA events around each pass of every later matvec and resets the accumulators and the
+ * kernel-launch counter; 0 switches event recording off (the counter keeps counting).
+ * dafmm_pass_times synchronises on the last profiled matvec and writes the accumulated
+ * milliseconds per pass into ms_out[DAFMM_NUM_PASSES], in the order
  *   0 gather (caller order -> tree order, w scaling)
- *   1 P2M     2 M2M, all levels     3 M2L, all levels
- *   4 L2L, all levels     5 near field P2P + L2P + combine + scatter
+ *   1 P2M (plus the memsets of the expansion buffers)
+ *   2 M2M, all levels     3 M2L, all levels     4 L2L, all levels
+ *   5 near field P2P (on the handle's internal side stream, concurrent with 1-4)
+ *   6 combine: L2P + identity + self term + scatter
+ *   7 span of the concurrent part: from the fork after the gather to the later of 4 and 5
  * plus the number of profiled matvecs and the number of kernels launched by the library since
- * the last reset (either pointer may be NULL).  The memsets of the expansion buffers fall in
- * pass 0.  Errors: DAFMM_EINVAL (null handle / host-only plan), DAFMM_ECUDA. */
-#define DAFMM_NUM_PASSES 6
+ * the last reset (either pointer may be NULL).  Passes 1-4 and 5 overlap in time, so their sum
+ * exceeds the matvec time; 0 + 7 + 6 is the matvec time.  Errors: DAFMM_EINVAL (null handle /
+ * host-only plan), DAFMM_ECUDA. */
+#define DAFMM_NUM_PASSES 8
 int dafmm_set_profiling(dafmm_handle h, int enable);
 int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64_t* launches_out);
 

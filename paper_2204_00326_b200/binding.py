@@ -16,8 +16,8 @@ EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_m
             "dafmm_matvec_host", "ls_gmres_solve", "dafmm_set_stream", "dafmm_stats", "dafmm_export_plan",
             "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times"]
 
-NUM_PASSES = 6
-PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near"]
+NUM_PASSES = 8
+PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near", "combine", "overlap_span"]
 
 DAFMM_OK, DAFMM_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "DAFMM_EINVAL", -2: "DAFMM_ECUDA", -3: "DAFMM_ENOMEM", -4: "DAFMM_ESETUP"}
@@ -43,8 +43,8 @@ class Stats(ctypes.Structure):
                 ("setup_tree_s", ctypes.c_double), ("setup_lists_s", ctypes.c_double),
                 ("setup_nca_s", ctypes.c_double), ("setup_ops_s", ctypes.c_double),
                 ("setup_pack_s", ctypes.c_double), ("setup_upload_s", ctypes.c_double),
-                ("aca_entries", ctypes.c_int64), ("m2l_band_entries", ctypes.c_int64 * 16),
-                ("p2p_band_entries", ctypes.c_int64 * 16)]
+                ("aca_entries", ctypes.c_int64), ("m2l_band_entries", ctypes.c_int64 * 48),
+                ("p2p_band_entries", ctypes.c_int64 * 48)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

@@ -208,8 +208,8 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->setup_pack_s = P.t_pack;
   out->setup_upload_s = P.t_upload;
   out->aca_entries = P.aca_entries;
-  for (size_t b = 0; b < h->m2l_band.size() && b < 16; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
-  for (size_t b = 0; b < h->p2p_band.size() && b < 16; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
+  for (size_t b = 0; b < h->m2l_band.size() && b < 48; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
+  for (size_t b = 0; b < h->p2p_band.size() && b < 48; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
   return DAFMM_OK;
 }
 

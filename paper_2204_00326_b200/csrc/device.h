@@ -10,7 +10,10 @@
 namespace dafmm {
 
 // Passes timed by the profiler, in launch order (DAFMM_PASS_* of dafmm.h).
-constexpr int kNumPasses = 6;  // gather, p2m, m2m, m2l, l2l, near (P2P + L2P + combine)
+// gather, p2m, m2m, m2l, l2l, near (P2P, side stream), combine (L2P + identity + scatter), and the
+// span of the concurrent part (from the fork to the later of P2P and L2L)
+constexpr int kNumPasses = 8;
+enum ProfEvent { EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_NEAR0, EV_NEAR1, EV_JOIN, EV_END, EV_COUNT };
 
 struct DevBatch {
   int items = 0;
@@ -25,17 +28,18 @@ struct DevBatch {
 struct DevPlan {
   int64_t n = 0;
   int kernel_mode = 0;
-  KernelConsts kc{};
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // the caller's stream (dafmm_set_stream)
+  cudaStream_t side = nullptr;     // internal stream: P2P runs here, concurrent with the far field
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // per tree point
-  double2* pts_t = nullptr;
+  double2* pts_t = nullptr;  // kappa-scaled coordinates
   double* w_t = nullptr;
   double* qk2_t = nullptr;
   double2* D_t = nullptr;
   int32_t* perm = nullptr;
   // expansions and pivots
   int64_t n_mult = 0, n_loc = 0;
-  double2* so_xy = nullptr;
+  double2* so_xy = nullptr;  // kappa-scaled pivot coordinates
   double2* ti_xy = nullptr;
   double2* ops = nullptr;
   int64_t ops_len = 0;
@@ -43,11 +47,12 @@ struct DevPlan {
   std::vector<DevBatch> m2m, l2l;
   // M2L
   int m2l_targets = 0;
+  int m2l_grid = 1;               // persistent CTAs (SMs x resident CTAs per SM)
+  int* m2l_ticket = nullptr;      // work counter, reset per matvec
   int64_t* m2l_loc_off = nullptr;
   int32_t* m2l_rows = nullptr;
-  int32_t* m2l_src_ptr = nullptr;
-  int64_t* m2l_src_off = nullptr;
-  int32_t* m2l_src_cnt = nullptr;
+  int64_t* m2l_stream_ptr = nullptr;  // per target: its source stream in m2l_stream_idx
+  int32_t* m2l_stream_idx = nullptr;  // multipole slot of every source pivot, target by target
   int32_t* m2l_item_ptr = nullptr;
   int32_t* m2l_item_code = nullptr;
   int32_t* m2l_item_begin = nullptr;
@@ -66,6 +71,7 @@ struct DevPlan {
   // scratch
   double2* x_t = nullptr;
   double2* v_t = nullptr;
+  double2* phi = nullptr;          // P2P result (H0 units, tree order)
   double2* mult = nullptr;
   double2* loc = nullptr;
   double2* host_stage = nullptr;  // device vectors for dafmm_matvec_host (x, y)
@@ -84,7 +90,7 @@ struct DevPlan {
   int64_t launches = 0;          // kernels launched by run_matvec / run_gmres since the last reset
   bool prof = false;
   bool prof_pending = false;     // events of the last profiled matvec not yet harvested
-  cudaEvent_t prof_ev[kNumPasses + 1] = {};
+  cudaEvent_t prof_ev[EV_COUNT] = {};
   double prof_ms[kNumPasses] = {};
   int64_t prof_count = 0;        // profiled matvecs harvested
 };

@@ -1,20 +1,23 @@
 // H0^(1)(z) = J0(z) + i Y0(z) for the product (host setup and device kernels share this code).
 //
 // The paper only names the kernel G_k(x,y) = (i/4) H0^(1)(k|x-y|).  This is
-// the product's own evaluator (DESIGN.md §H0), independent of the oracle's series / Miller /
-// asymptotic bands.  Every entry point takes the squared distance r2 = |x - y|^2.
+// the product's own evaluator (DESIGN.md §6), independent of the oracle's series / Miller /
+// asymptotic bands.  Every entry point takes z2 = (kappa |x - y|)^2: the kernels store
+// kappa-scaled coordinates, so no per-entry multiplication by kappa is needed.
 //
-//   near band, z <= 8:  J0 = pJ(t), Y0 = (1/pi) ln(u) J0 + pR(t),  u = z^2/4, t = u/8 - 1
-//   far-type band b, z in [ZLO_b, ZHI_b]:
-//       H0 = sqrt(2/(pi z)) (P_b(x) + i Q_b(x)) e^{i(z - pi/4)},  x = A_b / z + B_b
-//   generic (any z > 0): per-lane choice of the near band or far band 0 ([8, inf)).
+//   near-type band Zn in {8, 12} (z <= Zn):
+//       J0 = pJ(t), Y0 = (1/pi) ln(z2/4) J0 + pR(t),  t = z2 T_SCALE - 1        (code)
+//   far-type band [zlo, zhi]:
+//       H0 = sqrt(2/(pi z)) (P(x) + i Q(x)) e^{i(z - pi/4)},  x = A/z + B
+//       generic band [8, inf) as code; 29 narrower bands as data (FarBand, shared memory)
+//   generic (any z > 0): per-lane choice of near band 8 or the generic far band.
 //
 // Evaluators are lane-blocked: one call evaluates TB independent entries in lockstep, so each
-// literal coefficient (one uniform-register immediate) is shared by TB FMAs and the TB Horner
-// chains hide each other's latency.  Kernels pick one band per CTA-uniform work segment (setup
-// classifies every interaction by the exact [z_min, z_max] of its point pairs, DESIGN.md
-// §Kernels), so the band is a template parameter and inner loops never diverge.  ln u uses a
-// 128-entry table of (1/c_i, ln c_i): device callers pass its shared-memory copy
+// coefficient (a uniform-register immediate, or one broadcast shared-memory load for data
+// bands) is shared by TB FMAs and the TB Horner chains hide each other's latency.  Kernels
+// pick one band per CTA-uniform work segment (setup classifies every interaction by the exact
+// [z_min, z_max] of its point pairs), so the band never diverges inside a warp.
+// ln u uses a 128-entry table of (1/c_i, ln c_i): device callers pass its shared-memory copy
 // (load_log_table), host callers kLogTabHost.
 #pragma once
 #include "common.h"
@@ -23,38 +26,30 @@
 namespace dafmm {
 
 constexpr double kPi = 3.14159265358979323846;
+constexpr double kZ2Safe = 4.0;  // a z^2 inside every band's domain (z = 2), for masked lanes
 
+using dafmm_fit::FarBand;
 using dafmm_fit::Pair;
 
-struct KernelConsts {
-  double kappa;       // wavenumber
-  double inv_kappa;   // 1 / kappa
-  double quarter_k2;  // kappa^2 / 4   (u = z^2 / 4 = quarter_k2 * r2)
-  double amp_k;       // sqrt(2 / (pi kappa))
-  double r2_safe;     // a squared distance inside every band's domain (u = 1), for masked lanes
-};
-
-inline KernelConsts make_kernel_consts(double kappa) {
-  return {kappa, 1.0 / kappa, 0.25 * kappa * kappa, std::sqrt(2.0 / (kPi * kappa)), 4.0 / (kappa * kappa)};
-}
-
-// Band codes of a work segment: 0 generic, 1 near, 2 + b far-type band b.
+// Band codes of a work segment: 0 generic, 1 near z <= 8, 2 near z <= 12, 3 + b data band b.
 constexpr int kBandGeneric = 0;
-constexpr int kBandNear = 1;
-constexpr int kNumBandCodes = 2 + dafmm_fit::NUM_FAR;
+constexpr int kBandNear8 = 1;
+constexpr int kBandNear12 = 2;
+constexpr int kBandFarData = 3;
+constexpr int kNumBandCodes = kBandFarData + dafmm_fit::NUM_FAR;
 
-// ln u for TB positive normal u.
+// ln(z2 / 4) for TB positive normal z2.
 template <int TB>
-DAFMM_HD void log_vec(const double* u, double* out, const Pair* logtab) {
+DAFMM_HD void log_quarter_vec(const double* z2, double* out, const Pair* logtab) {
 #ifdef __CUDA_ARCH__
   double r[TB], r2[TB], qe[TB], qo[TB], lc[TB];
   int e[TB];
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    const int hi = __double2hiint(u[i]);
-    e[i] = (hi >> 20) - 1023;
+    const int hi = __double2hiint(z2[i]);
+    e[i] = (hi >> 20) - 1025;  // exponent of z2 / 4
     const int ix = (hi >> (20 - dafmm_fit::LOG_BITS)) & ((1 << dafmm_fit::LOG_BITS) - 1);
-    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(u[i]));  // [1, 2)
+    const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(z2[i]));  // [1, 2)
     const Pair tb = logtab[ix];
     r[i] = fma(m, tb.a, -1.0);  // |r| <= 2^-8
     lc[i] = tb.b;
@@ -66,21 +61,19 @@ DAFMM_HD void log_vec(const double* u, double* out, const Pair* logtab) {
     out[i] = fma((double)e[i], dafmm_fit::LN2, lc[i] + fma(r2[i], fma(r[i], qo[i], qe[i]), r[i]));
 #else
   (void)logtab;
-  for (int i = 0; i < TB; ++i) out[i] = std::log(u[i]);
+  for (int i = 0; i < TB; ++i) out[i] = std::log(0.25 * z2[i]);
 #endif
 }
 
-// Near band (z <= 8): valid for 0 < r2 with kappa^2 r2 / 4 <= 16.
-template <int TB>
-DAFMM_HD void h0_near_vec(const double* r2, double* re, double* im, const KernelConsts& k, const Pair* logtab) {
-  double u[TB], t[TB], j0[TB], rr[TB], lu[TB];
+// Near-type band ZN (z <= ZN): valid for 0 < z2 <= ZN^2.
+template <int ZN, int TB>
+DAFMM_HD void h0_near_vec(const double* z2, double* re, double* im, const Pair* logtab) {
+  using NB = dafmm_fit::NearJR<ZN>;
+  double t[TB], j0[TB], rr[TB], lu[TB];
 #pragma unroll
-  for (int i = 0; i < TB; ++i) {
-    u[i] = k.quarter_k2 * r2[i];
-    t[i] = fma(u[i], dafmm_fit::T_SCALE, -1.0);
-  }
-  dafmm_fit::near_jr<TB>(t, j0, rr);
-  log_vec<TB>(u, lu, logtab);
+  for (int i = 0; i < TB; ++i) t[i] = fma(z2[i], NB::T_SCALE, -1.0);
+  NB::template eval<TB>(t, j0, rr);
+  log_quarter_vec<TB>(z2, lu, logtab);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
     re[i] = j0[i];
@@ -88,46 +81,41 @@ DAFMM_HD void h0_near_vec(const double* r2, double* re, double* im, const Kernel
   }
 }
 
-// y = r2^(-1/4) = r^(-1/2): fp32 MUFU seed (r2 must lie in the normal fp32 range), two Newton
-// steps y <- y (5 - r2 y^4) / 4 in fp64.
-DAFMM_HD double rsqrt_sqrt(double r2) {
+// y = z2^(-1/4) = z^(-1/2): fp32 MUFU seed (z2 must lie in the normal fp32 range), then one
+// third-order step y <- y (1 + h/4 + 5h^2/32), h = 1 - z2 y^4 (seed error 2^-22 -> ~1e-19).
+DAFMM_HD double rsqrt_sqrt(double z2) {
 #ifdef __CUDA_ARCH__
-  float f = __double2float_rn(r2), g;
+  float f = __double2float_rn(z2), g;
   asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(g) : "f"(f));
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(f) : "f"(g));
-  double y = (double)f;
-  const double mq = -0.25 * r2;
-  double y2 = y * y;
-  y *= fma(mq, y2 * y2, 1.25);
-  y2 = y * y;
-  y *= fma(mq, y2 * y2, 1.25);
-  return y;
+  const double y = (double)f;
+  const double y2 = y * y;
+  const double h = fma(-z2, y2 * y2, 1.0);
+  return fma(y, h * fma(h, 0.15625, 0.25), y);
 #else
-  return 1.0 / std::sqrt(std::sqrt(r2));
+  return 1.0 / std::sqrt(std::sqrt(z2));
 #endif
 }
 
-// Far-type band B: valid for z = kappa r in [FAR_ZLO[B], FAR_ZHI[B]].
-template <int B, int TB>
-DAFMM_HD void h0_far_vec(const double* r2, double* re, double* im, const KernelConsts& k) {
+// Far-type evaluation with a caller-supplied (P, Q) evaluator: pq(x, P, Q) over TB lanes.
+template <int TB, class PQ>
+DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, double B, const PQ& pq) {
   double y[TB], z[TB], x[TB], P[TB], Q[TB], rho[TB], rh2[TB], sp[TB], c[TB];
   int quad[TB];
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    y[i] = rsqrt_sqrt(r2[i]);            // r^(-1/2)
-    const double ir = y[i] * y[i];       // 1/r
-    z[i] = k.kappa * (r2[i] * ir);       // kappa r
-    x[i] = fma(ir * k.inv_kappa, dafmm_fit::FarPQ<B>::A, dafmm_fit::FarPQ<B>::B);
+    y[i] = rsqrt_sqrt(z2[i]);   // z^(-1/2)
+    const double iz = y[i] * y[i];
+    z[i] = z2[i] * iz;
+    x[i] = fma(iz, A, B);
   }
-  dafmm_fit::FarPQ<B>::template eval<TB>(x, P, Q);
+  pq(x, P, Q);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    // theta = z - pi/4 = rho + q pi/2, m = q + 1/2, rho = z - m pi/2 (Cody-Waite, 3 parts)
+    // theta = z - pi/4 = rho + q pi/2, m = q + 1/2, rho = z - m pi/2 (two-part Cody-Waite)
     const double qf = rint(fma(z[i], dafmm_fit::TWO_OVER_PI, -0.5));
     const double m = qf + 0.5;
-    double t = fma(-m, dafmm_fit::PIO2_1, z[i]);
-    t = fma(-m, dafmm_fit::PIO2_2, t);
-    rho[i] = fma(-m, dafmm_fit::PIO2_3, t);
+    rho[i] = fma(-m, dafmm_fit::PIO2_2, fma(-m, dafmm_fit::PIO2_1, z[i]));
     rh2[i] = rho[i] * rho[i];
     quad[i] = ((int)qf) & 3;
   }
@@ -141,36 +129,58 @@ DAFMM_HD void h0_far_vec(const double* r2, double* re, double* im, const KernelC
     double sr = swap ? c[i] : s;
     if (quad[i] == 1 || quad[i] == 2) cr = -cr;
     if (quad[i] >= 2) sr = -sr;
-    const double amp = k.amp_k * y[i];   // sqrt(2/(pi z))
+    const double amp = dafmm_fit::SQRT_2_OVER_PI * y[i];  // sqrt(2/(pi z))
     const double pr = amp * P[i], pi_ = amp * Q[i];
     re[i] = fma(pr, cr, -pi_ * sr);
     im[i] = fma(pr, sr, pi_ * cr);
   }
 }
 
+template <int TB>
+struct GenericFarPQ {
+  DAFMM_HD void operator()(const double* x, double* P, double* Q) const { dafmm_fit::generic_far_pq<TB>(x, P, Q); }
+};
+
+// (P, Q) of a data band (coefficients in shared memory on the device; n is CTA-uniform).
+template <int TB>
+struct DataFarPQ {
+  const FarBand* band;
+  DAFMM_HD void operator()(const double* x, double* P, double* Q) const {
+    const int n = band->n;
+    Pair c = band->pq[n - 1];
+#pragma unroll
+    for (int i = 0; i < TB; ++i) {
+      P[i] = c.a;
+      Q[i] = c.b;
+    }
+#pragma unroll 2
+    for (int k = n - 2; k >= 0; --k) {
+      c = band->pq[k];
+#pragma unroll
+      for (int i = 0; i < TB; ++i) {
+        P[i] = fma(P[i], x[i], c.a);
+        Q[i] = fma(Q[i], x[i], c.b);
+      }
+    }
+  }
+};
+
 // Generic: any z > 0 (per-lane band choice; used where a segment straddles the bands).
 template <int TB>
-DAFMM_HD void h0_generic_vec(const double* r2, double* re, double* im, const KernelConsts& k,
-                             const Pair* logtab) {
+DAFMM_HD void h0_generic_vec(const double* z2, double* re, double* im, const Pair* logtab) {
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    if (k.quarter_k2 * r2[i] <= dafmm_fit::U_MAX) h0_near_vec<1>(r2 + i, re + i, im + i, k, logtab);
-    else h0_far_vec<0, 1>(r2 + i, re + i, im + i, k);
+    if (z2[i] <= dafmm_fit::NearJR<8>::Z2_MAX)
+      h0_near_vec<8, 1>(z2 + i, re + i, im + i, logtab);
+    else
+      h0_far_vec<1>(z2 + i, re + i, im + i, dafmm_fit::GENERIC_FAR_A, dafmm_fit::GENERIC_FAR_B, GenericFarPQ<1>());
   }
 }
 
-// Evaluation by band code (compile-time).
-template <int CODE, int TB>
-DAFMM_HD void h0_band_vec(const double* r2, double* re, double* im, const KernelConsts& k, const Pair* logtab) {
-  if constexpr (CODE == kBandGeneric) h0_generic_vec<TB>(r2, re, im, k, logtab);
-  else if constexpr (CODE == kBandNear) h0_near_vec<TB>(r2, re, im, k, logtab);
-  else h0_far_vec<CODE - 2, TB>(r2, re, im, k);
-}
-
-// Scalar host evaluation (setup: ACA entries and operators).
-inline cplx h0(double r2, const KernelConsts& k) {
+// Scalar host evaluation (setup: ACA entries and operators); z2 = (kappa r)^2.
+inline cplx h0(double z2) {
   double re, im;
-  h0_generic_vec<1>(&r2, &re, &im, k, dafmm_fit::kLogTabHost);
+  h0_generic_vec<1>(&z2, &re, &im, dafmm_fit::kLogTabHost);
   return {re, im};
 }
 
@@ -179,16 +189,20 @@ inline cplx h0(double r2, const KernelConsts& k) {
 inline int choose_band(double zmin, double zmax) {
   int best = kBandGeneric;
   double cost = 1e30;
-  if (zmax <= dafmm_fit::Z_NEAR) {
-    best = kBandNear;
-    cost = 52.0;
+  if (zmax <= 8.0) {
+    best = kBandNear8;
+    cost = 51.0;
+  } else if (zmax <= 12.0) {
+    best = kBandNear12;
+    cost = 59.0;
   }
   for (int b = 0; b < dafmm_fit::NUM_FAR; ++b) {
-    if (zmin >= dafmm_fit::FAR_ZLO[b] && zmax <= dafmm_fit::FAR_ZHI[b]) {
-      double c = 44.0 + 2.0 * dafmm_fit::FAR_N[b];
+    const FarBand& F = dafmm_fit::kFarBandsHost[b];
+    if (zmin >= F.zlo && zmax <= F.zhi) {
+      double c = 40.0 + 2.0 * F.n;
       if (c < cost) {
         cost = c;
-        best = 2 + b;
+        best = kBandFarData + b;
       }
     }
   }
@@ -200,6 +214,13 @@ inline int choose_band(double zmin, double zmax) {
 __device__ __forceinline__ void load_log_table(Pair* dst) {
   for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) dst[i] = dafmm_fit::kLogTabDev[i];
   __syncthreads();
+}
+// Copy data band b into shared memory (all threads; the caller's next barrier publishes it).
+__device__ __forceinline__ void load_far_band(FarBand* dst, int b) {
+  static_assert(sizeof(FarBand) % sizeof(Pair) == 0, "FarBand is copied as pairs");
+  const Pair* src = reinterpret_cast<const Pair*>(&dafmm_fit::kFarBandsDev[b]);
+  Pair* d = reinterpret_cast<Pair*>(dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(FarBand) / sizeof(Pair)); i += blockDim.x) d[i] = src[i];
 }
 #endif
 

@@ -11,6 +11,7 @@
 // Every kernel works in H0 units; the (i/4) of G is applied once per target in `near`.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <vector>
 
@@ -23,7 +24,9 @@ namespace {
 
 constexpr int kNearThreads = 256;
 constexpr int kM2LThreads = 128;
-constexpr int kStage = 512;  // staged source pivots / points per chunk (32 B each)
+constexpr int kM2LStage = 320;   // M2L: staged source pivots per chunk (32 B each, double-buffered)
+constexpr int kNearStage = 320;  // near field: staged source points per chunk
+constexpr int kCombineThreads = 64;
 constexpr int kTB = 4;       // kernel entries evaluated in lockstep per thread (shared coefficients)
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
@@ -40,88 +43,115 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ perm, const
 }
 
 // ---- batched translation: dst[dst_off + r] (+)= sum_terms Mat (rows x cols, col-major) src ----
-// One warp per item; lanes own rows (coalesced column reads of the operator block).
+// One warp per item; lanes own rows (coalesced column reads of the operator block).  Columns
+// are consumed 4 at a time into 4 independent accumulators so 8 loads are in flight per lane
+// and the FMA chains do not serialise on one accumulator (the stage is HBM-bound).
 __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
                                  const int32_t* __restrict__ term_ptr, const int64_t* __restrict__ mat_off,
                                  const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
                                  const double2* __restrict__ ops, const double2* __restrict__ src,
                                  double2* __restrict__ dst, int accumulate) {
-  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int lane = threadIdx.x & 31;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (warp >= items) return;
-  int rows = dst_rows[warp];
-  int tb = term_ptr[warp], te = term_ptr[warp + 1];
-  int64_t doff = dst_off[warp];
+  const int rows = dst_rows[warp];
+  const int tb = term_ptr[warp], te = term_ptr[warp + 1];
+  const int64_t doff = dst_off[warp];
   for (int r0 = 0; r0 < rows; r0 += 32) {
-    int r = r0 + lane;
-    double ar = 0.0, ai = 0.0;
+    const int r = r0 + lane;
+    if (r >= rows) break;
+    double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
     for (int t = tb; t < te; ++t) {
-      const double2* M = ops + mat_off[t];
-      const double2* s = src + src_off[t];
-      int cols = src_cols[t];
-      if (r < rows) {
-#pragma unroll 4
-        for (int c = 0; c < cols; ++c) {
-          double2 m = ld2(M + (int64_t)c * rows + r);
-          double2 v = ld2(s + c);
-          ar = fma(m.x, v.x, fma(-m.y, v.y, ar));
-          ai = fma(m.x, v.y, fma(m.y, v.x, ai));
+      const double2* M = ops + mat_off[t] + r;
+      const double2* sv = src + src_off[t];
+      const int cols = src_cols[t];
+      int c = 0;
+      for (; c + 4 <= cols; c += 4) {
+        double2 m[4], v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          m[q] = ld2(M + (int64_t)(c + q) * rows);
+          v[q] = ld2(sv + c + q);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          ar[q] = fma(m[q].x, v[q].x, fma(-m[q].y, v[q].y, ar[q]));
+          ai[q] = fma(m[q].x, v[q].y, fma(m[q].y, v[q].x, ai[q]));
         }
       }
-    }
-    if (r < rows) {
-      double2 o = make_double2(ar, ai);
-      if (accumulate) {
-        double2 p = dst[doff + r];
-        o.x += p.x;
-        o.y += p.y;
+      for (; c < cols; ++c) {
+        const double2 m = ld2(M + (int64_t)c * rows), v = ld2(sv + c);
+        ar[0] = fma(m.x, v.x, fma(-m.y, v.y, ar[0]));
+        ai[0] = fma(m.x, v.y, fma(m.y, v.x, ai[0]));
       }
-      dst[doff + r] = o;
     }
+    double2 o = make_double2((ar[0] + ar[1]) + (ar[2] + ar[3]), (ai[0] + ai[1]) + (ai[2] + ai[3]));
+    if (accumulate) {
+      const double2 p = dst[doff + r];
+      o.x += p.x;
+      o.y += p.y;
+    }
+    dst[doff + r] = o;
   }
 }
 
-// Stage (x, y, value) of `take` consecutive sources into shared memory.
-__device__ __forceinline__ void stage_sources(double4* sbuf, int fill, const double2* xy, const double2* val,
-                                              int64_t off, int take) {
-  for (int q = threadIdx.x; q < take; q += blockDim.x) {
-    double2 p = ld2(xy + off + q);
-    double2 v = ld2(val + off + q);
-    sbuf[fill + q] = make_double4(p.x, p.y, v.x, v.y);
-  }
-}
+// ---- source streams ----------------------------------------------------------------------------
+// P2P and M2L share one engine: a CTA owns a set of targets (the points of a leaf or the pivots
+// of a node, one per thread "t", with nsl source slices) and a stream of sources given as a CSR
+// list of contiguous runs (entry e -> (first, count)).  The stream is staged through shared
+// memory in double-buffered chunks with cp.async (x, y, value: 32 B per source) while the
+// previous chunk is consumed; the stream is cut into band-uniform items [pb, pe) (stream
+// offsets) whose band code is CTA-uniform, so every inner loop is one templated evaluator.
 
-// Source lists as CSR entries e -> (first source, count).
-struct M2LSources {
-  const int64_t* off;
-  const int32_t* cnt;
-  __device__ __forceinline__ int64_t first(int e) const { return off[e]; }
-  __device__ __forceinline__ int count(int e) const { return cnt[e]; }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Stagers: copy the next chunk of a CTA's source stream into shared memory (asynchronous, one
+// cp.async commit group per call; returns the number of sources staged, 0 at the end).
+// IndexStager: the M2L stream is a flat list of multipole slots (idx), so every thread finds
+// its source directly.  RunStager: the near-field stream is a few runs of consecutive points
+// (the neighbour leaves), walked with a cursor that every thread advances identically.
+struct IndexStager {
+  const int32_t* idx;
+  int64_t base;
+  int total;
+  const double2* xy;
+  const double2* val;
+  template <int STAGE>
+  __device__ __forceinline__ int stage(double4* buf, int c0) {
+    const int fill = min(STAGE, total - c0);
+    for (int q = threadIdx.x; q < fill; q += blockDim.x) {
+      const int k = __ldg(idx + base + c0 + q);
+      double2* d = reinterpret_cast<double2*>(buf + q);
+      cp_async16(d, xy + k);
+      cp_async16(d + 1, val + k);
+    }
+    cp_async_commit();
+    return max(fill, 0);
+  }
 };
-struct NearSources {
+struct RunStager {
   const int32_t* begin;
   const int32_t* end;
-  __device__ __forceinline__ int64_t first(int e) const { return begin[e]; }
-  __device__ __forceinline__ int count(int e) const { return end[e] - begin[e]; }
-};
-
-// acc += sum over the source entries [e, pe) of H0_band(kappa |xt - s_j|) v_j.  Sources are
-// staged through shared memory in chunks of kStage; thread (t, slice) takes every nsl-th
-// staged source.  CTA-uniform (contains barriers): every thread calls it with the same
-// arguments apart from xt / active / slice.  GUARD: the segment may contain the pair i == j
-// (the own leaf of the near field), whose entry is excluded (its value is the self term D_i).
-template <int CODE, bool GUARD, class Src>
-__device__ __forceinline__ void accumulate(double4* sbuf, const Src& src, int e, int pe, const double2* __restrict__ xy,
-                                           const double2* __restrict__ val, double2 xt, bool active, int slice,
-                                           int nsl, double& ar, double& ai, const KernelConsts& kc,
-                                           const Pair* logtab) {
-  int kin = 0;
-  while (e < pe) {
+  int e, kin, pe;
+  const double2* xy;
+  const double2* val;
+  template <int STAGE>
+  __device__ __forceinline__ int stage(double4* buf, int) {
     int fill = 0;
-    while (e < pe && fill < kStage) {
-      int cnt = src.count(e);
-      int take = min(cnt - kin, kStage - fill);
-      stage_sources(sbuf, fill, xy, val, src.first(e) + kin, take);
+    while (e < pe && fill < STAGE) {
+      const int first = begin[e], cnt = end[e] - first;
+      const int take = min(cnt - kin, STAGE - fill);
+      const int64_t off = (int64_t)first + kin;
+      for (int q = threadIdx.x; q < take; q += blockDim.x) {
+        double2* d = reinterpret_cast<double2*>(buf + fill + q);
+        cp_async16(d, xy + off + q);
+        cp_async16(d + 1, val + off + q);
+      }
       fill += take;
       kin += take;
       if (kin == cnt) {
@@ -129,125 +159,219 @@ __device__ __forceinline__ void accumulate(double4* sbuf, const Src& src, int e,
         kin = 0;
       }
     }
-    __syncthreads();
-    if (active) {
-      // kTB staged sources per step (j, j + nsl, ...), evaluated in lockstep; lanes past the
-      // fill (and the i == j pair under GUARD) get a safe distance and a zero weight
-      for (int j = slice; j < fill; j += kTB * nsl) {
-        double r2[kTB], vr[kTB], vi[kTB], hr[kTB], hi[kTB];
+    cp_async_commit();
+    return fill;
+  }
+};
+
+// Items of an M2L target: band code and stream range, from the packed plan.
+struct M2LItems {
+  const int32_t* code_;
+  const int32_t* pb_;
+  const int32_t* pe_;
+  int is, ie;
+  __device__ __forceinline__ int code(int i) const { return code_[i]; }
+  __device__ __forceinline__ bool guard(int) const { return false; }
+  __device__ __forceinline__ int pb(int i) const { return pb_[i]; }
+  __device__ __forceinline__ int pe(int i) const { return pe_[i]; }
+};
+// Items of a near-field leaf: its own block [0, own) (contains i == j) and the rest.
+struct NearItems {
+  int band, own, total, is, ie;
+  __device__ __forceinline__ int code(int) const { return band; }
+  __device__ __forceinline__ bool guard(int i) const { return i == 0; }
+  __device__ __forceinline__ int pb(int i) const { return i == 0 ? 0 : own; }
+  __device__ __forceinline__ int pe(int i) const { return i == 0 ? own : total; }
+};
+
+// Band evaluator by code (compile time): generic, near 8, near 12, or a data band.
+template <int CODE>
+__device__ __forceinline__ void eval_band(const double* z2, double* re, double* im, const Pair* logtab,
+                                          const FarBand* band) {
+  if constexpr (CODE == kBandGeneric) h0_generic_vec<kTB>(z2, re, im, logtab);
+  else if constexpr (CODE == kBandNear8) h0_near_vec<8, kTB>(z2, re, im, logtab);
+  else if constexpr (CODE == kBandNear12) h0_near_vec<12, kTB>(z2, re, im, logtab);
+  else h0_far_vec<kTB>(z2, re, im, band->A, band->B, DataFarPQ<kTB>{band});
+}
+
+// One lockstep block of kTB staged sources p[0], p[stride], ...: acc += sum_q H0(|xt - s_q|) v_q.
+// MASK: only the first `valid` sources count (tail block); GUARD: the pair i == j (own leaf of
+// the near field; its value is the self term D_i) is excluded.  Excluded lanes get a safe z^2
+// and a zero weight so the evaluator stays branch-free.
+template <int CODE, bool GUARD, bool MASK>
+__device__ __forceinline__ void consume_block(const double4* p, int stride, int valid, double2 xt, double& ar, double& ai,
+                                              const Pair* logtab, const FarBand* band) {
+  double z2[kTB], hr[kTB], hi[kTB];
+  bool use[kTB];
 #pragma unroll
-        for (int b = 0; b < kTB; ++b) {
-          const int jb = j + b * nsl;
-          const bool ok = jb < fill;
-          const double4 sv = sbuf[ok ? jb : j];
-          const double dx = xt.x - sv.x, dy = xt.y - sv.y;
-          const double d2 = fma(dx, dx, dy * dy);
-          const bool use = ok && (!GUARD || d2 > 0.0);
-          r2[b] = use ? d2 : kc.r2_safe;
-          vr[b] = use ? sv.z : 0.0;
-          vi[b] = use ? sv.w : 0.0;
-        }
-        h0_band_vec<CODE, kTB>(r2, hr, hi, kc, logtab);
+  for (int q = 0; q < kTB; ++q) {
+    const bool ok = !MASK || q < valid;
+    const double2 sp = *reinterpret_cast<const double2*>(p + ((MASK && !ok) ? 0 : q * stride));
+    const double dx = xt.x - sp.x, dy = xt.y - sp.y;
+    const double d2 = fma(dx, dx, dy * dy);
+    use[q] = ok && (!GUARD || d2 > 0.0);
+    z2[q] = (MASK || GUARD) ? (use[q] ? d2 : kZ2Safe) : d2;
+  }
+  eval_band<CODE>(z2, hr, hi, logtab, band);
+  // the weights are re-read from shared memory after the evaluation (not held in registers
+  // across it: the evaluator needs every register it can get)
 #pragma unroll
-        for (int b = 0; b < kTB; ++b) {
-          ar = fma(hr[b], vr[b], fma(-hi[b], vi[b], ar));
-          ai = fma(hr[b], vi[b], fma(hi[b], vr[b], ai));
-        }
-      }
+  for (int q = 0; q < kTB; ++q) {
+    double2 v = reinterpret_cast<const double2*>(p + ((MASK && q >= valid) ? 0 : q * stride))[1];
+    if (MASK || GUARD) {
+      v.x = use[q] ? v.x : 0.0;
+      v.y = use[q] ? v.y : 0.0;
     }
-    __syncthreads();
+    ar = fma(hr[q], v.x, fma(-hi[q], v.y, ar));
+    ai = fma(hr[q], v.y, fma(hi[q], v.x, ai));
   }
 }
 
-// Dispatch a CTA-uniform band code to its instantiation.
-template <bool GUARD, class Src>
-__device__ __forceinline__ void accumulate_code(int code, double4* sbuf, const Src& src, int e, int pe,
-                                                const double2* __restrict__ xy, const double2* __restrict__ val,
-                                                double2 xt, bool active, int slice, int nsl, double& ar, double& ai,
-                                                const KernelConsts& kc, const Pair* logtab) {
-#define DAFMM_BAND_CASE(C) \
-  case C: accumulate<C, GUARD>(sbuf, src, e, pe, xy, val, xt, active, slice, nsl, ar, ai, kc, logtab); break;
-  switch (code) {
-    DAFMM_BAND_CASE(1)
-    DAFMM_BAND_CASE(2)
-    DAFMM_BAND_CASE(3)
-    DAFMM_BAND_CASE(4)
-    DAFMM_BAND_CASE(5)
-    DAFMM_BAND_CASE(6)
-    DAFMM_BAND_CASE(7)
-    DAFMM_BAND_CASE(8)
-    DAFMM_BAND_CASE(9)
-    default: accumulate<kBandGeneric, GUARD>(sbuf, src, e, pe, xy, val, xt, active, slice, nsl, ar, ai, kc, logtab);
-  }
-#undef DAFMM_BAND_CASE
+// acc += sum_{j in [a, b)} H0(|xt - s_j|) v_j over staged sources (kappa-scaled coordinates).
+// The range is cut into blocks of kTB consecutive sources, dealt to the slices cyclically
+// (block k to slice k mod nsl); only the last block of the range can be partial (masked).
+template <int CODE, bool GUARD>
+__device__ __forceinline__ void consume(const double4* sb, int a, int b, double2 xt, int slice, int nsl, double& ar,
+                                        double& ai, const Pair* logtab, const FarBand* band) {
+  const int n = b - a;
+  const int full = n / kTB;
+  for (int k = slice; k < full; k += nsl)
+    consume_block<CODE, GUARD, false>(sb + a + k * kTB, 1, kTB, xt, ar, ai, logtab, band);
+  if ((n % kTB) && slice == full % nsl)
+    consume_block<CODE, GUARD, true>(sb + a + full * kTB, 1, n % kTB, xt, ar, ai, logtab, band);
 }
-static_assert(kNumBandCodes == 10, "accumulate_code lists the band codes 1..9 explicitly");
+
+template <bool GUARD>
+__device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
+                                             double& ar, double& ai, const Pair* logtab, const FarBand* bands) {
+  switch (code) {
+    case kBandNear8:
+      consume<kBandNear8, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+      break;
+    case kBandNear12:
+      if constexpr (!GUARD) consume<kBandNear12, false>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+      else consume<kBandGeneric, true>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+      break;
+    case kBandGeneric:
+      consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+      break;
+    default:
+      if constexpr (!GUARD)
+        consume<kBandFarData, false>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands + (code - kBandFarData));
+      else consume<kBandGeneric, true>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+  }
+}
+
+// Run a CTA over one source stream (stager `st`, items of `items`).  CTA-uniform (barriers);
+// `buf` holds 2 x STAGE double4: the next chunk is staged while the current one is consumed.
+// Ends with a barrier.
+template <int STAGE, class Stager, class Items>
+__device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, const Items& items, double2 xt, bool active,
+                                                  int slice, int nsl, double& ar, double& ai, const Pair* logtab,
+                                                  const FarBand* bands) {
+  int c0 = 0, which = 0, it0 = items.is;
+  int fill = st.template stage<STAGE>(buf, 0);
+  while (fill > 0) {
+    cp_async_wait_all();
+    __syncthreads();  // chunk `which` visible to all; everyone is done with the other buffer
+    const int next = st.template stage<STAGE>(buf + (which ^ 1) * STAGE, c0 + fill);
+    const int c1 = c0 + fill;
+    while (it0 < items.ie && items.pe(it0) <= c0) ++it0;
+    if (active) {
+      const double4* sb = buf + which * STAGE;
+      for (int it = it0; it < items.ie && items.pb(it) < c1; ++it) {
+        const int a = max(items.pb(it), c0) - c0, b = min(items.pe(it), c1) - c0;
+        if (items.guard(it)) consume_code<true>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+        else consume_code<false>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+      }
+    }
+    c0 = c1;
+    fill = next;
+    which ^= 1;
+  }
+  __syncthreads();
+}
+
+// Copy the log table and every data band into shared memory (all threads; then a barrier).
+__device__ __forceinline__ void load_tables(Pair* logtab, FarBand* bands) {
+  for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) logtab[i] = dafmm_fit::kLogTabDev[i];
+  static_assert(sizeof(FarBand) % sizeof(Pair) == 0, "FarBand is copied as pairs");
+  const Pair* src = reinterpret_cast<const Pair*>(dafmm_fit::kFarBandsDev);
+  Pair* d = reinterpret_cast<Pair*>(bands);
+  constexpr int n = (int)(dafmm_fit::NUM_FAR * sizeof(FarBand) / sizeof(Pair));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
+  __syncthreads();
+}
 
 // ---- M2L: u[t] = sum_{src nodes} sum_k H0(kappa |t - s_k|) m_k --------------------
-// One CTA per target node; its source nodes come in band-uniform segments (items).
-__global__ void __launch_bounds__(kM2LThreads) m2l_kernel(
-    const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows, const int32_t* __restrict__ item_ptr,
-    const int32_t* __restrict__ item_code, const int32_t* __restrict__ item_begin,
-    const int32_t* __restrict__ item_end, const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cnt,
-    const double2* __restrict__ ti_xy, const double2* __restrict__ so_xy, const double2* __restrict__ mult,
-    double2* __restrict__ loc, KernelConsts kc) {
-  __shared__ double4 sbuf[kStage];
+// One CTA per target node; its source stream is cut into band-uniform items.
+__global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
+    int ntargets, int* __restrict__ ticket, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx, const int32_t* __restrict__ item_ptr,
+    const int32_t* __restrict__ item_code, const int32_t* __restrict__ item_pb, const int32_t* __restrict__ item_pe,
+    const double2* __restrict__ ti_xy, const double2* __restrict__ so_xy,
+    const double2* __restrict__ mult, double2* __restrict__ loc) {
+  __shared__ __align__(16) double4 buf[2 * kM2LStage];
   __shared__ double2 red[kM2LThreads];
   __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
-  load_log_table(logtab);
-  const int tgt = blockIdx.x;
-  const int r = rows[tgt];
-  const int64_t lo = loc_off[tgt];
-  const int is = item_ptr[tgt], ie = item_ptr[tgt + 1];
-  const M2LSources src{src_off, src_cnt};
-  for (int t0 = 0; t0 < r; t0 += kM2LThreads) {
-    const int rc = min(kM2LThreads, r - t0);
-    const int nsl = kM2LThreads / rc;
-    const int t = threadIdx.x % rc;
-    const int slice = threadIdx.x / rc;
-    const bool active = slice < nsl;
-    double2 xt = ld2(ti_xy + lo + t0 + t);
-    double ar = 0.0, ai = 0.0;
-    for (int it = is; it < ie; ++it)
-      accumulate_code<false>(item_code[it], sbuf, src, item_begin[it], item_end[it], so_xy, mult, xt, active, slice,
-                             nsl, ar, ai, kc, logtab);
-    red[threadIdx.x] = make_double2(ar, ai);
+  __shared__ FarBand bands[dafmm_fit::NUM_FAR];
+  __shared__ int next;
+  load_tables(logtab, bands);
+  // persistent CTAs take target nodes from a ticket counter (targets are packed by
+  // decreasing cost, so the dynamic order balances the tail)
+  while (true) {
+    if (threadIdx.x == 0) next = atomicAdd(ticket, 1);
     __syncthreads();
-    if (threadIdx.x < rc) {
-      double sr = 0.0, si = 0.0;
-      for (int s = 0; s < nsl; ++s) {
-        double2 v = red[threadIdx.x + s * rc];
-        sr += v.x;
-        si += v.y;
+    const int tgt = next;
+    __syncthreads();
+    if (tgt >= ntargets) break;
+    const int r = rows[tgt];
+    const int64_t lo = loc_off[tgt];
+    const M2LItems items{item_code, item_pb, item_pe, item_ptr[tgt], item_ptr[tgt + 1]};
+    for (int t0 = 0; t0 < r; t0 += kM2LThreads) {
+      const int rc = min(kM2LThreads, r - t0);
+      const int nsl = kM2LThreads / rc;
+      const int t = threadIdx.x % rc;
+      const int slice = threadIdx.x / rc;
+      const bool active = slice < nsl;
+      double2 xt = ld2(ti_xy + lo + t0 + t);
+      double ar = 0.0, ai = 0.0;
+      IndexStager st{stream_idx, stream_ptr[tgt], (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]), so_xy, mult};
+      stream_accumulate<kM2LStage>(buf, st, items, xt, active, slice, nsl, ar, ai, logtab, bands);
+      red[threadIdx.x] = make_double2(ar, ai);
+      __syncthreads();
+      if (threadIdx.x < rc) {
+        double sr = 0.0, si = 0.0;
+        for (int s = 0; s < nsl; ++s) {
+          double2 v = red[threadIdx.x + s * rc];
+          sr += v.x;
+          si += v.y;
+        }
+        loc[lo + t0 + threadIdx.x] = make_double2(sr, si);
       }
-      loc[lo + t0 + threadIdx.x] = make_double2(sr, si);
+      __syncthreads();
     }
-    __syncthreads();
   }
 }
 
-// ---- near field + L2P + combine ------------------------------------------------
-// phi_t = (i/4) [ sum_{j in N(leaf), j != t} H0 v_j + (U u)_t ] + D_t x_t
-// y[perm[t]] = x_t + kappa^2 q_t phi_t   (kernel_mode 0)   or   phi_t   (kernel_mode 1)
+// ---- near field P2P ------------------------------------------------------------
+// phi_t = sum_{j in N(leaf), j != t} H0(kappa |x_t - x_j|) v_j   (H0 units, tree order).
 // The leaf's own block is the first near entry (the only one with i == j pairs).
-__global__ void __launch_bounds__(kNearThreads) near_kernel(
+__global__ void __launch_bounds__(kNearThreads, 3) p2p_kernel(
     const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end, const int32_t* __restrict__ near_ptr,
     const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int32_t* __restrict__ leaf_band,
-    const int64_t* __restrict__ leaf_loc_off, const int32_t* __restrict__ leaf_rank,
-    const int64_t* __restrict__ leaf_U_off, const double2* __restrict__ ops, const double2* __restrict__ loc,
-    const double2* __restrict__ pts_t, const double2* __restrict__ v_t, const double2* __restrict__ x_t,
-    const double* __restrict__ qk2_t, const double2* __restrict__ D_t, const int32_t* __restrict__ perm,
-    double2* __restrict__ y, KernelConsts kc, int kernel_mode, unsigned mask) {
-  __shared__ double4 sbuf[kStage];
+    const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi) {
+  __shared__ __align__(16) double4 buf[2 * kNearStage];
   __shared__ double2 red[kNearThreads];
   __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
-  load_log_table(logtab);
+  for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) logtab[i] = dafmm_fit::kLogTabDev[i];
+  __syncthreads();
   const int leaf = blockIdx.x;
   const int tb = leaf_begin[leaf], m = leaf_end[leaf] - tb;
   const int ps = near_ptr[leaf], pe = near_ptr[leaf + 1];
-  const bool do_near = mask & 1u, do_far = (mask & 2u) && leaf_loc_off[leaf] >= 0;
-  const int band = leaf_band[leaf];
-  const NearSources src{near_begin, near_end};
+  int total = 0;
+  for (int e = ps; e < pe; ++e) total += near_end[e] - near_begin[e];
+  const NearItems items{leaf_band[leaf], pe > ps ? near_end[ps] - near_begin[ps] : 0, total, 0, 2};
   for (int t0 = 0; t0 < m; t0 += kNearThreads) {
     const int rc = min(kNearThreads, m - t0);
     const int nsl = kNearThreads / rc;
@@ -256,58 +380,87 @@ __global__ void __launch_bounds__(kNearThreads) near_kernel(
     const bool active = slice < nsl;
     double2 xt = ld2(pts_t + tb + t0 + t);
     double ar = 0.0, ai = 0.0;
-    if (do_near && pe > ps) {
-      if (band == kBandNear) {
-        accumulate<kBandNear, true>(sbuf, src, ps, ps + 1, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
-        accumulate<kBandNear, false>(sbuf, src, ps + 1, pe, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
-      } else {
-        accumulate<kBandGeneric, true>(sbuf, src, ps, ps + 1, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
-        accumulate<kBandGeneric, false>(sbuf, src, ps + 1, pe, pts_t, v_t, xt, active, slice, nsl, ar, ai, kc, logtab);
-      }
+    if (pe > ps) {
+      RunStager st{near_begin, near_end, ps, 0, pe, pts_t, v_t};
+      stream_accumulate<kNearStage>(buf, st, items, xt, active, slice, nsl, ar, ai, logtab, nullptr);
     }
     red[threadIdx.x] = make_double2(ar, ai);
     __syncthreads();
     if (threadIdx.x < rc) {
-      const int tt = t0 + threadIdx.x;
       double sr = 0.0, si = 0.0;
       for (int s = 0; s < nsl; ++s) {
         double2 v = red[threadIdx.x + s * rc];
         sr += v.x;
         si += v.y;
       }
-      if (do_far) {  // L2P: (U u)_t, U column-major m x r
-        const int rk = leaf_rank[leaf];
-        const double2* U = ops + leaf_U_off[leaf];
-        const double2* u = loc + leaf_loc_off[leaf];
-        for (int c = 0; c < rk; ++c) {
-          double2 a = ld2(U + (int64_t)c * m + tt);
-          double2 b = ld2(u + c);
-          sr = fma(a.x, b.x, fma(-a.y, b.y, sr));
-          si = fma(a.x, b.y, fma(a.y, b.x, si));
-        }
-      }
-      // phi = (i/4) (sr + i si) + D x
-      double2 xv = x_t[tb + tt];
-      double pr = -0.25 * si, pi = 0.25 * sr;
-      if (do_near) {
-        double2 d = D_t[tb + tt];
-        pr = fma(d.x, xv.x, fma(-d.y, xv.y, pr));
-        pi = fma(d.x, xv.y, fma(d.y, xv.x, pi));
-      }
-      double2 out;
-      if (kernel_mode == 0) {
-        double s = qk2_t[tb + tt];
-        out = make_double2(s * pr, s * pi);
-        if (do_near) {
-          out.x += xv.x;
-          out.y += xv.y;
-        }
-      } else {
-        out = make_double2(pr, pi);
-      }
-      y[perm[tb + tt]] = out;
+      phi[tb + t0 + threadIdx.x] = make_double2(sr, si);
     }
     __syncthreads();
+  }
+}
+
+// ---- L2P + combine + scatter ---------------------------------------------------
+// phi_t = (i/4) [ P2P_t + (U u)_t ] + D_t x_t;   y[perm[t]] = x_t + kappa^2 q_t phi_t (mode 0)
+// or phi_t (mode 1).  One CTA per leaf, one thread per point (coalesced columns of U).
+__global__ void combine_kernel(const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end,
+                               const int64_t* __restrict__ leaf_loc_off, const int32_t* __restrict__ leaf_rank,
+                               const int64_t* __restrict__ leaf_U_off, const double2* __restrict__ ops,
+                               const double2* __restrict__ loc, const double2* __restrict__ phi,
+                               const double2* __restrict__ x_t, const double* __restrict__ qk2_t,
+                               const double2* __restrict__ D_t, const int32_t* __restrict__ perm,
+                               double2* __restrict__ y, int kernel_mode, int do_near, int do_far_in) {
+  const int leaf = blockIdx.x;
+  const int tb = leaf_begin[leaf], m = leaf_end[leaf] - tb;
+  const bool do_far = do_far_in && leaf_loc_off[leaf] >= 0;
+  for (int tt = threadIdx.x; tt < m; tt += blockDim.x) {
+    double sr = 0.0, si = 0.0;
+    if (do_near) {
+      const double2 p = phi[tb + tt];
+      sr = p.x;
+      si = p.y;
+    }
+    if (do_far) {  // L2P: (U u)_t, U column-major m x r
+      const int rk = leaf_rank[leaf];
+      const double2* U = ops + leaf_U_off[leaf];
+      const double2* u = loc + leaf_loc_off[leaf];
+      double ar[2] = {0.0, 0.0}, ai[2] = {0.0, 0.0};
+      int c = 0;
+      for (; c + 2 <= rk; c += 2) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double2 a = ld2(U + (int64_t)(c + q) * m + tt), b = ld2(u + c + q);
+          ar[q] = fma(a.x, b.x, fma(-a.y, b.y, ar[q]));
+          ai[q] = fma(a.x, b.y, fma(a.y, b.x, ai[q]));
+        }
+      }
+      if (c < rk) {
+        const double2 a = ld2(U + (int64_t)c * m + tt), b = ld2(u + c);
+        ar[0] = fma(a.x, b.x, fma(-a.y, b.y, ar[0]));
+        ai[0] = fma(a.x, b.y, fma(a.y, b.x, ai[0]));
+      }
+      sr += ar[0] + ar[1];
+      si += ai[0] + ai[1];
+    }
+    // phi = (i/4) (sr + i si) + D x
+    const double2 xv = x_t[tb + tt];
+    double pr = -0.25 * si, pi = 0.25 * sr;
+    if (do_near) {
+      const double2 d = D_t[tb + tt];
+      pr = fma(d.x, xv.x, fma(-d.y, xv.y, pr));
+      pi = fma(d.x, xv.y, fma(d.y, xv.x, pi));
+    }
+    double2 out;
+    if (kernel_mode == 0) {
+      const double q = qk2_t[tb + tt];
+      out = make_double2(q * pr, q * pi);
+      if (do_near) {
+        out.x += xv.x;
+        out.y += xv.y;
+      }
+    } else {
+      out = make_double2(pr, pi);
+    }
+    y[perm[tb + tt]] = out;
   }
 }
 
@@ -458,7 +611,6 @@ int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, do
 int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err) {
   d.n = plan.n;
   d.kernel_mode = plan.opt.kernel_mode;
-  d.kc = make_kernel_consts(plan.kappa);
   std::vector<double2> pts(plan.n), D(plan.n);
   for (int64_t t = 0; t < plan.n; ++t) {
     pts[t] = make_double2(pk.pts_t[2 * t], pk.pts_t[2 * t + 1]);
@@ -481,8 +633,8 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err);
   d.m2l_targets = (int)pk.m2l_loc_off.size();
   ok = ok && upload(d, &d.m2l_loc_off, pk.m2l_loc_off, err) && upload(d, &d.m2l_rows, pk.m2l_rows, err) &&
-       upload(d, &d.m2l_src_ptr, pk.m2l_src_ptr, err) && upload(d, &d.m2l_src_off, pk.m2l_src_off, err) &&
-       upload(d, &d.m2l_src_cnt, pk.m2l_src_cnt, err) && upload(d, &d.m2l_item_ptr, pk.m2l_item_ptr, err) &&
+       upload(d, &d.m2l_stream_ptr, pk.m2l_stream_ptr, err) && upload(d, &d.m2l_stream_idx, pk.m2l_stream_idx, err) &&
+       upload(d, &d.m2l_item_ptr, pk.m2l_item_ptr, err) &&
        upload(d, &d.m2l_item_code, pk.m2l_item_code, err) && upload(d, &d.m2l_item_begin, pk.m2l_item_begin, err) &&
        upload(d, &d.m2l_item_end, pk.m2l_item_end, err);
   d.nleaves = (int)pk.leaf_begin.size();
@@ -492,13 +644,28 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
        upload(d, &d.near_end, pk.near_end, err) && upload(d, &d.leaf_loc_off, pk.leaf_loc_off, err) &&
        upload(d, &d.leaf_rank, pk.leaf_rank, err) && upload(d, &d.leaf_U_off, pk.leaf_U_off, err) &&
        upload(d, &d.leaf_band, pk.leaf_band, err);
-  ok = ok && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
+  if (ok) {
+    int per_sm = 0, sms = 0, dev = 0;
+    ok = ck(cudaGetDevice(&dev), err, "cudaGetDevice") &&
+         ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), err, "SM count") &&
+         ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
+    d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
+  }
+  ok = ok && ck(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking), err, "side stream") &&
+       ck(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming), err, "fork event") &&
+       ck(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming), err, "join event") &&
+       alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 1, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
        alloc(d, &d.loc, pk.n_loc, err) && alloc(d, &d.host_stage, 2 * plan.n, err);
   if (!ok) return DAFMM_ECUDA;
   return DAFMM_OK;
 }
 
 void free_plan(DevPlan& d) {
+  if (d.ev_fork) cudaEventDestroy(d.ev_fork);
+  if (d.ev_join) cudaEventDestroy(d.ev_join);
+  if (d.side) cudaStreamDestroy(d.side);
+  d.ev_fork = d.ev_join = nullptr;
+  d.side = nullptr;
   for (auto& e : d.prof_ev)
     if (e) {
       cudaEventDestroy(e);
@@ -524,54 +691,87 @@ int set_profiling(DevPlan& d, bool on, std::string& err) {
 
 int harvest_profile(DevPlan& d, std::string& err) {
   if (!d.prof_pending) return DAFMM_OK;
-  if (!ck(cudaEventSynchronize(d.prof_ev[kNumPasses]), err, "profile event sync")) return DAFMM_ECUDA;
-  for (int p = 0; p < kNumPasses; ++p) {
+  if (!ck(cudaEventSynchronize(d.prof_ev[EV_END]), err, "profile event sync")) return DAFMM_ECUDA;
+  auto el = [&](int a, int b, double& out) -> bool {
     float ms = 0.f;
-    if (!ck(cudaEventElapsedTime(&ms, d.prof_ev[p], d.prof_ev[p + 1]), err, "profile elapsed")) return DAFMM_ECUDA;
-    d.prof_ms[p] += ms;
-  }
+    if (!ck(cudaEventElapsedTime(&ms, d.prof_ev[a], d.prof_ev[b]), err, "profile elapsed")) return false;
+    out = ms;
+    return true;
+  };
+  double t[kNumPasses], near_end = 0.0, far_end = 0.0;
+  if (!el(EV_START, EV_FORK, t[0]) || !el(EV_FORK, EV_P2M, t[1]) || !el(EV_P2M, EV_M2M, t[2]) ||
+      !el(EV_M2M, EV_M2L, t[3]) || !el(EV_M2L, EV_L2L, t[4]) || !el(EV_NEAR0, EV_NEAR1, t[5]) ||
+      !el(EV_JOIN, EV_END, t[6]) || !el(EV_FORK, EV_NEAR1, near_end) || !el(EV_FORK, EV_L2L, far_end))
+    return DAFMM_ECUDA;
+  t[7] = std::max(near_end, far_end);
+  for (int p = 0; p < kNumPasses; ++p) d.prof_ms[p] += t[p];
   ++d.prof_count;
   d.prof_pending = false;
   return DAFMM_OK;
 }
 
+// y = A x.  The near field (P2P) only needs the gathered vector, so it runs on the side stream
+// concurrently with the far field (P2M, M2M, M2L, L2L) on the handle's stream; the combine
+// (L2P + identity + scatter) joins both.  No host synchronisation.
 int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::string& err) {
   cudaStream_t s = d.stream;
   if (d.prof && harvest_profile(d, err) != DAFMM_OK) return DAFMM_ECUDA;
-  // profiling marks: event p is recorded before pass p (p = 0..5) and event 6 after the last
-  auto mark = [&](int p) {
-    if (d.prof) cudaEventRecord(d.prof_ev[p], s);
+  auto mark = [&](int e, cudaStream_t st) {
+    if (d.prof) cudaEventRecord(d.prof_ev[e], st);
   };
-  mark(0);
+  const bool near = mask & 1u;
+  const bool far = (mask & 2u) && d.n_mult > 0;
+  const bool fork = near && far && d.side != nullptr;
+  mark(EV_START, s);
   gather_kernel<<<grid_for(d.n, 256, 148 * 16), 256, 0, s>>>(d.n, d.perm, d.w_t, x, d.x_t, d.v_t);
   ++d.launches;
-  const bool far = (mask & 2u) && d.n_mult > 0;
+  mark(EV_FORK, s);
+  cudaStream_t ns = s;  // stream of the P2P kernel
+  if (fork) {
+    cudaEventRecord(d.ev_fork, s);
+    cudaStreamWaitEvent(d.side, d.ev_fork, 0);
+    ns = d.side;
+  }
+  auto launch_p2p = [&]() {
+    mark(EV_NEAR0, ns);
+    if (near) {
+      p2p_kernel<<<d.nleaves, kNearThreads, 0, ns>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
+                                                     d.leaf_band, d.pts_t, d.v_t, d.phi);
+      ++d.launches;
+    }
+    mark(EV_NEAR1, ns);
+  };
+  if (fork || !far) launch_p2p();  // concurrent with the far field, or near only
+  if (fork) cudaEventRecord(d.ev_join, d.side);
   if (far) {
     cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, s);
     cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, s);
+    if (d.m2l_targets > 0) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), s);
   }
-  mark(1);
+  mark(EV_P2M, s);
   if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0);  // P2M
-  mark(2);
+  mark(EV_M2M, s);
   if (far)
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0);  // M2M
-  mark(3);
-  if (far && d.m2l_targets > 0) {  // M2L
-    m2l_kernel<<<d.m2l_targets, kM2LThreads, 0, s>>>(d.m2l_loc_off, d.m2l_rows, d.m2l_item_ptr, d.m2l_item_code,
-                                                      d.m2l_item_begin, d.m2l_item_end, d.m2l_src_off,
-                                                      d.m2l_src_cnt, d.ti_xy, d.so_xy, d.mult, d.loc, d.kc);
+  mark(EV_M2L, s);
+  if (far && d.m2l_targets > 0) {  // M2L, persistent CTAs
+    m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, s>>>(d.m2l_targets, d.m2l_ticket, d.m2l_loc_off, d.m2l_rows,
+                                                   d.m2l_stream_ptr, d.m2l_stream_idx, d.m2l_item_ptr, d.m2l_item_code,
+                                                   d.m2l_item_begin, d.m2l_item_end, d.ti_xy, d.so_xy,
+                                                   d.mult, d.loc);
     ++d.launches;
   }
-  mark(4);
   if (far)
     for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1);  // L2L
-  mark(5);
-  near_kernel<<<d.nleaves, kNearThreads, 0, s>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
-                                                 d.leaf_band, d.leaf_loc_off, d.leaf_rank, d.leaf_U_off, d.ops, d.loc, d.pts_t,
-                                                 d.v_t, d.x_t, d.qk2_t, d.D_t, d.perm, y, d.kc, d.kernel_mode,
-                                                 far ? mask : (mask & 1u));
+  mark(EV_L2L, s);
+  if (far && near && !fork) launch_p2p();  // no side stream: sequential
+  if (fork) cudaStreamWaitEvent(s, d.ev_join, 0);
+  mark(EV_JOIN, s);
+  combine_kernel<<<d.nleaves, kCombineThreads, 0, s>>>(d.leaf_begin, d.leaf_end, d.leaf_loc_off, d.leaf_rank,
+                                                        d.leaf_U_off, d.ops, d.loc, d.phi, d.x_t, d.qk2_t, d.D_t,
+                                                        d.perm, y, d.kernel_mode, near ? 1 : 0, far ? 1 : 0);
   ++d.launches;
-  mark(6);
+  mark(EV_END, s);
   if (d.prof) d.prof_pending = true;
   return ck(cudaGetLastError(), err, "matvec launch") ? DAFMM_OK : DAFMM_ECUDA;
 }

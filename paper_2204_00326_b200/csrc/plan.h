@@ -13,6 +13,8 @@
 
 namespace dafmm {
 
+static_assert(kNumBandCodes <= 48, "dafmm_stats_t band arrays hold 48 codes");
+
 using zd = std::complex<double>;
 
 struct Options {
@@ -95,9 +97,12 @@ struct Packed {
   std::vector<int32_t> m2l_src_ptr;  // targets + 1
   std::vector<int64_t> m2l_src_off;  // per source entry: multipole offset
   std::vector<int32_t> m2l_src_cnt;  // per source entry: r_o
+  std::vector<int64_t> m2l_stream_ptr;  // targets + 1: each target's source-pivot stream
+  std::vector<int32_t> m2l_stream_idx;  // multipole slot of every pivot of the stream
   // band-uniform segments of each target's source list: items of target
-  // t are [m2l_item_ptr[t], m2l_item_ptr[t+1]); item i covers source entries
-  // [m2l_item_begin[i], m2l_item_end[i]) whose point pairs all lie in band m2l_item_code[i]
+  // t are [m2l_item_ptr[t], m2l_item_ptr[t+1]); item i covers the pivots
+  // [m2l_item_begin[i], m2l_item_end[i]) of t's concatenated source stream, whose pairs with
+  // t's pivots all lie in band m2l_item_code[i]
   std::vector<int32_t> m2l_item_ptr;   // targets + 1
   std::vector<int32_t> m2l_item_code, m2l_item_begin, m2l_item_end;
   std::vector<int64_t> m2l_band_entries = std::vector<int64_t>(kNumBandCodes, 0);

@@ -115,13 +115,13 @@ struct LU {
 
 struct Ctx {
   const Plan& p;
-  KernelConsts kc;
-  explicit Ctx(const Plan& plan) : p(plan), kc(make_kernel_consts(plan.kappa)) {}
+  double k2;
+  explicit Ctx(const Plan& plan) : p(plan), k2(plan.kappa * plan.kappa) {}
   // H0^(1)(kappa |x_i - x_j|), i != j (original indices)
   zd H(int32_t i, int32_t j) const {
     double dx = p.pts[2 * (size_t)i] - p.pts[2 * (size_t)j];
     double dy = p.pts[2 * (size_t)i + 1] - p.pts[2 * (size_t)j + 1];
-    cplx h = h0(dx * dx + dy * dy, kc);
+    cplx h = h0(k2 * (dx * dx + dy * dy));
     return zd(h.re, h.im);
   }
   // K_ij = G(x_i, x_j) w_j: the discretised volume potential compressed by the NCA (reading R9)
@@ -570,8 +570,8 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
   pk.D_t.resize(n);
   for (int64_t t = 0; t < n; ++t) {
     int32_t o = P.perm[t];
-    pk.pts_t[2 * t] = P.pts[2 * (size_t)o];
-    pk.pts_t[2 * t + 1] = P.pts[2 * (size_t)o + 1];
+    pk.pts_t[2 * t] = P.kappa * P.pts[2 * (size_t)o];  // kappa-scaled (the kernels evaluate H0 of z^2)
+    pk.pts_t[2 * t + 1] = P.kappa * P.pts[2 * (size_t)o + 1];
     pk.w_t[t] = P.w[o];
     pk.qk2_t[t] = P.kappa * P.kappa * P.q[o];
     pk.D_t[t] = {P.D[o].real(), P.D[o].imag()};
@@ -598,12 +598,12 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     for (size_t nd = 0; nd < P.levels[l].nodes.size(); ++nd) {
       const NodePivots& np = P.piv[l][nd];
       for (size_t k = 0; k < np.so.size(); ++k) {
-        pk.so_xy[2 * (moff[l][nd] + k)] = P.pts[2 * (size_t)np.so[k]];
-        pk.so_xy[2 * (moff[l][nd] + k) + 1] = P.pts[2 * (size_t)np.so[k] + 1];
+        pk.so_xy[2 * (moff[l][nd] + k)] = P.kappa * P.pts[2 * (size_t)np.so[k]];
+        pk.so_xy[2 * (moff[l][nd] + k) + 1] = P.kappa * P.pts[2 * (size_t)np.so[k] + 1];
       }
       for (size_t k = 0; k < np.ti.size(); ++k) {
-        pk.ti_xy[2 * (loff[l][nd] + k)] = P.pts[2 * (size_t)np.ti[k]];
-        pk.ti_xy[2 * (loff[l][nd] + k) + 1] = P.pts[2 * (size_t)np.ti[k] + 1];
+        pk.ti_xy[2 * (loff[l][nd] + k)] = P.kappa * P.pts[2 * (size_t)np.ti[k]];
+        pk.ti_xy[2 * (loff[l][nd] + k) + 1] = P.kappa * P.pts[2 * (size_t)np.ti[k] + 1];
       }
     }
   // ---- operator block descriptors; blocks are filled in parallel afterwards ----
@@ -750,36 +750,51 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       codes[i][e] = choose_band(P.kappa * std::sqrt(lo), P.kappa * std::sqrt(hi));
     }
   }
+  // targets in order of decreasing work (the persistent M2L kernel takes them in this order)
+  std::vector<int64_t> tcost(tg.size(), 0);
+  for (size_t i = 0; i < tg.size(); ++i) {
+    int64_t so = 0;
+    for (int sn : tg[i].src) so += (int64_t)P.piv[tg[i].level][sn].so.size();
+    tcost[i] = so * (int64_t)P.piv[tg[i].level][tg[i].node].ti.size();
+  }
+  std::vector<size_t> torder(tg.size());
+  std::iota(torder.begin(), torder.end(), 0);
+  std::stable_sort(torder.begin(), torder.end(), [&](size_t a, size_t b) { return tcost[a] > tcost[b]; });
   pk.m2l_src_ptr.push_back(0);
   pk.m2l_item_ptr.push_back(0);
-  for (size_t i = 0; i < tg.size(); ++i) {
+  pk.m2l_stream_ptr.push_back(0);
+  for (size_t i : torder) {
     const int l = tg[i].level;
     const int ri = (int)P.piv[l][tg[i].node].ti.size();
     std::vector<int> order(tg[i].src.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return codes[i][a] < codes[i][b]; });
     int prev = -1;
+    int32_t cum = 0;  // offset in the target's source-pivot stream
     for (int e : order) {
       int sn = tg[i].src[e];
       int ro = (int)P.piv[l][sn].so.size();
       int code = codes[i][e];
       if (code != prev) {
-        if (prev >= 0) pk.m2l_item_end.push_back((int32_t)pk.m2l_src_off.size());
+        if (prev >= 0) pk.m2l_item_end.push_back(cum);
         pk.m2l_item_code.push_back(code);
-        pk.m2l_item_begin.push_back((int32_t)pk.m2l_src_off.size());
+        pk.m2l_item_begin.push_back(cum);
         prev = code;
       }
       pk.m2l_src_off.push_back(moff[l][sn]);
       pk.m2l_src_cnt.push_back(ro);
+      for (int k = 0; k < ro; ++k) pk.m2l_stream_idx.push_back((int32_t)(moff[l][sn] + k));
+      cum += ro;
       pk.m2l_entries += (int64_t)ri * ro;
       pk.m2l_band_entries[code] += (int64_t)ri * ro;
       ++pk.m2l_pairs;
     }
-    pk.m2l_item_end.push_back((int32_t)pk.m2l_src_off.size());
+    pk.m2l_item_end.push_back(cum);
     pk.m2l_item_ptr.push_back((int32_t)pk.m2l_item_code.size());
     pk.m2l_loc_off.push_back(loff[l][tg[i].node]);
     pk.m2l_rows.push_back(ri);
     pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
+    pk.m2l_stream_ptr.push_back((int64_t)pk.m2l_stream_idx.size());
   }
   // leaves: near field (own leaf first: the only segment with i == j pairs), L2P
   auto bbox = [&](const Box& B, double* bb) {
@@ -818,7 +833,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     }
     pairs -= (B.end - B.begin);
     pk.p2p_pairs += pairs;
-    int band = zmax <= dafmm_fit::Z_NEAR ? kBandNear : kBandGeneric;
+    int band = zmax <= 8.0 ? kBandNear8 : kBandGeneric;
     pk.leaf_band.push_back(band);
     pk.p2p_band_entries[band] += pairs;
     pk.near_ptr.push_back((int32_t)pk.near_begin.size());

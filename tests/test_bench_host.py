@@ -57,11 +57,13 @@ def test_clock_summary_flags_throttle():
     assert bench.summarize_clocks([])["reasons"] == ["no samples"]
 
 
-def test_roofline_entry_picks_dominant_kernel():
+def test_roofline_entry_overlap_span():
     stats = {"p2p_pairs": 1000, "m2l_entries": 4000}
-    inputs = {"fp64_tflops_measured": 34.0, "kernels": {"m2l": {"fp64_flops_per_entry": 100.0,
-                                                                "dram_bytes_per_launch": 123}}}
-    r = bench.roofline_entry({"near": 1.0, "m2l": 4.0}, 2, stats, inputs)
-    assert r["kernel"] == "m2l" and r["bound"] == "alu" and r["unit"] == "TFLOP/s"
-    assert r["achieved"] == pytest.approx(4000 * 100.0 / 2e-3 / 1e12)
-    assert r["frac"] == pytest.approx(r["achieved"] / 34.0) and r["traffic"] == 123
+    inputs = {"fp64_tflops_measured": 34.0,
+              "kernels": {"m2l": {"fp64_flops_per_entry": 100.0, "dram_bytes_per_launch": 123},
+                          "p2p": {"fp64_flops_per_entry": 50.0, "dram_bytes_per_launch": 7}}}
+    r = bench.roofline_entry({"near": 1.0, "m2l": 4.0, "overlap_span": 5.0}, 2, stats, inputs)
+    assert r["bound"] == "alu" and r["unit"] == "TFLOP/s" and r["span_ms"] == 2.5
+    assert r["achieved"] == pytest.approx((4000 * 100.0 + 1000 * 50.0) / 2.5e-3 / 1e12)
+    assert r["frac"] == pytest.approx(r["achieved"] / 34.0) and r["traffic"] == 130
+    assert r["kernels"]["m2l"]["launch_ms_concurrent"] == 2.0
