@@ -17,10 +17,12 @@ enum ProfEvent { EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_NEAR0, EV
 
 struct DevBatch {
   int items = 0;
+  bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;
-  int64_t* mat_off = nullptr;
+  int64_t* item_mat_off = nullptr;
+  int32_t* item_cols = nullptr;
   int64_t* src_off = nullptr;
   int32_t* src_cols = nullptr;
 };
@@ -29,8 +31,9 @@ struct DevPlan {
   int64_t n = 0;
   int kernel_mode = 0;
   cudaStream_t stream = nullptr;   // the caller's stream (dafmm_set_stream)
-  cudaStream_t side = nullptr;     // internal stream: P2P runs here, concurrent with the far field
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t s_far = nullptr;    // internal high-priority stream: far field (P2M ... L2L)
+  cudaStream_t s_near = nullptr;   // internal low-priority stream: P2P, concurrent with the far field
+  cudaEvent_t ev_fork = nullptr, ev_join_far = nullptr, ev_join_near = nullptr;
   // per tree point
   double2* pts_t = nullptr;  // kappa-scaled coordinates
   double* w_t = nullptr;

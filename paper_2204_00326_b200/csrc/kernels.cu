@@ -42,48 +42,109 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ perm, const
   }
 }
 
-// ---- batched translation: dst[dst_off + r] (+)= sum_terms Mat (rows x cols, col-major) src ----
-// One warp per item; lanes own rows (coalesced column reads of the operator block).  Columns
-// are consumed 4 at a time into 4 independent accumulators so 8 loads are in flight per lane
-// and the FMA chains do not serialise on one accumulator (the stage is HBM-bound).
+// ---- batched translation (P2M, M2M, L2L): dst[dst_off + r] (+)= sum_c M[r][c] s_c -------------
+// One warp per item.  The item's operator is one row-major block (its terms side by side), so
+// every row is a contiguous run: the lanes first gather the item's sources for columns
+// c = lane + 32 k (k < kTCK) into registers, then each row is one coalesced pass over the
+// row (all 32 lanes busy) and a warp reduction.  Items wider than 32 kTCK columns are handled
+// in column blocks.  HBM-bound: every operator element is read once per matvec.
+constexpr int kTCK = 8;
 __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
-                                 const int32_t* __restrict__ term_ptr, const int64_t* __restrict__ mat_off,
-                                 const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
-                                 const double2* __restrict__ ops, const double2* __restrict__ src,
-                                 double2* __restrict__ dst, int accumulate) {
+                                 const int64_t* __restrict__ item_mat_off, const int32_t* __restrict__ item_cols,
+                                 const int32_t* __restrict__ term_ptr, const int64_t* __restrict__ src_off,
+                                 const int32_t* __restrict__ src_cols, const double2* __restrict__ ops,
+                                 const double2* __restrict__ src, double2* __restrict__ dst, int accumulate) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= items) return;
-  const int rows = dst_rows[warp];
+  const int R = dst_rows[warp], C = item_cols[warp];
   const int tb = term_ptr[warp], te = term_ptr[warp + 1];
   const int64_t doff = dst_off[warp];
-  for (int r0 = 0; r0 < rows; r0 += 32) {
-    const int r = r0 + lane;
-    if (r >= rows) break;
+  const double2* M = ops + item_mat_off[warp];
+  for (int cb = 0; cb < C; cb += 32 * kTCK) {
+    double2 v[kTCK];
+#pragma unroll
+    for (int k = 0; k < kTCK; ++k) v[k] = make_double2(0.0, 0.0);
+    int cs = 0;
+    for (int t = tb; t < te; ++t) {  // sources of the columns this lane holds
+      const int ce = cs + src_cols[t];
+      if (ce > cb && cs < cb + 32 * kTCK) {
+        const double2* sv = src + src_off[t] - cs;
+#pragma unroll
+        for (int k = 0; k < kTCK; ++k) {
+          const int c = cb + lane + 32 * k;
+          if (c >= cs && c < ce) v[k] = ld2(sv + c);
+        }
+      }
+      cs = ce;
+    }
+    const int kmax = min(kTCK, (C - cb + 31) / 32);
+    for (int r = 0; r < R; ++r) {
+      const double2* row = M + (int64_t)r * C + cb + lane;
+      double ar = 0.0, ai = 0.0;
+#pragma unroll
+      for (int k = 0; k < kTCK; ++k) {
+        if (k < kmax && cb + lane + 32 * k < C) {
+          const double2 m = ld2(row + 32 * k);
+          ar = fma(m.x, v[k].x, fma(-m.y, v[k].y, ar));
+          ai = fma(m.x, v[k].y, fma(m.y, v[k].x, ai));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+      }
+      if (lane == (r & 31)) {
+        double2 o = make_double2(ar, ai);
+        if (accumulate || cb > 0) {
+          const double2 p = dst[doff + r];
+          o.x += p.x;
+          o.y += p.y;
+        }
+        dst[doff + r] = o;
+      }
+    }
+  }
+}
+
+// Narrow items (few columns, e.g. directional L2L with 2 parent cones): one warp per item,
+// lanes own rows and walk their contiguous row, 4 columns per step into 4 accumulators.
+__global__ void translate_rows_kernel(int items, const int64_t* __restrict__ dst_off,
+                                      const int32_t* __restrict__ dst_rows, const int64_t* __restrict__ item_mat_off,
+                                      const int32_t* __restrict__ item_cols, const int32_t* __restrict__ term_ptr,
+                                      const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
+                                      const double2* __restrict__ ops, const double2* __restrict__ src,
+                                      double2* __restrict__ dst, int accumulate) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= items) return;
+  const int R = dst_rows[warp], C = item_cols[warp];
+  const int tb = term_ptr[warp], te = term_ptr[warp + 1];
+  const int64_t doff = dst_off[warp];
+  for (int r = lane; r < R; r += 32) {
+    const double2* row = ops + item_mat_off[warp] + (int64_t)r * C;
     double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
+    int cs = 0;
     for (int t = tb; t < te; ++t) {
-      const double2* M = ops + mat_off[t] + r;
+      const int n = src_cols[t];
       const double2* sv = src + src_off[t];
-      const int cols = src_cols[t];
+      const double2* m = row + cs;
       int c = 0;
-      for (; c + 4 <= cols; c += 4) {
-        double2 m[4], v[4];
+      for (; c + 4 <= n; c += 4) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          m[q] = ld2(M + (int64_t)(c + q) * rows);
-          v[q] = ld2(sv + c + q);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          ar[q] = fma(m[q].x, v[q].x, fma(-m[q].y, v[q].y, ar[q]));
-          ai[q] = fma(m[q].x, v[q].y, fma(m[q].y, v[q].x, ai[q]));
+          const double2 a = ld2(m + c + q), b = ld2(sv + c + q);
+          ar[q] = fma(a.x, b.x, fma(-a.y, b.y, ar[q]));
+          ai[q] = fma(a.x, b.y, fma(a.y, b.x, ai[q]));
         }
       }
-      for (; c < cols; ++c) {
-        const double2 m = ld2(M + (int64_t)c * rows), v = ld2(sv + c);
-        ar[0] = fma(m.x, v.x, fma(-m.y, v.y, ar[0]));
-        ai[0] = fma(m.x, v.y, fma(m.y, v.x, ai[0]));
+      for (; c < n; ++c) {
+        const double2 a = ld2(m + c), b = ld2(sv + c);
+        ar[0] = fma(a.x, b.x, fma(-a.y, b.y, ar[0]));
+        ai[0] = fma(a.x, b.y, fma(a.y, b.x, ai[0]));
       }
+      cs += n;
     }
     double2 o = make_double2((ar[0] + ar[1]) + (ar[2] + ar[3]), (ai[0] + ai[1]) + (ai[2] + ai[3]));
     if (accumulate) {
@@ -486,20 +547,46 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* sh) {
   return r;
 }
 
-// part[b * stride + i] = sum over the block's slice of conj(V_i) w, i < k
+// part[bx * stride + i] = sum over block bx's slice of conj(V_i) w for the kMD vectors
+// i = blockIdx.y * kMD + g of this block: w is read once per group of kMD basis vectors and
+// each thread keeps kMD complex partial sums (one pass, no per-vector barriers).
+constexpr int kMD = 8;
 __global__ void multidot_kernel(int64_t n, int k, const double2* __restrict__ V, const double2* __restrict__ w,
                                 double2* __restrict__ part, int stride) {
-  __shared__ double2 sh[32];
-  for (int i = 0; i < k; ++i) {
-    const double2* v = V + (int64_t)i * n;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-      double2 a = ld2(v + e), b = ld2(w + e);
-      acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
-      acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+  __shared__ double2 sh[kMD][kVecThreads / 32];
+  const int i0 = blockIdx.y * kMD;
+  const int nv = min(kMD, k - i0);
+  double ar[kMD], ai[kMD];
+#pragma unroll
+  for (int g = 0; g < kMD; ++g) ar[g] = ai[g] = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const double2 b = ld2(w + e);
+#pragma unroll
+    for (int g = 0; g < kMD; ++g) {
+      if (g < nv) {
+        const double2 a = ld2(V + (int64_t)(i0 + g) * n + e);
+        ar[g] = fma(a.x, b.x, fma(a.y, b.y, ar[g]));
+        ai[g] = fma(a.x, b.y, fma(-a.y, b.x, ai[g]));
+      }
     }
-    double2 s = block_sum2(acc, sh);
-    if (threadIdx.x == 0) part[(int64_t)blockIdx.x * stride + i] = s;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int g = 0; g < kMD; ++g) {
+    for (int o = 16; o > 0; o >>= 1) {
+      ar[g] += __shfl_down_sync(0xffffffffu, ar[g], o);
+      ai[g] += __shfl_down_sync(0xffffffffu, ai[g], o);
+    }
+    if (lane == 0) sh[g][wid] = make_double2(ar[g], ai[g]);
+  }
+  __syncthreads();
+  if (threadIdx.x < nv) {
+    double sr = 0.0, si = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+      sr += sh[threadIdx.x][q].x;
+      si += sh[threadIdx.x][q].y;
+    }
+    part[(int64_t)blockIdx.x * stride + i0 + threadIdx.x] = make_double2(sr, si);
   }
 }
 
@@ -592,17 +679,28 @@ bool alloc(DevPlan& d, T** dst, size_t count, std::string& err) {
 
 bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& err) {
   b.items = (int)h.dst_off.size();
+  // kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32 lanes
+  // and reduce across the warp; narrow ones give each lane a row
+  int64_t cols = 0;
+  for (int32_t c : h.item_cols) cols += c;
+  b.wide = b.items > 0 && cols >= 48 * (int64_t)b.items;
   return upload(d, &b.dst_off, h.dst_off, err) && upload(d, &b.dst_rows, h.dst_rows, err) &&
-         upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.mat_off, h.mat_off, err) &&
+         upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.item_mat_off, h.item_mat_off, err) &&
+         upload(d, &b.item_cols, h.item_cols, err) &&
          upload(d, &b.src_off, h.src_off, err) && upload(d, &b.src_cols, h.src_cols, err);
 }
 
-int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate) {
+int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate,
+                     cudaStream_t st) {
   if (b.items == 0) return 0;
   int threads = 256;
   int blocks = (b.items * 32 + threads - 1) / threads;
-  translate_kernel<<<blocks, threads, 0, d.stream>>>(b.items, b.dst_off, b.dst_rows, b.term_ptr, b.mat_off, b.src_off,
-                                                     b.src_cols, d.ops, src, dst, accumulate);
+  if (b.wide)
+    translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                 b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
+  else
+    translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                      b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
   return 1;
 }
 
@@ -651,9 +749,13 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
          ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
     d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
   }
-  ok = ok && ck(cudaStreamCreateWithFlags(&d.side, cudaStreamNonBlocking), err, "side stream") &&
+  int prio_lo = 0, prio_hi = 0;
+  ok = ok && ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), err, "stream priorities") &&
+       ck(cudaStreamCreateWithPriority(&d.s_far, cudaStreamNonBlocking, prio_hi), err, "far stream") &&
+       ck(cudaStreamCreateWithPriority(&d.s_near, cudaStreamNonBlocking, prio_lo), err, "near stream") &&
        ck(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming), err, "fork event") &&
-       ck(cudaEventCreateWithFlags(&d.ev_join, cudaEventDisableTiming), err, "join event") &&
+       ck(cudaEventCreateWithFlags(&d.ev_join_far, cudaEventDisableTiming), err, "join event") &&
+       ck(cudaEventCreateWithFlags(&d.ev_join_near, cudaEventDisableTiming), err, "join event") &&
        alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 1, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
        alloc(d, &d.loc, pk.n_loc, err) && alloc(d, &d.host_stage, 2 * plan.n, err);
   if (!ok) return DAFMM_ECUDA;
@@ -661,11 +763,16 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
 }
 
 void free_plan(DevPlan& d) {
-  if (d.ev_fork) cudaEventDestroy(d.ev_fork);
-  if (d.ev_join) cudaEventDestroy(d.ev_join);
-  if (d.side) cudaStreamDestroy(d.side);
-  d.ev_fork = d.ev_join = nullptr;
-  d.side = nullptr;
+  for (cudaEvent_t* e : {&d.ev_fork, &d.ev_join_far, &d.ev_join_near})
+    if (*e) {
+      cudaEventDestroy(*e);
+      *e = nullptr;
+    }
+  for (cudaStream_t* st : {&d.s_far, &d.s_near})
+    if (*st) {
+      cudaStreamDestroy(*st);
+      *st = nullptr;
+    }
   for (auto& e : d.prof_ev)
     if (e) {
       cudaEventDestroy(e);
@@ -714,58 +821,61 @@ int harvest_profile(DevPlan& d, std::string& err) {
 // concurrently with the far field (P2M, M2M, M2L, L2L) on the handle's stream; the combine
 // (L2P + identity + scatter) joins both.  No host synchronisation.
 int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::string& err) {
-  cudaStream_t s = d.stream;
+  const cudaStream_t s = d.stream;
   if (d.prof && harvest_profile(d, err) != DAFMM_OK) return DAFMM_ECUDA;
   auto mark = [&](int e, cudaStream_t st) {
     if (d.prof) cudaEventRecord(d.prof_ev[e], st);
   };
   const bool near = mask & 1u;
   const bool far = (mask & 2u) && d.n_mult > 0;
-  const bool fork = near && far && d.side != nullptr;
+  const bool fork = near && far && d.s_far != nullptr;
+  // fork: the far field runs on a high-priority internal stream so its short, latency-bound
+  // translation kernels and the persistent M2L CTAs are scheduled ahead of the pending P2P
+  // CTAs (low-priority stream) as SM slots free up; both join back on the caller's stream
+  const cudaStream_t fs = fork ? d.s_far : s, ns = fork ? d.s_near : s;
   mark(EV_START, s);
   gather_kernel<<<grid_for(d.n, 256, 148 * 16), 256, 0, s>>>(d.n, d.perm, d.w_t, x, d.x_t, d.v_t);
   ++d.launches;
   mark(EV_FORK, s);
-  cudaStream_t ns = s;  // stream of the P2P kernel
   if (fork) {
     cudaEventRecord(d.ev_fork, s);
-    cudaStreamWaitEvent(d.side, d.ev_fork, 0);
-    ns = d.side;
+    cudaStreamWaitEvent(d.s_far, d.ev_fork, 0);
+    cudaStreamWaitEvent(d.s_near, d.ev_fork, 0);
   }
-  auto launch_p2p = [&]() {
-    mark(EV_NEAR0, ns);
-    if (near) {
-      p2p_kernel<<<d.nleaves, kNearThreads, 0, ns>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
-                                                     d.leaf_band, d.pts_t, d.v_t, d.phi);
-      ++d.launches;
-    }
-    mark(EV_NEAR1, ns);
-  };
-  if (fork || !far) launch_p2p();  // concurrent with the far field, or near only
-  if (fork) cudaEventRecord(d.ev_join, d.side);
   if (far) {
-    cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, s);
-    cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, s);
-    if (d.m2l_targets > 0) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), s);
+    cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, fs);
+    cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, fs);
+    if (d.m2l_targets > 0) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), fs);
   }
-  mark(EV_P2M, s);
-  if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0);  // P2M
-  mark(EV_M2M, s);
+  mark(EV_P2M, fs);
+  if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0, fs);  // P2M
+  mark(EV_M2M, fs);
   if (far)
-    for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0);  // M2M
-  mark(EV_M2L, s);
+    for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
+  mark(EV_M2L, fs);
   if (far && d.m2l_targets > 0) {  // M2L, persistent CTAs
-    m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, s>>>(d.m2l_targets, d.m2l_ticket, d.m2l_loc_off, d.m2l_rows,
-                                                   d.m2l_stream_ptr, d.m2l_stream_idx, d.m2l_item_ptr, d.m2l_item_code,
-                                                   d.m2l_item_begin, d.m2l_item_end, d.ti_xy, d.so_xy,
-                                                   d.mult, d.loc);
+    m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, fs>>>(d.m2l_targets, d.m2l_ticket, d.m2l_loc_off, d.m2l_rows,
+                                                    d.m2l_stream_ptr, d.m2l_stream_idx, d.m2l_item_ptr, d.m2l_item_code,
+                                                    d.m2l_item_begin, d.m2l_item_end, d.ti_xy, d.so_xy,
+                                                    d.mult, d.loc);
     ++d.launches;
   }
   if (far)
-    for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1);  // L2L
-  mark(EV_L2L, s);
-  if (far && near && !fork) launch_p2p();  // no side stream: sequential
-  if (fork) cudaStreamWaitEvent(s, d.ev_join, 0);
+    for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1, fs);  // L2L
+  mark(EV_L2L, fs);
+  mark(EV_NEAR0, ns);
+  if (near) {  // P2P
+    p2p_kernel<<<d.nleaves, kNearThreads, 0, ns>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
+                                                   d.leaf_band, d.pts_t, d.v_t, d.phi);
+    ++d.launches;
+  }
+  mark(EV_NEAR1, ns);
+  if (fork) {
+    cudaEventRecord(d.ev_join_far, d.s_far);
+    cudaEventRecord(d.ev_join_near, d.s_near);
+    cudaStreamWaitEvent(s, d.ev_join_far, 0);
+    cudaStreamWaitEvent(s, d.ev_join_near, 0);
+  }
   mark(EV_JOIN, s);
   combine_kernel<<<d.nleaves, kCombineThreads, 0, s>>>(d.leaf_begin, d.leaf_end, d.leaf_loc_off, d.leaf_rank,
                                                         d.leaf_U_off, d.ops, d.loc, d.phi, d.x_t, d.qk2_t, d.D_t,
@@ -836,7 +946,8 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
       ++iters;
       // CGS2: two passes of h = V^H w, w -= V h
       for (int pass = 0; pass < 2; ++pass) {
-        multidot_kernel<<<nb, kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_w, d.gm_part, stride);
+        multidot_kernel<<<dim3(nb, (j + 1 + kMD - 1) / kMD), kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_w, d.gm_part,
+                                                                                 stride);
         reduce_parts_kernel<<<1, 256, 0, s>>>(nb, j + 1, d.gm_part, stride, d.gm_h + pass * (m + 2));
         combine_kernel<<<nb, kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_h + pass * (m + 2), -1.0, d.gm_w);
       }

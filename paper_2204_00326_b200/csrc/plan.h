@@ -80,13 +80,17 @@ struct Packed {
   std::vector<double> so_xy, ti_xy;  // 2 per multipole / local slot
   std::vector<cplx> ops;             // all operator blocks, column-major
   // generic translation batches: item -> [term_ptr[i], term_ptr[i+1]) terms
+  // item i: dst[dst_off + r] (+)= sum_c M[r][c] s_c, M row-major (rows x item_cols) at
+  // ops[item_mat_off]; its columns are the terms [term_ptr[i], term_ptr[i+1]) side by side,
+  // term t taking src_cols[t] consecutive sources from src_off[t]
   struct Batch {
-    std::vector<int64_t> dst_off;     // per item
-    std::vector<int32_t> dst_rows;    // per item
-    std::vector<int32_t> term_ptr;    // items + 1
-    std::vector<int64_t> mat_off;     // per term (into ops)
-    std::vector<int64_t> src_off;     // per term
-    std::vector<int32_t> src_cols;    // per term
+    std::vector<int64_t> dst_off;       // per item
+    std::vector<int32_t> dst_rows;      // per item
+    std::vector<int64_t> item_mat_off;  // per item (into ops)
+    std::vector<int32_t> item_cols;     // per item
+    std::vector<int32_t> term_ptr;      // items + 1
+    std::vector<int64_t> src_off;       // per term
+    std::vector<int32_t> src_cols;      // per term
   };
   Batch p2m;                         // leaf: dst multipole, src tree points (v), 1 term
   std::vector<Batch> m2m;            // per parent level, processed from fine to coarse

@@ -607,17 +607,46 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       }
     }
   // ---- operator block descriptors; blocks are filled in parallel afterwards ----
+  // Translation items (P2M, M2M, L2L) store one row-major block per item: the terms' blocks side
+  // by side (row stride = the item's total column count), so the translate kernel reads each
+  // row as one contiguous run.  U (L2P) stays column-major (one point per thread in combine).
   struct Job {
     int kind;  // 0: V (P2M), 1: T (M2M), 2: C (L2L), 3: U (L2P)
     int level, node, child;  // node at `level`, child node at level + 1
-    int64_t off;
+    int64_t off;             // block start
+    int64_t stride;          // row stride (row-major item block); 0: column-major
+    int col_start;           // first column of this term inside the item block
   };
   std::vector<Job> jobs;
   int64_t ops_len = 0;
   auto add_job = [&](int kind, int l, int nd, int ch, int64_t len) {
-    jobs.push_back({kind, l, nd, ch, ops_len});
+    jobs.push_back({kind, l, nd, ch, ops_len, 0, 0});
     ops_len += len;
     return jobs.back().off;
+  };
+  // one translation item: rows x (sum of term columns); terms = (child/parent node, src offset, cols)
+  struct Term {
+    int node, child;
+    int64_t src_off;
+    int cols;
+  };
+  auto add_item = [&](Packed::Batch& bt, int kind, int l, int64_t dst_off, int rows, const std::vector<Term>& terms) {
+    int C = 0;
+    for (const Term& t : terms) C += t.cols;
+    const int64_t off = ops_len;
+    ops_len += (int64_t)rows * C;
+    bt.dst_off.push_back(dst_off);
+    bt.dst_rows.push_back(rows);
+    bt.item_mat_off.push_back(off);
+    bt.item_cols.push_back(C);
+    bt.term_ptr.push_back((int32_t)bt.src_off.size());
+    int cs = 0;
+    for (const Term& t : terms) {
+      jobs.push_back({kind, l, t.node, t.child, off, C, cs});
+      bt.src_off.push_back(t.src_off);
+      bt.src_cols.push_back(t.cols);
+      cs += t.cols;
+    }
   };
   const Level& leaf = P.levels[L];
   auto child_nodes = [&](int l, int nd, std::vector<int>& out) {
@@ -639,15 +668,9 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     int ro = (int)P.piv[L][nd].so.size();
     int m = B.end - B.begin;
     if (ro == 0) continue;
-    int64_t off = add_job(0, L, (int)nd, -1, (int64_t)ro * m);
-    pk.p2m.dst_off.push_back(moff[L][nd]);
-    pk.p2m.dst_rows.push_back(ro);
-    pk.p2m.term_ptr.push_back((int32_t)pk.p2m.mat_off.size());
-    pk.p2m.mat_off.push_back(off);
-    pk.p2m.src_off.push_back(B.begin);
-    pk.p2m.src_cols.push_back(m);
+    add_item(pk.p2m, 0, L, moff[L][nd], ro, {Term{(int)nd, -1, (int64_t)B.begin, m}});
   }
-  pk.p2m.term_ptr.push_back((int32_t)pk.p2m.mat_off.size());
+  pk.p2m.term_ptr.push_back((int32_t)pk.p2m.src_off.size());
   // M2M, fine to coarse
   std::vector<int> kids;
   pk.m2m.clear();
@@ -658,22 +681,14 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       int ro = (int)P.piv[l][nd].so.size();
       if (ro == 0) continue;
       child_nodes(l, (int)nd, kids);
-      bool any = false;
+      std::vector<Term> terms;
       for (int c : kids) {
         int rc = (int)P.piv[l + 1][c].so.size();
-        if (rc == 0) continue;
-        if (!any) {
-          bt.dst_off.push_back(moff[l][nd]);
-          bt.dst_rows.push_back(ro);
-          bt.term_ptr.push_back((int32_t)bt.mat_off.size());
-          any = true;
-        }
-        bt.mat_off.push_back(add_job(1, l, (int)nd, c, (int64_t)ro * rc));
-        bt.src_off.push_back(moff[l + 1][c]);
-        bt.src_cols.push_back(rc);
+        if (rc > 0) terms.push_back({(int)nd, c, moff[l + 1][c], rc});
       }
+      if (!terms.empty()) add_item(bt, 1, l, moff[l][nd], ro, terms);
     }
-    bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+    bt.term_ptr.push_back((int32_t)bt.src_off.size());
     pk.m2m.push_back(std::move(bt));
   }
   // L2L, coarse to fine: items are the child nodes, terms the parent nodes listing them
@@ -681,27 +696,21 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
   for (int l = 1; l <= L - 1; ++l) {
     const Level& lv = P.levels[l];
     const Level& ch = P.levels[l + 1];
-    std::vector<std::vector<std::pair<int, int>>> incoming(ch.nodes.size());  // child -> (parent node)
+    std::vector<std::vector<int>> incoming(ch.nodes.size());  // child -> parent nodes
     for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
       if (P.piv[l][nd].ti.empty()) continue;
       child_nodes(l, (int)nd, kids);
-      for (int c : kids) incoming[c].push_back({(int)nd, c});
+      for (int c : kids) incoming[c].push_back((int)nd);
     }
     Packed::Batch bt;
     for (size_t c = 0; c < ch.nodes.size(); ++c) {
       int rc = (int)P.piv[l + 1][c].ti.size();
       if (rc == 0 || incoming[c].empty()) continue;
-      bt.dst_off.push_back(loff[l + 1][c]);
-      bt.dst_rows.push_back(rc);
-      bt.term_ptr.push_back((int32_t)bt.mat_off.size());
-      for (auto& pr : incoming[c]) {
-        int rp = (int)P.piv[l][pr.first].ti.size();
-        bt.mat_off.push_back(add_job(2, l, pr.first, (int)c, (int64_t)rc * rp));
-        bt.src_off.push_back(loff[l][pr.first]);
-        bt.src_cols.push_back(rp);
-      }
+      std::vector<Term> terms;
+      for (int pn : incoming[c]) terms.push_back({pn, (int)c, loff[l][pn], (int)P.piv[l][pn].ti.size()});
+      add_item(bt, 2, l, loff[l + 1][c], rc, terms);
     }
-    bt.term_ptr.push_back((int32_t)bt.mat_off.size());
+    bt.term_ptr.push_back((int32_t)bt.src_off.size());
     pk.l2l.push_back(std::move(bt));
   }
   // M2L targets (all levels, one launch).  Each target's source nodes are
@@ -885,7 +894,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       for (size_t c = 0; c < cols.size(); ++c) {
         for (int a = 0; a < r; ++a) rhs[a] = cx.H(np.to[a], cols[c]);
         lu.solve(rhs.data());
-        for (int a = 0; a < r; ++a) out[(size_t)c * r + a] = {rhs[a].real(), rhs[a].imag()};
+        for (int a = 0; a < r; ++a) out[(size_t)a * J.stride + J.col_start + c] = {rhs[a].real(), rhs[a].imag()};
       }
     } else {
       // U~ = H(t, si) H(ti, si)^{-1}: rows = t (leaf points or child's ti), cols = ti.
@@ -912,7 +921,10 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       for (int a = 0; a < nr; ++a) {
         for (int c = 0; c < r; ++c) rhs[c] = cx.H(rows[a], np.si[c]);
         lu.solve(rhs.data());
-        for (int c = 0; c < r; ++c) out[(size_t)c * nr + a] = {rhs[c].real(), rhs[c].imag()};
+        for (int c = 0; c < r; ++c) {
+          const size_t at = J.kind == 3 ? (size_t)c * nr + a : (size_t)a * J.stride + J.col_start + c;
+          out[at] = {rhs[c].real(), rhs[c].imag()};
+        }
       }
     }
   }
