@@ -6,19 +6,19 @@
 // kappa-scaled coordinates, so no per-entry multiplication by kappa is needed.
 //
 //   near-type band Zn in {8, 12} (z <= Zn):
-//       J0 = pJ(t), Y0 = (1/pi) ln(z2/4) J0 + pR(t),  t = z2 T_SCALE - 1        (code)
+//       J0 = pJ(t), Y0 = (1/pi) ln(z2/4) J0 + pR(t),  t = z2 T_SCALE - 1
 //   far-type band [zlo, zhi]:
 //       H0 = sqrt(2/(pi z)) (P(x) + i Q(x)) e^{i(z - pi/4)},  x = A/z + B
-//       generic band [8, inf) as code; 29 narrower bands as data (FarBand, shared memory)
+//       generic band [8, inf) in PolyTable; 29 narrower bands in the FarBand table
 //   generic (any z > 0): per-lane choice of near band 8 or the generic far band.
 //
-// Evaluators are lane-blocked: one call evaluates TB independent entries in lockstep, so each
-// coefficient (a uniform-register immediate, or one broadcast shared-memory load for data
-// bands) is shared by TB FMAs and the TB Horner chains hide each other's latency.  Kernels
-// pick one band per CTA-uniform work segment (setup classifies every interaction by the exact
-// [z_min, z_max] of its point pairs), so the band never diverges inside a warp.
-// ln u uses a 128-entry table of (1/c_i, ln c_i): device callers pass its shared-memory copy
-// (load_log_table), host callers kLogTabHost.
+// Evaluators are lane-blocked: one call evaluates TB independent entries in lockstep.  Every
+// coefficient is data: a pair of doubles (two polynomials at the same argument) read with one
+// 128-bit broadcast shared-memory load that feeds 2 x TB FMAs.  Device callers pass the
+// tables' shared-memory copies (load_poly_table / load_far_bands); host callers kPolyHost /
+// kFarBandsHost.  Kernels pick one band per CTA-uniform work segment (setup classifies every
+// interaction by the exact [z_min, z_max] of its point pairs), so the band never diverges
+// inside a warp.
 #pragma once
 #include "common.h"
 #include "hankel_coeffs.h"
@@ -30,6 +30,7 @@ constexpr double kZ2Safe = 4.0;  // a z^2 inside every band's domain (z = 2), fo
 
 using dafmm_fit::FarBand;
 using dafmm_fit::Pair;
+using dafmm_fit::PolyTable;
 
 // Band codes of a work segment: 0 generic, 1 near z <= 8, 2 near z <= 12, 3 + b data band b.
 constexpr int kBandGeneric = 0;
@@ -38,9 +39,43 @@ constexpr int kBandNear12 = 2;
 constexpr int kBandFarData = 3;
 constexpr int kNumBandCodes = kBandFarData + dafmm_fit::NUM_FAR;
 
+// One coefficient pair.  On the device the tables live in shared memory and the load is a
+// volatile 128-bit LDS: otherwise the compiler hoists the loop-invariant coefficients of all
+// polynomials into registers (far more than a thread has) and spills.
+DAFMM_HD Pair ldp(const Pair* p) {
+#ifdef __CUDA_ARCH__
+  Pair r;
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(p);
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.a), "=d"(r.b) : "r"(sa));
+  return r;
+#else
+  return *p;
+#endif
+}
+
+// Two polynomials of N coefficients (pairs c[k] = (a_k, b_k)) at x[i], i < TB.
+template <int N, int TB>
+DAFMM_HD void horner2(const Pair* c, const double* x, double* a, double* b) {
+  Pair t = ldp(c + N - 1);
+#pragma unroll
+  for (int i = 0; i < TB; ++i) {
+    a[i] = t.a;
+    b[i] = t.b;
+  }
+#pragma unroll
+  for (int k = N - 2; k >= 0; --k) {
+    t = ldp(c + k);
+#pragma unroll
+    for (int i = 0; i < TB; ++i) {
+      a[i] = fma(a[i], x[i], t.a);
+      b[i] = fma(b[i], x[i], t.b);
+    }
+  }
+}
+
 // ln(z2 / 4) for TB positive normal z2.
 template <int TB>
-DAFMM_HD void log_quarter_vec(const double* z2, double* out, const Pair* logtab) {
+DAFMM_HD void log_quarter_vec(const double* z2, double* out, const PolyTable& T) {
 #ifdef __CUDA_ARCH__
   double r[TB], r2[TB], qe[TB], qo[TB], lc[TB];
   int e[TB];
@@ -50,30 +85,35 @@ DAFMM_HD void log_quarter_vec(const double* z2, double* out, const Pair* logtab)
     e[i] = (hi >> 20) - 1025;  // exponent of z2 / 4
     const int ix = (hi >> (20 - dafmm_fit::LOG_BITS)) & ((1 << dafmm_fit::LOG_BITS) - 1);
     const double m = __hiloint2double((hi & 0x000fffff) | 0x3ff00000, __double2loint(z2[i]));  // [1, 2)
-    const Pair tb = logtab[ix];
-    r[i] = fma(m, tb.a, -1.0);  // |r| <= 2^-8
+    const Pair tb = T.log_tab[ix];  // per-lane index: an ordinary (gather) shared load
+    r[i] = fma(m, tb.a, -1.0);      // |r| <= 2^-8
     lc[i] = tb.b;
     r2[i] = r[i] * r[i];
   }
-  dafmm_fit::log1p_poly<TB>(r2, qe, qo);
+  horner2<dafmm_fit::LOG1P_N, TB>(T.log1p, r2, qe, qo);
 #pragma unroll
   for (int i = 0; i < TB; ++i)
     out[i] = fma((double)e[i], dafmm_fit::LN2, lc[i] + fma(r2[i], fma(r[i], qo[i], qe[i]), r[i]));
 #else
-  (void)logtab;
+  (void)T;
   for (int i = 0; i < TB; ++i) out[i] = std::log(0.25 * z2[i]);
 #endif
 }
 
-// Near-type band ZN (z <= ZN): valid for 0 < z2 <= ZN^2.
-template <int ZN, int TB>
-DAFMM_HD void h0_near_vec(const double* z2, double* re, double* im, const Pair* logtab) {
-  using NB = dafmm_fit::NearJR<ZN>;
+// Near-type band: z <= 8 (ZN = 8) or z <= 12 (ZN = 12).  IMM: the (J0, R) coefficients of
+// band 8 as immediates instead of shared-memory loads.
+template <int ZN, int TB, bool IMM = false>
+DAFMM_HD void h0_near_vec(const double* z2, double* re, double* im, const PolyTable& T) {
+  static_assert(ZN == 8 || ZN == 12, "near bands are z <= 8 and z <= 12");
+  static_assert(!IMM || ZN == 8, "immediates exist for band 8 only");
+  constexpr double ts = ZN == 8 ? dafmm_fit::NEAR8_T_SCALE : dafmm_fit::NEAR12_T_SCALE;
+  constexpr int n = ZN == 8 ? dafmm_fit::NEAR8_N : dafmm_fit::NEAR12_N;
   double t[TB], j0[TB], rr[TB], lu[TB];
 #pragma unroll
-  for (int i = 0; i < TB; ++i) t[i] = fma(z2[i], NB::T_SCALE, -1.0);
-  NB::template eval<TB>(t, j0, rr);
-  log_quarter_vec<TB>(z2, lu, logtab);
+  for (int i = 0; i < TB; ++i) t[i] = fma(z2[i], ts, -1.0);
+  if constexpr (IMM) dafmm_fit::near8_imm<TB>(t, j0, rr);
+  else horner2<n, TB>(ZN == 8 ? T.near8 : T.near12, t, j0, rr);
+  log_quarter_vec<TB>(z2, lu, T);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
     re[i] = j0[i];
@@ -97,38 +137,47 @@ DAFMM_HD double rsqrt_sqrt(double z2) {
 #endif
 }
 
+// Negate a double when `mask` (0 or 0x80000000) is set: one XOR on the high word.
+DAFMM_HD double flip_sign(double v, unsigned mask) {
+#ifdef __CUDA_ARCH__
+  return __hiloint2double(__double2hiint(v) ^ (int)mask, __double2loint(v));
+#else
+  return mask ? -v : v;
+#endif
+}
+
 // Far-type evaluation with a caller-supplied (P, Q) evaluator: pq(x, P, Q) over TB lanes.
 template <int TB, class PQ>
-DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, double B, const PQ& pq) {
-  double y[TB], z[TB], x[TB], P[TB], Q[TB], rho[TB], rh2[TB], sp[TB], c[TB];
+DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, double B, const PQ& pq,
+                         const PolyTable& T) {
+  double y[TB], x[TB], P[TB], Q[TB], rho[TB], rh2[TB], sp[TB], c[TB];
   int quad[TB];
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    y[i] = rsqrt_sqrt(z2[i]);   // z^(-1/2)
-    const double iz = y[i] * y[i];
-    z[i] = z2[i] * iz;
-    x[i] = fma(iz, A, B);
+    y[i] = rsqrt_sqrt(z2[i]);  // z^(-1/2)
+    x[i] = fma(y[i] * y[i], A, B);
   }
   pq(x, P, Q);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
+    const double z = z2[i] * (y[i] * y[i]);
     // theta = z - pi/4 = rho + q pi/2, m = q + 1/2, rho = z - m pi/2 (two-part Cody-Waite)
-    const double qf = rint(fma(z[i], dafmm_fit::TWO_OVER_PI, -0.5));
+    const double qf = rint(fma(z, dafmm_fit::TWO_OVER_PI, -0.5));
     const double m = qf + 0.5;
-    rho[i] = fma(-m, dafmm_fit::PIO2_2, fma(-m, dafmm_fit::PIO2_1, z[i]));
+    rho[i] = fma(-m, dafmm_fit::PIO2_2, fma(-m, dafmm_fit::PIO2_1, z));
     rh2[i] = rho[i] * rho[i];
-    quad[i] = ((int)qf) & 3;
+    quad[i] = (int)qf;
   }
-  dafmm_fit::sincos_poly<TB>(rh2, sp, c);
+  horner2<dafmm_fit::SC_N, TB>(T.sincos, rh2, sp, c);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
     const double s = rho[i] * sp[i];
-    // (cos theta, sin theta) = (c, s) rotated by quadrant * pi/2
-    const bool swap = quad[i] & 1;
-    double cr = swap ? s : c[i];
-    double sr = swap ? c[i] : s;
-    if (quad[i] == 1 || quad[i] == 2) cr = -cr;
-    if (quad[i] >= 2) sr = -sr;
+    // (cos theta, sin theta) = (c, s) rotated by q pi/2: swap for odd q, then signs
+    // cos: - for q = 1, 2 (mod 4); sin: - for q = 2, 3 (mod 4)
+    const int q = quad[i];
+    const bool swap = q & 1;
+    const double cr = flip_sign(swap ? s : c[i], (unsigned)((q + 1) & 2) << 30);
+    const double sr = flip_sign(swap ? c[i] : s, (unsigned)(q & 2) << 30);
     const double amp = dafmm_fit::SQRT_2_OVER_PI * y[i];  // sqrt(2/(pi z))
     const double pr = amp * P[i], pi_ = amp * Q[i];
     re[i] = fma(pr, cr, -pi_ * sr);
@@ -136,12 +185,17 @@ DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, dou
   }
 }
 
+// (P, Q) of the generic far band [8, inf).
 template <int TB>
 struct GenericFarPQ {
-  DAFMM_HD void operator()(const double* x, double* P, double* Q) const { dafmm_fit::generic_far_pq<TB>(x, P, Q); }
+  const PolyTable& T;
+  DAFMM_HD void operator()(const double* x, double* P, double* Q) const {
+    horner2<dafmm_fit::GENERIC_FAR_N, TB>(T.generic_far, x, P, Q);
+  }
 };
 
-// (P, Q) of a data band (coefficients in shared memory on the device; n is CTA-uniform).
+// (P, Q) of a data band (coefficients in shared memory on the device; n is odd and
+// CTA-uniform, so the loop runs in coefficient pairs without a remainder).
 template <int TB>
 struct DataFarPQ {
   const FarBand* band;
@@ -153,34 +207,43 @@ struct DataFarPQ {
       P[i] = c.a;
       Q[i] = c.b;
     }
-#pragma unroll 2
-    for (int k = n - 2; k >= 0; --k) {
-      c = band->pq[k];
+#pragma unroll 1
+    for (int k = n - 2; k > 0; k -= 2) {
+      const Pair c1 = band->pq[k], c0 = band->pq[k - 1];
 #pragma unroll
       for (int i = 0; i < TB; ++i) {
-        P[i] = fma(P[i], x[i], c.a);
-        Q[i] = fma(Q[i], x[i], c.b);
+        P[i] = fma(fma(P[i], x[i], c1.a), x[i], c0.a);
+        Q[i] = fma(fma(Q[i], x[i], c1.b), x[i], c0.b);
       }
     }
   }
 };
 
-// Generic: any z > 0 (per-lane band choice; used where a segment straddles the bands).
+// Generic: any z > 0, for segments that straddle the bands (rare).  Both the near-8 and the
+// generic far evaluation run on all TB lanes (inputs clamped into each domain) and every lane
+// keeps its own: twice the work, but no divergence and no extra code per lane.
 template <int TB>
-DAFMM_HD void h0_generic_vec(const double* z2, double* re, double* im, const Pair* logtab) {
+DAFMM_HD void h0_generic_vec(const double* z2, double* re, double* im, const PolyTable& T) {
+  double zn[TB], zf[TB], nr[TB], ni[TB], fr[TB], fi[TB];
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
-    if (z2[i] <= dafmm_fit::NearJR<8>::Z2_MAX)
-      h0_near_vec<8, 1>(z2 + i, re + i, im + i, logtab);
-    else
-      h0_far_vec<1>(z2 + i, re + i, im + i, dafmm_fit::GENERIC_FAR_A, dafmm_fit::GENERIC_FAR_B, GenericFarPQ<1>());
+    zn[i] = fmin(z2[i], dafmm_fit::NEAR8_Z2_MAX);
+    zf[i] = fmax(z2[i], dafmm_fit::NEAR8_Z2_MAX);
+  }
+  h0_near_vec<8, TB>(zn, nr, ni, T);
+  h0_far_vec<TB>(zf, fr, fi, dafmm_fit::GENERIC_FAR_A, dafmm_fit::GENERIC_FAR_B, GenericFarPQ<TB>{T}, T);
+#pragma unroll
+  for (int i = 0; i < TB; ++i) {
+    const bool near = z2[i] <= dafmm_fit::NEAR8_Z2_MAX;
+    re[i] = near ? nr[i] : fr[i];
+    im[i] = near ? ni[i] : fi[i];
   }
 }
 
 // Scalar host evaluation (setup: ACA entries and operators); z2 = (kappa r)^2.
 inline cplx h0(double z2) {
   double re, im;
-  h0_generic_vec<1>(&z2, &re, &im, dafmm_fit::kLogTabHost);
+  h0_generic_vec<1>(&z2, &re, &im, dafmm_fit::kPolyHost);
   return {re, im};
 }
 
@@ -210,17 +273,22 @@ inline int choose_band(double zmin, double zmax) {
 }
 
 #ifdef __CUDACC__
-// Copy the log table into shared memory (all threads; followed by a barrier).
-__device__ __forceinline__ void load_log_table(Pair* dst) {
-  for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) dst[i] = dafmm_fit::kLogTabDev[i];
+// Copy the fixed-degree polynomial table into shared memory (all threads; then a barrier).
+__device__ __forceinline__ void load_poly_table(PolyTable& dst) {
+  static_assert(sizeof(PolyTable) % sizeof(Pair) == 0, "PolyTable is copied as pairs");
+  const Pair* src = reinterpret_cast<const Pair*>(&dafmm_fit::kPolyDev);
+  Pair* d = reinterpret_cast<Pair*>(&dst);
+  for (int i = threadIdx.x; i < (int)(sizeof(PolyTable) / sizeof(Pair)); i += blockDim.x) d[i] = src[i];
   __syncthreads();
 }
-// Copy data band b into shared memory (all threads; the caller's next barrier publishes it).
-__device__ __forceinline__ void load_far_band(FarBand* dst, int b) {
+// Copy every data band into shared memory (all threads; then a barrier).
+__device__ __forceinline__ void load_far_bands(FarBand* dst) {
   static_assert(sizeof(FarBand) % sizeof(Pair) == 0, "FarBand is copied as pairs");
-  const Pair* src = reinterpret_cast<const Pair*>(&dafmm_fit::kFarBandsDev[b]);
+  const Pair* src = reinterpret_cast<const Pair*>(dafmm_fit::kFarBandsDev);
   Pair* d = reinterpret_cast<Pair*>(dst);
-  for (int i = threadIdx.x; i < (int)(sizeof(FarBand) / sizeof(Pair)); i += blockDim.x) d[i] = src[i];
+  constexpr int n = (int)(dafmm_fit::NUM_FAR * sizeof(FarBand) / sizeof(Pair));
+  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
+  __syncthreads();
 }
 #endif
 

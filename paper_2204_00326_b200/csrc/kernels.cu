@@ -27,7 +27,8 @@ constexpr int kM2LThreads = 128;
 constexpr int kM2LStage = 320;   // M2L: staged source pivots per chunk (32 B each, double-buffered)
 constexpr int kNearStage = 320;  // near field: staged source points per chunk
 constexpr int kCombineThreads = 64;
-constexpr int kTB = 4;       // kernel entries evaluated in lockstep per thread (shared coefficients)
+constexpr int kTB = 4;
+constexpr int kBandNear8Imm = -1;  // kernel-internal: band near-8 with immediate coefficients (P2P)       // kernel entries evaluated in lockstep per thread (shared coefficients)
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
@@ -227,6 +228,8 @@ struct RunStager {
 
 // Items of an M2L target: band code and stream range, from the packed plan.
 struct M2LItems {
+  static constexpr bool kGuarded = false;  // no i == j pairs
+  static constexpr bool kNearOnly = false;
   const int32_t* code_;
   const int32_t* pb_;
   const int32_t* pe_;
@@ -238,6 +241,8 @@ struct M2LItems {
 };
 // Items of a near-field leaf: its own block [0, own) (contains i == j) and the rest.
 struct NearItems {
+  static constexpr bool kGuarded = true;   // item 0 holds the i == j pairs
+  static constexpr bool kNearOnly = true;  // bands: near-8 or generic
   int band, own, total, is, ie;
   __device__ __forceinline__ int code(int) const { return band; }
   __device__ __forceinline__ bool guard(int i) const { return i == 0; }
@@ -247,12 +252,13 @@ struct NearItems {
 
 // Band evaluator by code (compile time): generic, near 8, near 12, or a data band.
 template <int CODE>
-__device__ __forceinline__ void eval_band(const double* z2, double* re, double* im, const Pair* logtab,
+__device__ __forceinline__ void eval_band(const double* z2, double* re, double* im, const PolyTable& T,
                                           const FarBand* band) {
-  if constexpr (CODE == kBandGeneric) h0_generic_vec<kTB>(z2, re, im, logtab);
-  else if constexpr (CODE == kBandNear8) h0_near_vec<8, kTB>(z2, re, im, logtab);
-  else if constexpr (CODE == kBandNear12) h0_near_vec<12, kTB>(z2, re, im, logtab);
-  else h0_far_vec<kTB>(z2, re, im, band->A, band->B, DataFarPQ<kTB>{band});
+  if constexpr (CODE == kBandGeneric) h0_generic_vec<kTB>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear8) h0_near_vec<8, kTB>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear8Imm) h0_near_vec<8, kTB, true>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear12) h0_near_vec<12, kTB>(z2, re, im, T);
+  else h0_far_vec<kTB>(z2, re, im, band->A, band->B, DataFarPQ<kTB>{band}, T);
 }
 
 // One lockstep block of kTB staged sources p[0], p[stride], ...: acc += sum_q H0(|xt - s_q|) v_q.
@@ -261,7 +267,21 @@ __device__ __forceinline__ void eval_band(const double* z2, double* re, double* 
 // and a zero weight so the evaluator stays branch-free.
 template <int CODE, bool GUARD, bool MASK>
 __device__ __forceinline__ void consume_block(const double4* p, int stride, int valid, double2 xt, double& ar, double& ai,
-                                              const Pair* logtab, const FarBand* band) {
+                                              const PolyTable& T, const FarBand* band) {
+  if constexpr (CODE == kBandGeneric) {  // rare (straddling segments): one lane at a time
+#pragma unroll 1
+    for (int q = 0; q < (MASK ? valid : kTB); ++q) {
+      const double4 sv = p[q * stride];
+      const double dx = xt.x - sv.x, dy = xt.y - sv.y;
+      const double d2 = fma(dx, dx, dy * dy);
+      if (GUARD && !(d2 > 0.0)) continue;
+      double hr, hi;
+      h0_generic_vec<1>(&d2, &hr, &hi, T);
+      ar = fma(hr, sv.z, fma(-hi, sv.w, ar));
+      ai = fma(hr, sv.w, fma(hi, sv.z, ai));
+    }
+    return;
+  }
   double z2[kTB], hr[kTB], hi[kTB];
   bool use[kTB];
 #pragma unroll
@@ -273,7 +293,7 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
     use[q] = ok && (!GUARD || d2 > 0.0);
     z2[q] = (MASK || GUARD) ? (use[q] ? d2 : kZ2Safe) : d2;
   }
-  eval_band<CODE>(z2, hr, hi, logtab, band);
+  eval_band<CODE>(z2, hr, hi, T, band);
   // the weights are re-read from shared memory after the evaluation (not held in registers
   // across it: the evaluator needs every register it can get)
 #pragma unroll
@@ -293,33 +313,37 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
 // (block k to slice k mod nsl); only the last block of the range can be partial (masked).
 template <int CODE, bool GUARD>
 __device__ __forceinline__ void consume(const double4* sb, int a, int b, double2 xt, int slice, int nsl, double& ar,
-                                        double& ai, const Pair* logtab, const FarBand* band) {
+                                        double& ai, const PolyTable& T, const FarBand* band) {
   const int n = b - a;
   const int full = n / kTB;
   for (int k = slice; k < full; k += nsl)
-    consume_block<CODE, GUARD, false>(sb + a + k * kTB, 1, kTB, xt, ar, ai, logtab, band);
+    consume_block<CODE, GUARD, false>(sb + a + k * kTB, 1, kTB, xt, ar, ai, T, band);
   if ((n % kTB) && slice == full % nsl)
-    consume_block<CODE, GUARD, true>(sb + a + full * kTB, 1, n % kTB, xt, ar, ai, logtab, band);
+    consume_block<CODE, GUARD, true>(sb + a + full * kTB, 1, n % kTB, xt, ar, ai, T, band);
 }
 
-template <bool GUARD>
+// Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only near-8 and generic
+// occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
+template <bool GUARD, bool NEAR_ONLY>
 __device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
-                                             double& ar, double& ai, const Pair* logtab, const FarBand* bands) {
-  switch (code) {
-    case kBandNear8:
-      consume<kBandNear8, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
-      break;
-    case kBandNear12:
-      if constexpr (!GUARD) consume<kBandNear12, false>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
-      else consume<kBandGeneric, true>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
-      break;
-    case kBandGeneric:
-      consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
-      break;
-    default:
-      if constexpr (!GUARD)
-        consume<kBandFarData, false>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands + (code - kBandFarData));
-      else consume<kBandGeneric, true>(sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+                                             double& ar, double& ai, const PolyTable& T, const FarBand* bands) {
+  if constexpr (NEAR_ONLY) {
+    if (code == kBandNear8) consume<kBandNear8Imm, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    else consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+  } else {
+    switch (code) {
+      case kBandNear8:
+        consume<kBandNear8, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        break;
+      case kBandNear12:
+        consume<kBandNear12, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        break;
+      case kBandGeneric:
+        consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        break;
+      default:
+        consume<kBandFarData, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands + (code - kBandFarData));
+    }
   }
 }
 
@@ -328,7 +352,7 @@ __device__ __forceinline__ void consume_code(int code, const double4* sb, int a,
 // Ends with a barrier.
 template <int STAGE, class Stager, class Items>
 __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, const Items& items, double2 xt, bool active,
-                                                  int slice, int nsl, double& ar, double& ai, const Pair* logtab,
+                                                  int slice, int nsl, double& ar, double& ai, const PolyTable& T,
                                                   const FarBand* bands) {
   int c0 = 0, which = 0, it0 = items.is;
   int fill = st.template stage<STAGE>(buf, 0);
@@ -342,25 +366,16 @@ __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, cons
       const double4* sb = buf + which * STAGE;
       for (int it = it0; it < items.ie && items.pb(it) < c1; ++it) {
         const int a = max(items.pb(it), c0) - c0, b = min(items.pe(it), c1) - c0;
-        if (items.guard(it)) consume_code<true>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
-        else consume_code<false>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, logtab, bands);
+        if (Items::kGuarded && items.guard(it))
+          consume_code<Items::kGuarded, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        else
+          consume_code<false, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
       }
     }
     c0 = c1;
     fill = next;
     which ^= 1;
   }
-  __syncthreads();
-}
-
-// Copy the log table and every data band into shared memory (all threads; then a barrier).
-__device__ __forceinline__ void load_tables(Pair* logtab, FarBand* bands) {
-  for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) logtab[i] = dafmm_fit::kLogTabDev[i];
-  static_assert(sizeof(FarBand) % sizeof(Pair) == 0, "FarBand is copied as pairs");
-  const Pair* src = reinterpret_cast<const Pair*>(dafmm_fit::kFarBandsDev);
-  Pair* d = reinterpret_cast<Pair*>(bands);
-  constexpr int n = (int)(dafmm_fit::NUM_FAR * sizeof(FarBand) / sizeof(Pair));
-  for (int i = threadIdx.x; i < n; i += blockDim.x) d[i] = src[i];
   __syncthreads();
 }
 
@@ -374,10 +389,11 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
     const double2* __restrict__ mult, double2* __restrict__ loc) {
   __shared__ __align__(16) double4 buf[2 * kM2LStage];
   __shared__ double2 red[kM2LThreads];
-  __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
+  __shared__ PolyTable T;
   __shared__ FarBand bands[dafmm_fit::NUM_FAR];
   __shared__ int next;
-  load_tables(logtab, bands);
+  load_poly_table(T);
+  load_far_bands(bands);
   // persistent CTAs take target nodes from a ticket counter (targets are packed by
   // decreasing cost, so the dynamic order balances the tail)
   while (true) {
@@ -398,7 +414,7 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
       double2 xt = ld2(ti_xy + lo + t0 + t);
       double ar = 0.0, ai = 0.0;
       IndexStager st{stream_idx, stream_ptr[tgt], (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]), so_xy, mult};
-      stream_accumulate<kM2LStage>(buf, st, items, xt, active, slice, nsl, ar, ai, logtab, bands);
+      stream_accumulate<kM2LStage>(buf, st, items, xt, active, slice, nsl, ar, ai, T, bands);
       red[threadIdx.x] = make_double2(ar, ai);
       __syncthreads();
       if (threadIdx.x < rc) {
@@ -424,9 +440,8 @@ __global__ void __launch_bounds__(kNearThreads, 3) p2p_kernel(
     const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi) {
   __shared__ __align__(16) double4 buf[2 * kNearStage];
   __shared__ double2 red[kNearThreads];
-  __shared__ Pair logtab[1 << dafmm_fit::LOG_BITS];
-  for (int i = threadIdx.x; i < (1 << dafmm_fit::LOG_BITS); i += blockDim.x) logtab[i] = dafmm_fit::kLogTabDev[i];
-  __syncthreads();
+  __shared__ PolyTable T;
+  load_poly_table(T);
   const int leaf = blockIdx.x;
   const int tb = leaf_begin[leaf], m = leaf_end[leaf] - tb;
   const int ps = near_ptr[leaf], pe = near_ptr[leaf + 1];
@@ -443,7 +458,7 @@ __global__ void __launch_bounds__(kNearThreads, 3) p2p_kernel(
     double ar = 0.0, ai = 0.0;
     if (pe > ps) {
       RunStager st{near_begin, near_end, ps, 0, pe, pts_t, v_t};
-      stream_accumulate<kNearStage>(buf, st, items, xt, active, slice, nsl, ar, ai, logtab, nullptr);
+      stream_accumulate<kNearStage>(buf, st, items, xt, active, slice, nsl, ar, ai, T, nullptr);
     }
     red[threadIdx.x] = make_double2(ar, ai);
     __syncthreads();

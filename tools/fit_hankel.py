@@ -8,18 +8,20 @@ arithmetic against mpmath before being written.
 
 All evaluators take z2 = (kappa r)^2 (the kernels store kappa-scaled coordinates).
 
-  near-type band Zn (z <= Zn), code:   H0 = J0 + i [ (1/pi) ln(u) J0 + R ],  u = z2/4,
+  near-type band Zn (z <= Zn):   H0 = J0 + i [ (1/pi) ln(u) J0 + R ],  u = z2/4,
         J0 and R (the regular part of Y0) polynomials in t = 2u/U - 1, U = Zn^2/4.
   far-type band, z in [zlo, zhi]:   H0 = sqrt(2/(pi z)) (P + i Q) e^{i (z - pi/4)},
         P, Q polynomials in x = A s + B, s = 1/z mapped from [1/zhi, 1/zlo] onto [-1, 1].
-        One band is emitted as code (the generic far band [8, inf)); the rest are a data
-        table the kernels copy into shared memory per work segment.
-  sincos on |rho| <= pi/4: sin(rho)/rho and cos(rho) polynomials in rho^2 (code).
+        The generic band [8, inf) sits in PolyTable; 29 narrower bands form the FarBand table.
+  sincos on |rho| <= pi/4: sin(rho)/rho and cos(rho) polynomials in rho^2.
   ln u = e ln2 + ln c_i + log1p(m/c_i - 1), u = 2^e m, with a 2^7-entry table (rcp_i, ln c_i)
-        indexed by the top mantissa bits (data) and a degree-9 log1p (code).
+        indexed by the top mantissa bits and a degree-9 log1p.
 
-Polynomials emitted as code are lane-blocked Horner evaluators with literal coefficients: on
-sm_100a each literal is a uniform-register immediate shared by the TB lanes of a block.
+All coefficients are data: pairs of doubles (two polynomials evaluated at the same argument)
+in PolyTable (fixed-degree polynomials and the log table) and in the FarBand table (data
+bands, padded to an odd coefficient count).  The kernels copy them to shared memory; one
+128-bit broadcast load then feeds the 2 x TB FMAs of a lane-blocked Horner step (on sm_100a
+DFMA takes no constant-bank operand and a 64-bit immediate costs two UMOVs).
 """
 import math
 import os
@@ -216,7 +218,7 @@ def main(out_path):
     c1, c2 = cody_waite()
     qe, qo = log1p_coeffs()
     lt = log_table()
-    maxn = max(f[2] for f in fars) + 1
+    maxn = max(f[2] for f in fars) + 2
     L = []
     w = L.append
     w("// GENERATED by tools/fit_hankel.py — do not edit.  Product-side H0^(1) fits (DESIGN.md §6).")
@@ -228,6 +230,34 @@ def main(out_path):
                                                                          max(f[2] for f in fars), TOL_FAR))
     w("#pragma once")
     w('#include "common.h"')
+    w("namespace dafmm_fit {")
+    w("constexpr double INV_PI = %.17e;" % float(1 / mp.pi))
+    w("constexpr double TWO_OVER_PI = %.17e;" % float(2 / mp.pi))
+    w("constexpr double SQRT_2_OVER_PI = %.17e;" % float(mp.sqrt(2 / mp.pi)))
+    w("constexpr double LN2 = %.17e;" % float(mp.log(2)))
+    w("constexpr double PIO2_1 = %.17e;\nconstexpr double PIO2_2 = %.17e;" % (c1, c2))
+    w("constexpr int LOG_BITS = 7;")
+    w("struct alignas(16) Pair {\n  double a, b;\n};")
+    # fixed-degree polynomials: pairs in one table (copied to shared memory by the kernels)
+    def pairlist(ca, cb):
+        n = max(len(ca), len(cb))
+        ca = [float(v) for v in ca] + [0.0] * (n - len(ca))
+        cb = [float(v) for v in cb] + [0.0] * (n - len(cb))
+        return n, "{" + ", ".join("{%.17e, %.17e}" % (x, y) for x, y in zip(ca, cb)) + "}"
+    n8, near8 = pairlist(nears[0][0], nears[0][1])
+    n12, near12 = pairlist(nears[1][0], nears[1][1])
+    ngf, gf = pairlist(gfar[0], gfar[1])
+    nsc, sc = pairlist(cs, cc)
+    nlp, lp = pairlist(qe, qo)
+    w("// near-type bands: (J0, R) polynomials in t = z2 * T_SCALE - 1")
+    for zn, n in zip(NEAR_BANDS, (n8, n12)):
+        U = zn * zn / 4
+        w("constexpr double NEAR%d_Z2_MAX = %.17g;  // z^2 <= Z2_MAX" % (int(zn), zn * zn))
+        w("constexpr double NEAR%d_T_SCALE = %.17g;  // t = z2 * T_SCALE - 1 = 2 (z2/4) / U - 1" % (int(zn), 0.5 / U))
+        w("constexpr int NEAR%d_N = %d;" % (int(zn), n))
+    w("constexpr double GENERIC_FAR_ZLO = %.17g;" % GENERIC_FAR[0])
+    w("constexpr double GENERIC_FAR_A = %.17e, GENERIC_FAR_B = %.17e;" % (gfar[4], gfar[5]))
+    w("constexpr int GENERIC_FAR_N = %d, SC_N = %d, LOG1P_N = %d;" % (ngf, nsc, nlp))
     w("#define DAFMM_H2_INIT(ca, cb)                 \\")
     w("  _Pragma(\"unroll\") for (int i = 0; i < TB; ++i) { \\")
     w("    a[i] = ca;                                \\")
@@ -238,29 +268,26 @@ def main(out_path):
     w("    a[i] = fma(a[i], x[i], ca);               \\")
     w("    b[i] = fma(b[i], x[i], cb);               \\")
     w("  }")
-    w("namespace dafmm_fit {")
-    w("constexpr double INV_PI = %.17e;" % float(1 / mp.pi))
-    w("constexpr double TWO_OVER_PI = %.17e;" % float(2 / mp.pi))
-    w("constexpr double SQRT_2_OVER_PI = %.17e;" % float(mp.sqrt(2 / mp.pi)))
-    w("constexpr double LN2 = %.17e;" % float(mp.log(2)))
-    w("constexpr double PIO2_1 = %.17e;\nconstexpr double PIO2_2 = %.17e;" % (c1, c2))
-    w("constexpr int LOG_BITS = 7;")
-    w("struct alignas(16) Pair {\n  double a, b;\n};")
-    w("// near-type bands: NearJR<Zn>::eval evaluates (J0, R) at t = z2 * T_SCALE - 1")
-    w("template <int ZN>\nstruct NearJR;")
-    for zn, f in zip(NEAR_BANDS, nears):
-        U = zn * zn / 4
-        body = h2_function("eval", f[0], f[1], "(J0, R) in t = 2u/U - 1, U = %g (degree %d)" % (U, f[2]),
-                           template="template <int TB>", prefix="static DAFMM_HD void")
-        w("template <>\nstruct NearJR<%d> {\n  static constexpr double Z2_MAX = %.17g;  // z^2 <= Z2_MAX\n"
-          "  static constexpr double T_SCALE = %.17g;  // t = z2 * T_SCALE - 1 = 2 (z2/4) / U - 1\n%s\n};"
-          % (int(zn), zn * zn, 0.5 / U, body))
-    w(h2_function("generic_far_pq", gfar[0], gfar[1],
-                  "(P, Q) of the generic far band [%g, inf) in x = A/z + B (degree %d)" % (GENERIC_FAR[0], gfar[2])))
-    w("constexpr double GENERIC_FAR_ZLO = %.17g;" % GENERIC_FAR[0])
-    w("constexpr double GENERIC_FAR_A = %.17e, GENERIC_FAR_B = %.17e;" % (gfar[4], gfar[5]))
-    w(h2_function("sincos_poly", cs, cc, "(sin(rho)/rho, cos(rho)) in rho^2 (degree %d)" % sc_deg))
-    w(h2_function("log1p_poly", qe, qo, "(qe, qo) in r^2: log1p(r) = r + r^2 (qe + r qo)"))
+    w(h2_function("near8_imm", nears[0][0], nears[0][1],
+                  "(J0, R) of the near band z <= 8 with the coefficients as immediates (the P2P kernel: "
+                  "fp64-pipe-bound, it prefers issue slots to shared-memory latency)"))
+    w("// Coefficient pairs of every fixed-degree polynomial and the log table.  The kernels copy it")
+    w("// to shared memory once per CTA; one 128-bit broadcast load then feeds the 2 x TB FMAs of a")
+    w("// lane-blocked Horner step (64-bit immediates would cost two UMOVs each on sm_100a).")
+    w("struct PolyTable {")
+    w("  Pair near8[NEAR8_N];            // (J0_k, R_k), z <= 8")
+    w("  Pair near12[NEAR12_N];          // (J0_k, R_k), z <= 12")
+    w("  Pair generic_far[GENERIC_FAR_N];  // (P_k, Q_k), z >= 8")
+    w("  Pair sincos[SC_N];              // (sin(rho)/rho, cos(rho)) in rho^2")
+    w("  Pair log1p[LOG1P_N];            // (qe_k, qo_k): log1p(r) = r + r^2 (qe(r^2) + r qo(r^2))")
+    w("  Pair log_tab[1 << LOG_BITS];    // (rcp_i, ln c_i), i = top LOG_BITS mantissa bits")
+    w("};")
+    lt_init = "{" + ", ".join("{%.17e, %.17e}" % t for t in lt) + "}"
+    init = "{\n%s,\n%s,\n%s,\n%s,\n%s,\n%s}" % (near8, near12, gf, sc, lp, lt_init)
+    w("#if defined(__CUDACC__)")
+    w("static __constant__ PolyTable kPolyDev = %s;" % init)
+    w("#endif")
+    w("static const PolyTable kPolyHost = %s;" % init)
     w("// far-type data bands: x = A / z + B; pq[k] = (P_k, Q_k), k < n")
     w("constexpr int NUM_FAR = %d;" % len(fars))
     w("constexpr int FAR_MAXN = %d;" % maxn)
@@ -268,6 +295,10 @@ def main(out_path):
     rows = []
     for (zlo, zhi), f in zip(menu, fars):
         n = f[2] + 1
+        if n % 2 == 0:  # pad to an odd coefficient count with a zero leading (highest) coefficient:
+            # the kernels' Horner loop then runs in coefficient pairs without a remainder
+            f = (list(f[0]) + [mp.mpf(0)], list(f[1]) + [mp.mpf(0)]) + tuple(f[2:])
+            n += 1
         pqs = ", ".join("{%.17e, %.17e}" % (float(a), float(b)) for a, b in zip(f[0], f[1]))
         pqs += "".join(", {0.0, 0.0}" for _ in range(maxn - n))
         rows.append("{%.17g, %s, %.17e, %.17e, %d, 0, {%s}}" % (zlo, "1e308" if zhi == float("inf") else
@@ -277,12 +308,6 @@ def main(out_path):
     w("static __constant__ FarBand kFarBandsDev[NUM_FAR] = %s;" % init)
     w("#endif")
     w("static const FarBand kFarBandsHost[NUM_FAR] = %s;" % init)
-    w("// log table (rcp_i, ln c_i), i = top LOG_BITS mantissa bits")
-    init = "{" + ", ".join("{%.17e, %.17e}" % t for t in lt) + "}"
-    w("#if defined(__CUDACC__)")
-    w("static __constant__ Pair kLogTabDev[1 << LOG_BITS] = %s;" % init)
-    w("#endif")
-    w("static const Pair kLogTabHost[1 << LOG_BITS] = %s;" % init)
     w("}  // namespace dafmm_fit")
     with open(out_path, "w") as f:
         f.write("\n".join(L) + "\n")
