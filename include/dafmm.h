@@ -59,7 +59,7 @@ typedef struct {
   int self_term;       /* 1: disk self term D1 (default); 0: D_i = 0 (point kernel) */
   int kernel_mode;     /* 0: Lippmann-Schwinger y = x + kappa^2 q o (K x) (default);
                           1: potential y = K x (the N-body sum of Experiment 1) */
-  int max_level;       /* deepest tree level allowed (default 16) */
+  int max_level;       /* deepest tree level allowed (default 20, the maximum) */
   int num_threads;     /* host threads for setup; 0 = OpenMP default */
   int host_only;       /* 1: build the host plan only (no device upload; for inspection and
                           dafmm_export_plan on machines without a GPU); matvec / GMRES then

@@ -117,6 +117,11 @@ def _union(arrays):
     return np.unique(np.concatenate(arrays))
 
 
+def is_leaf_node(tree, level, node):
+    """Leaves are LFR boxes (refinement rule 3), so a leaf node is a box key."""
+    return not tree.is_hfr(level) and tree.is_leaf(level, node)
+
+
 def node_points(tree, level, node):
     box = node[0] if tree.is_hfr(level) else node
     return tree.boxes[level][box]
@@ -135,13 +140,19 @@ class NCA:
     checking them."""
 
     def __init__(self, prob, tree, lists, eps, pivots=None):
+        # reading R17: nested-basis errors compound over the LFR levels of an adaptive tree, so
+        # the ACA runs at eps / 2 when leaves lie on several levels
+        if len({l for l, _ in tree.all_leaves()}) > 1:
+            eps = 0.5 * eps
         self.prob, self.tree, self.lists, self.eps = prob, tree, lists, eps
         L = tree.L
         self.search = [dict() for _ in range(L + 1)]
         if pivots is None:
             self.pivots = [dict() for _ in range(L + 1)]
             for level in range(L, 0, -1):
-                for node in sorted(lists.active[level]):
+                # leaf nodes first: a non-leaf node's search sets use the pivots of the leaves
+                # in its interaction list (adaptive trees)
+                for node in sorted(lists.active[level], key=lambda nd: (not is_leaf_node(tree, level, nd), nd)):
                     ts = self.search_sets(level, node)
                     self.search[level][node] = ts
                     ti, si = aca_pivots(prob, ts["ti"], ts["si"], eps)
@@ -158,17 +169,36 @@ class NCA:
         """Step 1 of P:597-631: t~^{B,i}, s~^{B,i}, t~^{B,o}, s~^{B,o}."""
         tree, lists = self.tree, self.lists
         far = lists.far_list(level, node)
-        if level == tree.L:  # leaf (P:599-606)
+        if is_leaf_node(tree, level, node):  # leaf (P:599-606)
             own = node_points(tree, level, node)
-            far_pts = _union([tree.boxes[level][a] for a, _ in far])
+            far_pts = _union([tree.boxes[level][a] for a, _ in far] + self.parent_far_points(level, node))
             return dict(ti=own, si=far_pts, to=far_pts, so=own)
         kids = children_nodes(tree, level, node)  # P:607-631
         ti = _union([self.pivots[level + 1][c]["ti"] for c in kids])
         so = _union([self.pivots[level + 1][c]["so"] for c in kids])
         far_kids = [c for e in far for c in far_child_nodes(tree, level, e)]
-        si = _union([self.pivots[level + 1][c]["so"] for c in far_kids])
-        to = _union([self.pivots[level + 1][c]["ti"] for c in far_kids])
+        # a leaf in the interaction list (adaptive trees) has no children: its own pivots at
+        # this level stand for its points (it enters M2L through s^{A,o} / t^{A,i})
+        far_leaves = [e[0] for e in far if e[1] is None and tree.is_leaf(level, e[0])]
+        si = _union([self.pivots[level + 1][c]["so"] for c in far_kids] +
+                    [self.pivots[level][a]["so"] for a in far_leaves])
+        to = _union([self.pivots[level + 1][c]["ti"] for c in far_kids] +
+                    [self.pivots[level][a]["ti"] for a in far_leaves])
         return dict(ti=ti, si=si, to=to, so=so)
+
+    def parent_far_points(self, level, node):
+        """Reading R16 (adaptive trees): a leaf whose LFR parent P has a leaf among its
+        neighbours gets no interaction-list boxes in that direction (IL(B) is made of the children
+        of P's neighbours), although sources there reach it through P's local expansion.  Its
+        far-field search sets then also take the points of IL(P), so the leaf's bases see every
+        direction its far field arrives from.  Never triggers on a uniform tree."""
+        tree, lists = self.tree, self.lists
+        if level < 2 or tree.is_hfr(level - 1):
+            return []
+        par = (node[0] >> 1, node[1] >> 1)
+        if not any(tree.is_leaf(level - 1, a) for a in lists.N[level - 1][par]):
+            return []
+        return [tree.boxes[level - 1][a] for a in lists.IL[level - 1][par]]
 
     def build_operators(self):
         """U, V* of leaves; C, T of parents: by LU solves (R12)."""
@@ -179,10 +209,10 @@ class NCA:
                 p = self.pivots[level][node]
                 Mi = K_block(prob, p["ti"], p["si"])
                 Mo = K_block(prob, p["to"], p["so"])
-                if level == tree.L:
+                if is_leaf_node(tree, level, node):
                     own = node_points(tree, level, node)
-                    self.U[node] = solve_right(K_block(prob, own, p["si"]), Mi)
-                    self.V[node] = solve_left(Mo, K_block(prob, p["to"], own))
+                    self.U[(level, node)] = solve_right(K_block(prob, own, p["si"]), Mi)
+                    self.V[(level, node)] = solve_left(Mo, K_block(prob, p["to"], own))
                 else:
                     for c in children_nodes(tree, level, node):
                         pc = self.pivots[level + 1][c]
@@ -206,11 +236,13 @@ class NCA:
         L = tree.L
         if "far" in parts:
             mult = [dict() for _ in range(L + 1)]
-            # Upward pass: P2M, then M2M / directional M2M
-            for node in lists.active[L]:
-                mult[L][node] = self.V[node] @ x[node_points(tree, L, node)]
-            for level in range(L - 1, 0, -1):
+            # Upward pass, fine to coarse: P2M at the leaves, M2M / directional M2M
+            # at the other nodes; leaves of an adaptive tree sit on several levels
+            for level in range(L, 0, -1):
                 for node in lists.active[level]:
+                    if is_leaf_node(tree, level, node):
+                        mult[level][node] = self.V[(level, node)] @ x[node_points(tree, level, node)]
+                        continue
                     r = len(self.pivots[level][node]["so"])
                     acc = np.zeros(r, dtype=np.complex128)
                     for c in children_nodes(tree, level, node):
@@ -236,13 +268,17 @@ class NCA:
                 for node in lists.active[level]:
                     for c in children_nodes(tree, level, node):
                         loc[level + 1][c] = loc[level + 1][c] + self.C[(level, node, c)] @ loc[level][node]
-            # L2P
-            for node in lists.active[L]:
-                y[node_points(tree, L, node)] += self.U[node] @ loc[L][node]
+            # L2P at every leaf
+            for level in range(1, L + 1):
+                for node in lists.active[level]:
+                    if is_leaf_node(tree, level, node):
+                        y[node_points(tree, level, node)] += self.U[(level, node)] @ loc[level][node]
         if "near" in parts:
-            # Near field over N(B), B itself included (R6); diagonal per D1
-            for b, own in tree.boxes[L].items():
-                nb = _union([tree.boxes[L][a] for a in lists.N[L][b]])
+            # Near field of every leaf (B itself included, R6; adaptive U/W/X lists
+            # folded in, Lists._near_lists); diagonal per D1
+            for (l, b), near in lists.near.items():
+                own = tree.boxes[l][b]
+                nb = _union([tree.boxes[m][a] for m, a in near])
                 y[own] += K_block(prob, own, nb) @ x[nb]
         return y
 

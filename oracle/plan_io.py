@@ -23,7 +23,8 @@ def load_plan(path):
         pre = "l%d_" % l
         boxes = [tuple(int(v) for v in b) for b in ld(pre + "boxes.npy").reshape(-1, 2)]
         hfr, ncones = (int(v) for v in ld(pre + "info.npy"))
-        lv = dict(boxes=boxes, hfr=bool(hfr), ncones=ncones)
+        leaf = ld(pre + "leaf.npy")
+        lv = dict(boxes=boxes, hfr=bool(hfr), ncones=ncones, leaves={b for b, f in zip(boxes, leaf) if f})
 
         def csr(name):
             ptr, idx = ld(pre + name + "_ptr.npy"), ld(pre + name + "_idx.npy")
@@ -45,6 +46,13 @@ def load_plan(path):
             lv["nodes"] = keys
             lv["pivots"] = piv
         out["levels"].append(lv)
+    # near field: leaf (level, key) -> source boxes (level, key) (non-leaf boxes stand for all
+    # their leaves)
+    lvs = out["levels"]
+    leaves = [(int(l), lvs[int(l)]["boxes"][int(b)]) for l, b in ld("leaves.npy").reshape(-1, 2)]
+    ptr, src = ld("near_ptr.npy"), ld("near_src.npy").reshape(-1, 2)
+    out["near"] = {leaves[i]: [(int(l), lvs[int(l)]["boxes"][int(b)]) for l, b in src[ptr[i]:ptr[i + 1]]]
+                   for i in range(len(leaves))}
     return out
 
 
@@ -54,6 +62,7 @@ def compare_lists(plan, tree, lists):
     assert (plan["meta"]["W"], plan["meta"]["x0"], plan["meta"]["y0"]) == (tree.W, tree.x0, tree.y0)
     for l, lv in enumerate(plan["levels"]):
         assert sorted(lv["boxes"]) == sorted(tree.boxes[l].keys()), "boxes differ at level %d" % l
+        assert lv["leaves"] == tree.leaves[l], "leaves differ at level %d" % l
         assert lv["hfr"] == tree.is_hfr(l)
         if lv["hfr"]:
             assert lv["ncones"] == tree.n_cones(l)
@@ -66,6 +75,11 @@ def compare_lists(plan, tree, lists):
                 for b in tree.boxes[l]:
                     assert lv["ILdir"].get(b, {}) == lists.ILdir[l][b], "IL(B,l) differs at %d %s" % (l, b)
             assert set(lv["nodes"]) == lists.active[l], "active nodes differ at level %d" % l
+    # near field: the same source leaves for every leaf (compared as sets of leaves)
+    assert set(plan["near"]) == set(lists.near), "near-field leaves differ"
+    for b, src in plan["near"].items():
+        got = sorted(c for m, a in src for c in tree.leaf_descendants(m, a))
+        assert got == sorted(lists.near[b]), "near field of leaf %s differs" % (b,)
 
 
 def validate_pivots(nca_like, pivots):

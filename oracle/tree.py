@@ -1,7 +1,7 @@
 """ORACLE — TEST INFRASTRUCTURE ONLY.  Quadtree, frequency regimes, cones and the
 neighbour / interaction lists of the DAFMM.
 
-Readings: R2 uniform tree whose leaves are LFR (paper rule 3);
+Readings: R2 adaptive tree whose leaves are LFR (paper rule 3);
 R3 T = 16; R4 w = circumradius b/sqrt(2); R5 nested cone geometry; R6 N(B) contains B.
 
 Boxes are keyed (level, ix, iy) with integer lattice indices; only non-empty boxes exist.
@@ -23,17 +23,23 @@ def morton(ix, iy):
     return code
 
 
+MAXL = 20  # points are binned on the 2^20 lattice once; a box at level l is that index >> (20 - l)
+
+
 class Tree:
-    """Uniform quadtree over the root square of the points' quadrature cells.
+    """Adaptive quadtree over the root square of the points' quadrature cells.
 
     Root (R2): the smallest axis-aligned square containing every cell [x_j +- sqrt(w_j)/2]^2,
-    centred on their bounding box.  Leaf level L = the smallest level at which (a) every
-    leaf holds <= leaf_size points and (b) leaves are in the low-frequency regime
-    ((kappa b)^2 <= T, refinement rule 3 of P:204).  Box index of a point at the leaf level:
-    ix = floor(((x - x0) / W) * 2^L), clamped; coarser levels by right shifts.
-    """
+    centred on their bounding box.  A box is split while it holds more than leaf_size points
+    or is in the high-frequency regime ((kappa b)^2 > T: refinement rule 3 of P:204, so every
+    leaf is LFR), up to max_level.  Lattice index of a point: ix = floor(((x - x0) / W) 2^20),
+    clamped; its box at level l is ix >> (20 - l).  For the uniform configs every leaf lies on
+    one level L and the tree is the uniform tree.
 
-    def __init__(self, points, weights, kappa, leaf_size, T=16.0, max_level=20):
+    boxes[l]: {(ix, iy): sorted point indices} of the boxes that exist at level l (the root
+    and the children of split boxes, non-empty); leaves[l]: the keys of boxes not split."""
+
+    def __init__(self, points, weights, kappa, leaf_size, T=16.0, max_level=MAXL):
         pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
         half = 0.5 * np.sqrt(np.asarray(weights, dtype=np.float64))
         lo_x, hi_x = float(np.min(pts[:, 0] - half)), float(np.max(pts[:, 0] + half))
@@ -43,37 +49,56 @@ class Tree:
         self.x0, self.y0 = cx - 0.5 * self.W, cy - 0.5 * self.W
         self.kappa, self.T, self.n = float(kappa), float(T), pts.shape[0]
         self.points = pts
-
+        self.fx, self.fy = self._lattice(pts, MAXL)
+        self.boxes = [{(0, 0): np.arange(self.n)}]
+        self.leaves = []
         level = 0
-        while self.kappa * self.width(level) * (self.kappa * self.width(level)) > self.T:
-            level += 1
         while True:
-            ix, iy = self._lattice(pts, level)
-            _, counts = np.unique(ix.astype(np.int64) << 32 | iy.astype(np.int64), return_counts=True)
-            if counts.max() <= leaf_size or level >= max_level:
+            nxt, leaves = {}, set()
+            for key, idx in self.boxes[level].items():
+                split = (idx.size > leaf_size or self.is_hfr(level)) and level < max_level
+                if not split:
+                    if idx.size > leaf_size:
+                        raise ValueError("leaf_size not reachable within max_level")
+                    leaves.add(key)
+                    continue
+                sh = MAXL - (level + 1)
+                cxs, cys = self.fx[idx] >> sh, self.fy[idx] >> sh
+                for c in range(4):
+                    k = (2 * key[0] + (c & 1), 2 * key[1] + (c >> 1))
+                    sel = idx[(cxs == k[0]) & (cys == k[1])]
+                    if sel.size:
+                        nxt[k] = sel
+            self.leaves.append(leaves)
+            if not nxt:
                 break
+            self.boxes.append(nxt)
             level += 1
-        if counts.max() > leaf_size:
-            raise ValueError("leaf_size not reachable within max_level")
-        self.L = level
-        self.ix, self.iy = self._lattice(pts, level)
-        # boxes[l]: {(ix, iy): sorted array of point indices}
-        self.boxes = []
-        for l in range(self.L + 1):
-            sh = self.L - l
-            bx, by = self.ix >> sh, self.iy >> sh
-            order = np.lexsort((np.arange(self.n), by, bx))  # group by box, ascending point index
-            bxo, byo = bx[order], by[order]
-            cut = np.flatnonzero((np.diff(bxo) != 0) | (np.diff(byo) != 0)) + 1
-            starts = np.concatenate([[0], cut])
-            ends = np.concatenate([cut, [self.n]])
-            self.boxes.append({(int(bxo[s]), int(byo[s])): order[s:e] for s, e in zip(starts, ends)})
+        self.L = level  # deepest level
 
     def _lattice(self, pts, level):
         m = 1 << level
         ix = np.floor(((pts[:, 0] - self.x0) / self.W) * m).astype(np.int64)
         iy = np.floor(((pts[:, 1] - self.y0) / self.W) * m).astype(np.int64)
         return np.clip(ix, 0, m - 1), np.clip(iy, 0, m - 1)
+
+    def is_leaf(self, level, key):
+        return key in self.leaves[level]
+
+    def all_leaves(self):
+        """(level, key) of every leaf, coarse levels first, Morton order within a level."""
+        return [(l, k) for l in range(self.L + 1) for k in self.keys(l) if k in self.leaves[l]]
+
+    def leaf_descendants(self, level, key):
+        """Leaves inside box (level, key), itself included when it is a leaf."""
+        if key in self.leaves[level]:
+            return [(level, key)]
+        out = []
+        for c in range(4):
+            k = (2 * key[0] + (c & 1), 2 * key[1] + (c >> 1))
+            if level + 1 <= self.L and k in self.boxes[level + 1]:
+                out += self.leaf_descendants(level + 1, k)
+        return out
 
     def width(self, level):
         return math.ldexp(self.W, -level)
@@ -167,7 +192,27 @@ class Lists:
                         assert kp == (k + n // 2) % n
                         d.setdefault(k, []).append((a, kp))
                     self.ILdir[l][b] = {k: sorted(v) for k, v in d.items()}
+        self._near_lists()
         self._activate()
+
+    def _near_lists(self):
+        """Near field of every leaf B at level l (R6), for an adaptive tree: the
+        source leaves C whose ancestors at level min(l, l_C) are neighbours.  These are exactly
+        the pairs no interaction list covers (the U, W and X lists of adaptive FMMs, all folded
+        into the direct near field):
+          - leaves C at a level m <= l that neighbour B's ancestor at level m (B itself included);
+          - every leaf inside a non-leaf neighbour of B at level l."""
+        tree = self.tree
+        self.near = {}
+        for l, b in tree.all_leaves():
+            out = []
+            for m in range(l, -1, -1):
+                bm = (b[0] >> (l - m), b[1] >> (l - m))
+                out += [(m, a) for a in self.N[m][bm] if a in tree.leaves[m]]
+            for a in self.N[l][b]:
+                if a not in tree.leaves[l]:
+                    out += tree.leaf_descendants(l, a)
+            self.near[(l, b)] = sorted(out)
 
     def _activate(self):
         """Active nodes, top-down: a node needs bases if its interaction list is non-empty or

@@ -242,7 +242,7 @@ struct M2LItems {
 // Items of a near-field leaf: its own block [0, own) (contains i == j) and the rest.
 struct NearItems {
   static constexpr bool kGuarded = true;   // item 0 holds the i == j pairs
-  static constexpr bool kNearOnly = true;  // bands: near-8 or generic
+  static constexpr bool kNearOnly = true;  // bands: near-8, near-12 or generic
   int band, own, total, is, ie;
   __device__ __forceinline__ int code(int) const { return band; }
   __device__ __forceinline__ bool guard(int i) const { return i == 0; }
@@ -322,13 +322,14 @@ __device__ __forceinline__ void consume(const double4* sb, int a, int b, double2
     consume_block<CODE, GUARD, true>(sb + a + full * kTB, 1, n % kTB, xt, ar, ai, T, band);
 }
 
-// Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only near-8 and generic
-// occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
+// Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only near-8, near-12 and
+// generic occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
 template <bool GUARD, bool NEAR_ONLY>
 __device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
                                              double& ar, double& ai, const PolyTable& T, const FarBand* bands) {
   if constexpr (NEAR_ONLY) {
     if (code == kBandNear8) consume<kBandNear8Imm, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    else if (code == kBandNear12) consume<kBandNear12, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
     else consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
   } else {
     switch (code) {

@@ -21,14 +21,15 @@ struct Options {
   double T = 16.0;         // regime threshold (reading R3)
   int self_term = 1;       // 0 zero (point kernel, E1), 1 disk (reading D1)
   int kernel_mode = 0;     // 0 Lippmann-Schwinger y = x + k^2 q (K x); 1 potential y = K x
-  int max_level = 16;
+  int max_level = 20;
   int num_threads = 0;     // host setup threads (0: OpenMP default)
   int host_only = 0;       // skip the device upload
 };
 
 struct Box {
   int64_t ix, iy;
-  int32_t begin, end;  // tree-order point range
+  int32_t begin, end;  // tree-order point range (every box of the adaptive tree is contiguous)
+  bool leaf;
 };
 
 struct Level {
@@ -56,12 +57,15 @@ struct Plan {
   int64_t n = 0;
   double kappa = 0, nca_tol = 0;
   double W = 0, x0 = 0, y0 = 0;
-  int L = 0;
+  int L = 0;                         // deepest level
+  bool multi_level_leaves = false;   // leaves on more than one level (adaptive tree)
   // input copies (original order)
   std::vector<double> pts, w, q;
   std::vector<zd> D;                 // self terms D_i (original order)
   std::vector<int32_t> perm;         // tree index -> original index
   std::vector<Level> levels;
+  std::vector<std::pair<int, int>> leaves;                  // (level, box), coarse levels first
+  std::vector<std::vector<std::pair<int, int>>> near;       // per leaf: source boxes (level, box)
   std::vector<std::vector<NodePivots>> piv;  // [level][node]
   // statistics
   double t_tree = 0, t_lists = 0, t_nca = 0, t_ops = 0, t_pack = 0, t_upload = 0;

@@ -276,64 +276,50 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
   P.x0 = cxr - 0.5 * P.W;
   P.y0 = cyr - 0.5 * P.W;
   auto width = [&](int l) { return std::ldexp(P.W, -l); };
-  // ---- leaf level: leaves LFR (rule 3) and <= leaf_size points ----
-  int L = 0;
-  while (kappa * width(L) * (kappa * width(L)) > opt.T) ++L;
-  std::vector<int64_t> ix(n), iy(n);
-  auto lattice = [&](int l) {
-    double m = std::ldexp(1.0, l);
-    int64_t mx = ((int64_t)1 << l) - 1;
+  // ---- adaptive tree (reading R2): a box is split while it holds more than
+  // leaf_size points or is in the high-frequency regime (refinement rule 3), up to
+  // max_level.  Points are binned once on the 2^20 lattice; a box at level l is that index
+  // >> (20 - l), and tree order (Morton order of the lattice cell, then input index) makes
+  // every box a contiguous range. ----
+  constexpr int kMaxL = 20;
+  if (opt.max_level > kMaxL) { err = "max_level must be <= 20"; return DAFMM_EINVAL; }
+  std::vector<int64_t> fx(n), fy(n);
+  {
+    const double m = std::ldexp(1.0, kMaxL);
+    const int64_t mx = ((int64_t)1 << kMaxL) - 1;
     for (int64_t i = 0; i < n; ++i) {
       int64_t a = (int64_t)std::floor(((P.pts[2 * i] - P.x0) / P.W) * m);
       int64_t b = (int64_t)std::floor(((P.pts[2 * i + 1] - P.y0) / P.W) * m);
-      ix[i] = std::min<int64_t>(std::max<int64_t>(a, 0), mx);
-      iy[i] = std::min<int64_t>(std::max<int64_t>(b, 0), mx);
+      fx[i] = std::min<int64_t>(std::max<int64_t>(a, 0), mx);
+      fy[i] = std::min<int64_t>(std::max<int64_t>(b, 0), mx);
     }
-  };
-  std::vector<uint64_t> keys(n);
-  while (true) {
-    if (L > opt.max_level) {
-      err = "leaf_size not reachable within max_level (adaptive trees are not supported yet)";
-      return DAFMM_EINVAL;
-    }
-    lattice(L);
-    for (int64_t i = 0; i < n; ++i) keys[i] = pack_key(ix[i], iy[i]);
-    std::vector<uint64_t> s = keys;
-    std::sort(s.begin(), s.end());
-    int64_t run = 1, mx = 1;
-    for (int64_t i = 1; i < n; ++i) {
-      run = (s[i] == s[i - 1]) ? run + 1 : 1;
-      mx = std::max(mx, run);
-    }
-    if (mx <= leaf_size) break;
-    ++L;
   }
-  P.L = L;
-  // ---- tree order: Morton code of the leaf, then original index ----
   std::vector<uint64_t> mcode(n);
-  for (int64_t i = 0; i < n; ++i) mcode[i] = morton(ix[i], iy[i]);
+  for (int64_t i = 0; i < n; ++i) mcode[i] = morton(fx[i], fy[i]);
   P.perm.resize(n);
   std::iota(P.perm.begin(), P.perm.end(), 0);
   std::sort(P.perm.begin(), P.perm.end(), [&](int32_t a, int32_t b) {
     return mcode[a] != mcode[b] ? mcode[a] < mcode[b] : a < b;
   });
-  // duplicate points (G is singular off the diagonal): compare within each leaf
+  // duplicate points (G is singular off the diagonal): they share a lattice cell
   {
-    int64_t s = 0;
-    while (s < n) {
-      int64_t e = s + 1;
-      while (e < n && mcode[P.perm[e]] == mcode[P.perm[s]]) ++e;
-      std::vector<std::pair<double, double>> xy;
-      for (int64_t t = s; t < e; ++t) xy.emplace_back(P.pts[2 * (size_t)P.perm[t]], P.pts[2 * (size_t)P.perm[t] + 1]);
-      std::sort(xy.begin(), xy.end());
-      for (size_t t = 1; t < xy.size(); ++t)
-        if (xy[t] == xy[t - 1]) { err = "duplicate points"; return DAFMM_EINVAL; }
-      s = e;
+    int64_t s0 = 0;
+    while (s0 < n) {
+      int64_t e = s0 + 1;
+      while (e < n && mcode[P.perm[e]] == mcode[P.perm[s0]]) ++e;
+      if (e - s0 > 1) {
+        std::vector<std::pair<double, double>> xy;
+        for (int64_t t = s0; t < e; ++t)
+          xy.emplace_back(P.pts[2 * (size_t)P.perm[t]], P.pts[2 * (size_t)P.perm[t] + 1]);
+        std::sort(xy.begin(), xy.end());
+        for (size_t t = 1; t < xy.size(); ++t)
+          if (xy[t] == xy[t - 1]) { err = "duplicate points"; return DAFMM_EINVAL; }
+      }
+      s0 = e;
     }
   }
-  P.levels.assign(L + 1, Level());
-  for (int l = 0; l <= L; ++l) {
-    Level& lv = P.levels[l];
+  auto make_level = [&](int l) {
+    Level lv;
     lv.level = l;
     lv.b = width(l);
     lv.kb = kappa * lv.b;
@@ -344,18 +330,50 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
       while (nc < x) nc *= 2;
       lv.ncones = nc;
     }
-    int sh = L - l;
-    int64_t t = 0;
-    while (t < n) {
-      int32_t o = P.perm[t];
-      int64_t bx = ix[o] >> sh, by = iy[o] >> sh;
-      int64_t e = t + 1;
-      while (e < n && (ix[P.perm[e]] >> sh) == bx && (iy[P.perm[e]] >> sh) == by) ++e;
-      lv.index[pack_key(bx, by)] = (int)lv.boxes.size();
-      lv.boxes.push_back({bx, by, (int32_t)t, (int32_t)e});
-      t = e;
+    return lv;
+  };
+  P.levels.clear();
+  P.levels.push_back(make_level(0));
+  P.levels[0].index[pack_key(0, 0)] = 0;
+  P.levels[0].boxes.push_back({0, 0, 0, (int32_t)n, false});
+  for (int l = 0;; ++l) {
+    Level& lv = P.levels[l];
+    Level next = make_level(l + 1);
+    const int sh = kMaxL - (l + 1);
+    for (Box& B : lv.boxes) {
+      const int cnt = B.end - B.begin;
+      const bool split = (cnt > leaf_size || lv.hfr) && l < opt.max_level;
+      if (!split) {
+        if (cnt > leaf_size) {
+          err = "leaf_size not reachable within max_level";
+          return DAFMM_EINVAL;
+        }
+        B.leaf = true;
+        continue;
+      }
+      int32_t t = B.begin;
+      while (t < B.end) {  // children: contiguous runs of the level-(l+1) cell
+        const int32_t o = P.perm[t];
+        const int64_t cx = fx[o] >> sh, cy = fy[o] >> sh;
+        int32_t e = t + 1;
+        while (e < B.end && (fx[P.perm[e]] >> sh) == cx && (fy[P.perm[e]] >> sh) == cy) ++e;
+        next.index[pack_key(cx, cy)] = (int)next.boxes.size();
+        next.boxes.push_back({cx, cy, t, e, false});
+        t = e;
+      }
     }
+    if (next.boxes.empty()) break;
+    P.levels.push_back(std::move(next));
   }
+  const int L = (int)P.levels.size() - 1;
+  P.L = L;
+  int leaf_levels = 0;
+  for (const Level& lv : P.levels) {
+    bool any = false;
+    for (const Box& B : lv.boxes) any = any || B.leaf;
+    leaf_levels += any ? 1 : 0;
+  }
+  P.multi_level_leaves = leaf_levels > 1;
   P.D.assign(n, zd(0.0, 0.0));
   if (opt.self_term == 1)
     for (int64_t i = 0; i < n; ++i) P.D[i] = self_term_disk(kappa, P.w[i]);
@@ -421,6 +439,31 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     }
   }
   if (!cone_ok) { err = "box centre on a cone boundary"; return DAFMM_ESETUP; }
+  // ---- near field of every leaf (coarse levels first): the source leaves C whose ancestor
+  // at level min(l, l_C) neighbours B's (R6; the adaptive U, W and X lists folded
+  // into the direct near field): leaves at a level m <= l neighbouring B's ancestor at level m
+  // (B itself first: the only entry with i == j pairs), then the whole range of every non-leaf
+  // neighbour of B at level l (all its leaves) ----
+  P.leaves.clear();
+  P.near.clear();
+  for (int l = 0; l <= L; ++l) {
+    const Level& lv = P.levels[l];
+    for (size_t b = 0; b < lv.boxes.size(); ++b) {
+      const Box& B = lv.boxes[b];
+      if (!B.leaf) continue;
+      std::vector<std::pair<int, int>> src = {{l, (int)b}};
+      for (int m = l; m >= 0; --m) {
+        const Level& mv = P.levels[m];
+        const int bm = mv.index.at(pack_key(B.ix >> (l - m), B.iy >> (l - m)));
+        for (int a : mv.N[bm])
+          if (mv.boxes[a].leaf && !(m == l && a == (int)b)) src.push_back({m, a});
+      }
+      for (int a : lv.N[b])
+        if (!lv.boxes[a].leaf) src.push_back({l, a});
+      P.leaves.push_back({l, (int)b});
+      P.near.push_back(std::move(src));
+    }
+  }
   // ---- active nodes, top-down ----
   for (int l = 0; l <= L; ++l) {
     Level& lv = P.levels[l];
@@ -463,8 +506,6 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
   for (int l = L; l >= 1; --l) {
     Level& lv = P.levels[l];
     P.piv[l].assign(lv.nodes.size(), NodePivots());
-    const bool leaf = (l == L);
-    const Level* cv = leaf ? nullptr : &P.levels[l + 1];
     const Level& pv = P.levels[l - 1];
     // child node ids of (box, cone) at level l+1 (C(B) / C(B, k))
     auto children = [&](const Level& at, int lvl, int box, int cone, std::vector<int>& out) {
@@ -478,75 +519,97 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
         if (nd >= 0) out.push_back(nd);
       }
     };
+    // reading R17: nested-basis errors compound over the LFR levels of an adaptive tree, so
+    // the ACA runs at nca_tol / 2 when leaves lie on several levels
+    const double eps = P.multi_level_leaves ? 0.5 * nca_tol : nca_tol;
+    auto is_leaf_node = [&](int nd) { return !lv.hfr && lv.boxes[lv.nodes[nd].first].leaf; };
+    // leaf nodes first: a non-leaf node's search sets use the pivots of the leaves in its
+    // interaction list (adaptive trees); two parallel sweeps
     int64_t level_entries = 0;
-    int fail = 0;
+    for (int sweep = 0; sweep < 2; ++sweep) {
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : level_entries)
-    for (int nd = 0; nd < (int)lv.nodes.size(); ++nd) {
-      int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
-      // far list: IL(B) / IL(B,k); R7 substitute for an active HFR node with empty IL(B,k)
-      std::vector<std::pair<int, int>> far;
-      if (!lv.hfr) {
-        for (int a : lv.IL[b]) far.push_back({a, -1});
-      } else {
-        for (auto& e : lv.ILdir[b])
-          if (e[0] == k) far.push_back({e[1], e[2]});
-        if (far.empty()) {
-          const Box& B = lv.boxes[b];
-          int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
-          for (auto& e : pv.ILdir[pb]) {
-            if (e[0] != 2 * k && e[0] != 2 * k + 1) continue;
-            const Box& A = pv.boxes[e[1]];
-            for (int c = 0; c < 4; ++c) {
-              auto it = lv.index.find(pack_key(2 * A.ix + (c & 1), 2 * A.iy + (c >> 1)));
-              if (it != lv.index.end()) far.push_back({it->second, e[2] / 2});
+      for (int nd = 0; nd < (int)lv.nodes.size(); ++nd) {
+        const bool leafnode = is_leaf_node(nd);
+        if (leafnode != (sweep == 0)) continue;
+        int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
+        // far list: IL(B) / IL(B,k); R7 substitute for an active HFR node with empty IL(B,k)
+        std::vector<std::pair<int, int>> far;
+        if (!lv.hfr) {
+          for (int a : lv.IL[b]) far.push_back({a, -1});
+        } else {
+          for (auto& e : lv.ILdir[b])
+            if (e[0] == k) far.push_back({e[1], e[2]});
+          if (far.empty()) {
+            const Box& B = lv.boxes[b];
+            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+            for (auto& e : pv.ILdir[pb]) {
+              if (e[0] != 2 * k && e[0] != 2 * k + 1) continue;
+              const Box& A = pv.boxes[e[1]];
+              for (int c = 0; c < 4; ++c) {
+                auto it = lv.index.find(pack_key(2 * A.ix + (c & 1), 2 * A.iy + (c >> 1)));
+                if (it != lv.index.end()) far.push_back({it->second, e[2] / 2});
+              }
             }
+            std::sort(far.begin(), far.end());
+            far.erase(std::unique(far.begin(), far.end()), far.end());
           }
-          std::sort(far.begin(), far.end());
-          far.erase(std::unique(far.begin(), far.end()), far.end());
         }
-      }
-      std::vector<int32_t> ti, si, to, so;
-      if (leaf) {
-        const Box& B = lv.boxes[b];
-        for (int32_t t = B.begin; t < B.end; ++t) ti.push_back(P.perm[t]);
-        so = ti;
-        for (auto& f : far) {
-          const Box& A = lv.boxes[f.first];
-          for (int32_t t = A.begin; t < A.end; ++t) si.push_back(P.perm[t]);
-        }
-        sorted_union(ti);
-        sorted_union(so);
-        sorted_union(si);
-        to = si;
-      } else {
-        std::vector<int> kids;
-        children(lv, l, b, k, kids);
-        for (int c : kids) {
-          const NodePivots& pc = P.piv[l + 1][c];
-          ti.insert(ti.end(), pc.ti.begin(), pc.ti.end());
-          so.insert(so.end(), pc.so.begin(), pc.so.end());
-        }
-        for (auto& f : far) {
-          children(lv, l, f.first, f.second, kids);
+        std::vector<int32_t> ti, si, to, so;
+        if (leafnode) {
+          const Box& B = lv.boxes[b];
+          for (int32_t t = B.begin; t < B.end; ++t) ti.push_back(P.perm[t]);
+          so = ti;
+          auto add_box = [&](const Box& A) {
+            for (int32_t t = A.begin; t < A.end; ++t) si.push_back(P.perm[t]);
+          };
+          for (auto& f : far) add_box(lv.boxes[f.first]);
+          // reading R16: a leaf whose LFR parent has a leaf neighbour also searches IL(parent)
+          if (l >= 2 && !pv.hfr) {
+            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+            bool leaf_nb = false;
+            for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
+            if (leaf_nb)
+              for (int a : pv.IL[pb]) add_box(pv.boxes[a]);
+          }
+          sorted_union(ti);
+          sorted_union(so);
+          sorted_union(si);
+          to = si;
+        } else {
+          std::vector<int> kids;
+          children(lv, l, b, k, kids);
           for (int c : kids) {
             const NodePivots& pc = P.piv[l + 1][c];
-            si.insert(si.end(), pc.so.begin(), pc.so.end());
-            to.insert(to.end(), pc.ti.begin(), pc.ti.end());
+            ti.insert(ti.end(), pc.ti.begin(), pc.ti.end());
+            so.insert(so.end(), pc.so.begin(), pc.so.end());
           }
+          for (auto& f : far) {
+            if (!lv.hfr && lv.boxes[f.first].leaf) {
+              // a leaf in the interaction list has no children: its own pivots at this level
+              const NodePivots& pa = P.piv[l][lv.node_id(f.first, 0)];
+              si.insert(si.end(), pa.so.begin(), pa.so.end());
+              to.insert(to.end(), pa.ti.begin(), pa.ti.end());
+              continue;
+            }
+            children(lv, l, f.first, f.second, kids);
+            for (int c : kids) {
+              const NodePivots& pc = P.piv[l + 1][c];
+              si.insert(si.end(), pc.so.begin(), pc.so.end());
+              to.insert(to.end(), pc.ti.begin(), pc.ti.end());
+            }
+          }
+          sorted_union(ti);
+          sorted_union(so);
+          sorted_union(si);
+          sorted_union(to);
         }
-        sorted_union(ti);
-        sorted_union(so);
-        sorted_union(si);
-        sorted_union(to);
+        NodePivots& np = P.piv[l][nd];
+        int64_t ent = 0;
+        aca(cx, ti, si, eps, np.ti, np.si, ent);
+        aca(cx, to, so, eps, np.to, np.so, ent);
+        level_entries += ent;
       }
-      (void)cv;
-      NodePivots& np = P.piv[l][nd];
-      int64_t ent = 0;
-      aca(cx, ti, si, nca_tol, np.ti, np.si, ent);
-      aca(cx, to, so, nca_tol, np.to, np.so, ent);
-      level_entries += ent;
     }
-    (void)fail;
     total_entries += level_entries;
   }
   P.aca_entries = total_entries;
@@ -648,7 +711,6 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       cs += t.cols;
     }
   };
-  const Level& leaf = P.levels[L];
   auto child_nodes = [&](int l, int nd, std::vector<int>& out) {
     out.clear();
     const Level& lv = P.levels[l];
@@ -662,13 +724,16 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       if (cn >= 0) out.push_back(cn);
     }
   };
-  // P2M
-  for (size_t nd = 0; nd < leaf.nodes.size(); ++nd) {
-    const Box& B = leaf.boxes[leaf.nodes[nd].first];
-    int ro = (int)P.piv[L][nd].so.size();
-    int m = B.end - B.begin;
-    if (ro == 0) continue;
-    add_item(pk.p2m, 0, L, moff[L][nd], ro, {Term{(int)nd, -1, (int64_t)B.begin, m}});
+  // P2M at every leaf node (the leaves of an adaptive tree sit on several levels)
+  for (int l = 1; l <= L; ++l) {
+    const Level& lv = P.levels[l];
+    if (lv.hfr) continue;
+    for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
+      const Box& B = lv.boxes[lv.nodes[nd].first];
+      int ro = (int)P.piv[l][nd].so.size();
+      if (!B.leaf || ro == 0) continue;
+      add_item(pk.p2m, 0, l, moff[l][nd], ro, {Term{(int)nd, -1, (int64_t)B.begin, B.end - B.begin}});
+    }
   }
   pk.p2m.term_ptr.push_back((int32_t)pk.p2m.src_off.size());
   // M2M, fine to coarse
@@ -679,7 +744,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     const Level& lv = P.levels[l];
     for (size_t nd = 0; nd < lv.nodes.size(); ++nd) {
       int ro = (int)P.piv[l][nd].so.size();
-      if (ro == 0) continue;
+      if (ro == 0 || (!lv.hfr && lv.boxes[lv.nodes[nd].first].leaf)) continue;
       child_nodes(l, (int)nd, kids);
       std::vector<Term> terms;
       for (int c : kids) {
@@ -805,7 +870,12 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
     pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
     pk.m2l_stream_ptr.push_back((int64_t)pk.m2l_stream_idx.size());
   }
-  // leaves: near field (own leaf first: the only segment with i == j pairs), L2P
+  // leaves (every level, coarse first): near field and L2P.  The near field of a leaf B at
+  // level l is every source leaf C whose ancestor at level min(l, l_C) neighbours B's (P:750-755,
+  // R6; the adaptive U, W and X lists folded into the direct near field):
+  //   - leaves at a level m <= l neighbouring B's ancestor at level m (B itself first: the only
+  //     entry with i == j pairs);
+  //   - the whole range of every non-leaf neighbour of B at level l (all its leaves).
   auto bbox = [&](const Box& B, double* bb) {
     bb[0] = bb[1] = INFINITY;
     bb[2] = bb[3] = -INFINITY;
@@ -817,45 +887,48 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       bb[3] = std::max(bb[3], P.pts[2 * (size_t)o + 1]);
     }
   };
-  std::vector<double> lbb(4 * leaf.boxes.size());
-  for (size_t b = 0; b < leaf.boxes.size(); ++b) bbox(leaf.boxes[b], &lbb[4 * b]);
   pk.near_ptr.push_back(0);
   pk.max_leaf = 0;
-  for (size_t b = 0; b < leaf.boxes.size(); ++b) {
-    const Box& B = leaf.boxes[b];
-    pk.leaf_begin.push_back(B.begin);
-    pk.leaf_end.push_back(B.end);
-    pk.max_leaf = std::max(pk.max_leaf, B.end - B.begin);
-    std::vector<int> nb = leaf.N[b];
-    std::stable_partition(nb.begin(), nb.end(), [&](int a) { return a == (int)b; });
-    double zmax = 0.0;
-    int64_t pairs = 0;
-    for (int a : nb) {
-      pk.near_begin.push_back(leaf.boxes[a].begin);
-      pk.near_end.push_back(leaf.boxes[a].end);
-      pairs += (int64_t)(B.end - B.begin) * (leaf.boxes[a].end - leaf.boxes[a].begin);
-      const double* p = &lbb[4 * b];
-      const double* q = &lbb[4 * (size_t)a];
-      double dx = std::max(p[2] - q[0], q[2] - p[0]);
-      double dy = std::max(p[3] - q[1], q[3] - p[1]);
-      zmax = std::max(zmax, P.kappa * std::sqrt(dx * dx + dy * dy));
-    }
-    pairs -= (B.end - B.begin);
-    pk.p2p_pairs += pairs;
-    int band = zmax <= 8.0 ? kBandNear8 : kBandGeneric;
-    pk.leaf_band.push_back(band);
-    pk.p2p_band_entries[band] += pairs;
-    pk.near_ptr.push_back((int32_t)pk.near_begin.size());
-    int nd = leaf.node_of[b];
-    int ri = nd >= 0 ? (int)P.piv[L][nd].ti.size() : 0;
-    if (ri > 0) {
-      pk.leaf_loc_off.push_back(loff[L][nd]);
-      pk.leaf_rank.push_back(ri);
-      pk.leaf_U_off.push_back(add_job(3, L, nd, (int)b, (int64_t)(B.end - B.begin) * ri));
-    } else {
-      pk.leaf_loc_off.push_back(-1);
-      pk.leaf_rank.push_back(0);
-      pk.leaf_U_off.push_back(0);
+  for (int l = 0; l <= L; ++l) {
+    const Level& lv = P.levels[l];
+    for (size_t b = 0; b < lv.boxes.size(); ++b) {
+      const Box& B = lv.boxes[b];
+      if (!B.leaf) continue;
+      pk.leaf_begin.push_back(B.begin);
+      pk.leaf_end.push_back(B.end);
+      pk.max_leaf = std::max(pk.max_leaf, B.end - B.begin);
+      const size_t li = pk.leaf_begin.size() - 1;  // leaves are packed in P.leaves order
+      std::vector<const Box*> src;
+      for (const auto& e : P.near[li]) src.push_back(&P.levels[e.first].boxes[e.second]);
+      double pb[4], qb[4], zmax = 0.0;
+      bbox(B, pb);
+      int64_t pairs = 0;
+      for (const Box* A : src) {
+        pk.near_begin.push_back(A->begin);
+        pk.near_end.push_back(A->end);
+        pairs += (int64_t)(B.end - B.begin) * (A->end - A->begin);
+        bbox(*A, qb);
+        double dx = std::max(pb[2] - qb[0], qb[2] - pb[0]);
+        double dy = std::max(pb[3] - qb[1], qb[3] - pb[1]);
+        zmax = std::max(zmax, P.kappa * std::sqrt(dx * dx + dy * dy));
+      }
+      pairs -= (B.end - B.begin);
+      pk.p2p_pairs += pairs;
+      int band = zmax <= 8.0 ? kBandNear8 : zmax <= 12.0 ? kBandNear12 : kBandGeneric;
+      pk.leaf_band.push_back(band);
+      pk.p2p_band_entries[band] += pairs;
+      pk.near_ptr.push_back((int32_t)pk.near_begin.size());
+      int nd = lv.hfr ? -1 : lv.node_of[b];
+      int ri = nd >= 0 ? (int)P.piv[l][nd].ti.size() : 0;
+      if (ri > 0) {
+        pk.leaf_loc_off.push_back(loff[l][nd]);
+        pk.leaf_rank.push_back(ri);
+        pk.leaf_U_off.push_back(add_job(3, l, nd, (int)b, (int64_t)(B.end - B.begin) * ri));
+      } else {
+        pk.leaf_loc_off.push_back(-1);
+        pk.leaf_rank.push_back(0);
+        pk.leaf_U_off.push_back(0);
+      }
     }
   }
   // ---- operator blocks (column-major), in parallel ----
@@ -876,7 +949,8 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       int r = (int)np.so.size();
       std::vector<int32_t> cols;
       if (J.kind == 0) {
-        const Box& B = leaf.boxes[P.levels[L].nodes[J.node].first];
+        const Level& jl = P.levels[J.level];
+        const Box& B = jl.boxes[jl.nodes[J.node].first];
         for (int32_t t = B.begin; t < B.end; ++t) cols.push_back(P.perm[t]);
       } else {
         cols = P.piv[J.level + 1][J.child].so;
@@ -902,7 +976,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       int r = (int)np.ti.size();
       std::vector<int32_t> rows;
       if (J.kind == 3) {
-        const Box& B = leaf.boxes[J.child];
+        const Box& B = P.levels[J.level].boxes[J.child];
         for (int32_t t = B.begin; t < B.end; ++t) rows.push_back(P.perm[t]);
       } else {
         rows = P.piv[J.level + 1][J.child].ti;
@@ -968,12 +1042,29 @@ int export_plan(const Plan& P, const std::string& dir, std::string& err) {
   ok &= write_npy(dir + "/meta.npy", "<f8", meta, {(int64_t)meta.size()});
   std::vector<int64_t> perm(P.perm.begin(), P.perm.end());
   ok &= write_npy(dir + "/perm.npy", "<i8", perm, {(int64_t)perm.size()});
+  // leaves (level, box) and their near-field source boxes (level, box)
+  {
+    std::vector<int64_t> leaves, ptr = {0}, src;
+    for (size_t i = 0; i < P.leaves.size(); ++i) {
+      leaves.push_back(P.leaves[i].first);
+      leaves.push_back(P.leaves[i].second);
+      for (auto& e : P.near[i]) {
+        src.push_back(e.first);
+        src.push_back(e.second);
+      }
+      ptr.push_back((int64_t)src.size() / 2);
+    }
+    ok &= write_npy(dir + "/leaves.npy", "<i8", leaves, {(int64_t)P.leaves.size(), 2});
+    ok &= write_npy(dir + "/near_ptr.npy", "<i8", ptr, {(int64_t)ptr.size()});
+    ok &= write_npy(dir + "/near_src.npy", "<i8", src, {(int64_t)src.size() / 2, 2});
+  }
   for (int l = 0; l <= P.L; ++l) {
     const Level& lv = P.levels[l];
     std::string pre = dir + "/l" + std::to_string(l) + "_";
-    std::vector<int64_t> boxes;
-    for (auto& b : lv.boxes) { boxes.push_back(b.ix); boxes.push_back(b.iy); }
+    std::vector<int64_t> boxes, leaf;
+    for (auto& b : lv.boxes) { boxes.push_back(b.ix); boxes.push_back(b.iy); leaf.push_back(b.leaf ? 1 : 0); }
     ok &= write_npy(pre + "boxes.npy", "<i8", boxes, {(int64_t)lv.boxes.size(), 2});
+    ok &= write_npy(pre + "leaf.npy", "<i8", leaf, {(int64_t)lv.boxes.size()});
     std::vector<int64_t> info = {lv.hfr ? 1 : 0, lv.ncones};
     ok &= write_npy(pre + "info.npy", "<i8", info, {2});
     auto csr = [&](const std::vector<std::vector<int>>& lists, const std::string& name) {

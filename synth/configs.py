@@ -54,26 +54,71 @@ def plane_wave_rhs(pts, q, kappa, angle_deg=0.0):
     return -kappa * kappa * q * np.exp(1j * phase)
 
 
+def smoothed_disk_q(pts, radius=0.5, sharpness=200.0):
+    """q = (1 + tanh(sharpness (radius - r))) / 2 (config 5; SURVEY A15 reading)."""
+    r = np.sqrt(pts[:, 0] ** 2 + pts[:, 1] ** 2)
+    return 0.5 * (1.0 + np.tanh(sharpness * (radius - r)))
+
+
+def adaptive_leaves(kappa, max_depth, tol=1e-3, T=16.0, qfun=smoothed_disk_q):
+    """Leaves (level, i, j) of the config-5 quadtree on [-1,1]^2: split a box while
+    max over its corners |q(corner) - q(centre)| > tol, up to max_depth, and (refinement rule 3,
+    P:204) while it is in the high-frequency regime (kappa b)^2 > T, so every leaf is LFR."""
+    leaves, stack = [], [(0, 0, 0)]
+    while stack:
+        level, i, j = stack.pop()
+        b = 2.0 / (1 << level)
+        x0, y0 = -1.0 + i * b, -1.0 + j * b
+        c = np.array([[x0, y0], [x0 + b, y0], [x0, y0 + b], [x0 + b, y0 + b]])
+        qc = qfun(c)
+        qm = qfun(np.array([[x0 + 0.5 * b, y0 + 0.5 * b]]))[0]
+        split = level < max_depth and (np.max(np.abs(qc - qm)) > tol or (kappa * b) ** 2 > T)
+        if split:
+            stack += [(level + 1, 2 * i + di, 2 * j + dj) for dj in (1, 0) for di in (1, 0)]
+        else:
+            leaves.append((level, i, j))
+    return sorted(leaves)
+
+
+def adaptive_grid(leaves, per_side=8):
+    """per_side x per_side cell-centred points in every leaf; weight = leaf area / per_side^2."""
+    pts, w = [], []
+    for level, i, j in leaves:
+        b = 2.0 / (1 << level)
+        h = b / per_side
+        c = (np.arange(per_side) + 0.5) * h
+        xx, yy = np.meshgrid(-1.0 + i * b + c, -1.0 + j * b + c, indexing="xy")
+        pts.append(np.stack([xx.ravel(), yy.ravel()], axis=1))
+        w.append(np.full(per_side * per_side, h * h))
+    return np.concatenate(pts), np.concatenate(w)
+
+
 # name -> (grid n, kappa, contrast, nca_tol, rhs angle, gmres tol)
 CONFIGS = {
     "c1": dict(n=64, kappa=10.0, contrast="gaussian", nca_tol=1e-8, angle=0.0, gmres_tol=1e-8),
     "c2": dict(n=256, kappa=40.0, contrast="gaussian", nca_tol=1e-8, angle=0.0, gmres_tol=1e-8),
     "c3": dict(n=512, kappa=80.0, contrast="disk", nca_tol=1e-7, angle=30.0, gmres_tol=1e-6),
     "c4": dict(n=1024, kappa=160.0, contrast="bumps", nca_tol=1e-6, angle=0.0, gmres_tol=1e-6),
+    # adaptive (n = max depth): q = smoothed disk, plane wave along x1, nca_tol unstated (1e-6)
+    "c5": dict(n=10, kappa=200.0, contrast="smoothed_disk", nca_tol=1e-6, angle=0.0, gmres_tol=1e-6),
 }
 
 
 def make_problem(name, n=None, kappa=None):
     """Return dict(points, weights, q, kappa, nca_tol, leaf_size, x, f, gmres_tol) for a config.
-    `n` / `kappa` override the grid size / wavenumber for scaled-down variants that keep
-    kappa h fixed when both are scaled together."""
+    `n` / `kappa` override the grid size (the maximum depth for the adaptive config 5) and the
+    wavenumber, for scaled-down variants."""
     cfg = dict(CONFIGS[name])
     if n is not None:
         cfg["n"] = n
     if kappa is not None:
         cfg["kappa"] = kappa
-    pts, w = grid_points(cfg["n"])
-    q = {"gaussian": gaussian_q, "disk": disk_q, "bumps": bumps_q}[cfg["contrast"]](pts)
+    if cfg["contrast"] == "smoothed_disk":
+        pts, w = adaptive_grid(adaptive_leaves(cfg["kappa"], cfg["n"]))
+    else:
+        pts, w = grid_points(cfg["n"])
+    q = {"gaussian": gaussian_q, "disk": disk_q, "bumps": bumps_q,
+         "smoothed_disk": smoothed_disk_q}[cfg["contrast"]](pts)
     x = unit_phase_vector(pts.shape[0], seed=0)
     f = plane_wave_rhs(pts, q, cfg["kappa"], cfg["angle"])
     return dict(name=name, points=pts, weights=w, q=q, kappa=cfg["kappa"], nca_tol=cfg["nca_tol"],

@@ -47,7 +47,8 @@ def _host_plan(P, tmp_path, **opts):
     return load_plan(tmp_path / "plan"), stats
 
 
-@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0)])
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0), ("c5", 5, 12.0),
+                                          ("c5", 5, 8.0), ("c5", 6, 30.0)])
 def test_host_setup_matches_oracle_lists_and_pivots(name, n, kappa, tmp_path):
     P = make_problem(name, n=n, kappa=kappa)
     plan, stats = _host_plan(P, tmp_path)

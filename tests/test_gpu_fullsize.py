@@ -13,7 +13,7 @@ from synth.configs import make_problem
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,rows", [("c2", 128), ("c3", 96), ("c4", 64)])
+@pytest.mark.parametrize("name,rows", [("c2", 128), ("c3", 96), ("c4", 64), ("c5", 48)])
 def test_full_size_sampled_rows(name, rows):
     import paper_2204_00326_b200 as prod
     P = make_problem(name)

@@ -1,6 +1,7 @@
 """GPU parity: the CUDA DAFMM (through the C-ABI) against the oracle's serial DAFMM on the
 product's validated pivots (<= 1e-11 relative l2 on y - x, D10) and against the dense
-product (<= 10 nca_tol); edge cases; sampled rows at full config-4 size."""
+product (<= 10 nca_tol); uniform and adaptive (config 5, leaves on several levels) trees;
+edge cases."""
 import numpy as np
 import pytest
 
@@ -47,7 +48,8 @@ def _oracle_on_product_plan(P, op, tmp_path):
 
 
 @pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0),
-                                          ("c1", 128, 4.0), ("c1", 40, 7.0)])
+                                          ("c1", 128, 4.0), ("c1", 40, 7.0), ("c5", 5, 12.0), ("c5", 5, 8.0),
+                                          ("c5", 6, 30.0)])
 def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     P = make_problem(name, n=n, kappa=kappa)
     op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])

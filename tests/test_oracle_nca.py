@@ -142,7 +142,8 @@ def test_single_level_tree_equals_dense():
     assert np.allclose(nca.matvec(P["x"]), oracle.dense_matvec(prob, P["x"]), rtol=1e-14, atol=1e-15)
 
 
-@pytest.mark.parametrize("name,n,kappa", [("c2", 128, 20.0), ("c3", 128, 20.0), ("c1", 128, 4.0)])
+@pytest.mark.parametrize("name,n,kappa", [("c2", 128, 20.0), ("c3", 128, 20.0), ("c1", 128, 4.0), ("c5", 4, 12.0),
+                                          ("c5", 5, 8.0)])
 def test_dafmm_matches_dense_scaled_configs(name, n, kappa):
     """Config-2/3 geometry at quarter size (two HFR levels / disk contrast with exact zeros) and
     a low-frequency case with LFR non-leaf levels (plain M2M / L2L)."""

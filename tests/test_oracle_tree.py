@@ -14,28 +14,48 @@ def _build(name, n=None, kappa=None):
     return P, tree, Lists(tree)
 
 
-@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c1", 64, 3.0)])
-def test_pair_completeness(name, n, kappa):
-    """Every ordered pair of leaves is covered exactly once: by the leaf near field N(B), or by
-    exactly one (level, ancestor pair) of an interaction list (FMM partition of A)."""
-    _, tree, lists = _build(name, n, kappa)
-    L = tree.L
-    leaves = tree.keys(L)
+def _cover_matrix(tree, lists):
+    """How often each ordered pair of leaves (target, source) is covered: by the near field of
+    the target leaf, or by an interaction-list pair (level, B, A) of boxes containing them."""
+    leaves = tree.all_leaves()
     idx = {k: i for i, k in enumerate(leaves)}
+    under = {}
+    for l in range(tree.L + 1):
+        for key in tree.boxes[l]:
+            under[(l, key)] = [idx[c] for c in tree.leaf_descendants(l, key)]
     cover = np.zeros((len(leaves), len(leaves)), dtype=np.int64)
-    for b in leaves:
-        for a in lists.N[L][b]:
+    for b, near in lists.near.items():
+        for a in near:
             cover[idx[b], idx[a]] += 1
-    for l in range(1, L + 1):
-        sh = L - l
-        anc = {}
-        for k in leaves:
-            anc.setdefault((k[0] >> sh, k[1] >> sh), []).append(idx[k])
+    for l in range(1, tree.L + 1):
         for b, il in lists.IL[l].items():
             for a in il:
-                for i in anc[b]:
-                    cover[i, anc[a]] += 1
+                for i in under[(l, b)]:
+                    cover[i, under[(l, a)]] += 1
+    return cover
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c1", 64, 3.0), ("c5", 5, 12.0),
+                                          ("c5", 5, 8.0), ("c5", 6, 30.0)])
+def test_pair_completeness(name, n, kappa):
+    """Every ordered pair of leaves is covered exactly once: by the target leaf's near field, or
+    by exactly one (level, ancestor pair) of an interaction list (FMM partition of A,
+    P:643-755).  The c5 cases are adaptive trees with leaves on several levels."""
+    _, tree, lists = _build(name, n, kappa)
+    cover = _cover_matrix(tree, lists)
     assert cover.min() == 1 and cover.max() == 1
+
+
+def test_adaptive_tree_structure():
+    """Config-5 tree (scaled): leaves on levels 3-5, all LFR (rule 3), 64 points each,
+    points of every box contiguous in a Morton-ordered permutation."""
+    P, tree, lists = _build("c5", 5, 12.0)
+    levels = sorted({l for l, _ in tree.all_leaves()})
+    assert levels == [3, 4, 5]
+    for l, k in tree.all_leaves():
+        assert not tree.is_hfr(l) and tree.boxes[l][k].size == 64
+    n = sum(tree.boxes[l][k].size for l, k in tree.all_leaves())
+    assert n == P["points"].shape[0]
 
 
 def test_config1_pair_counts():
