@@ -196,9 +196,13 @@ def load_json(path):
 
 def workload_name(P):
     cfg = CONFIGS[P["name"]]
-    return ("%s: %dx%d cell-centred grid on [-1,1]^2, N=%d, kappa=%g, q=%s, x=unit-modulus seeded phases, "
-            "leaf 64, nca_tol %g" % (P["name"], cfg["n"], cfg["n"], P["points"].shape[0], P["kappa"],
-                                      cfg["contrast"], P["nca_tol"]))
+    n = P["points"].shape[0]
+    if cfg["contrast"] == "smoothed_disk":
+        grid = "adaptive quadtree (depth %d, refinement rule 3), 8x8 cell-centred points per leaf" % cfg["n"]
+    else:
+        grid = "%dx%d cell-centred grid on [-1,1]^2" % (cfg["n"], cfg["n"])
+    return ("%s: %s, N=%d, kappa=%g, q=%s, x=unit-modulus seeded phases, leaf 64, nca_tol %g"
+            % (P["name"], grid, n, P["kappa"], cfg["contrast"], P["nca_tol"]))
 
 
 # ---------------------------------------------------------------------------------------------

@@ -180,17 +180,18 @@ class NCA:
         # a leaf in the interaction list (adaptive trees) has no children: its own pivots at
         # this level stand for its points (it enters M2L through s^{A,o} / t^{A,i})
         far_leaves = [e[0] for e in far if e[1] is None and tree.is_leaf(level, e[0])]
+        parent_far = [] if tree.is_hfr(level) else self.parent_far_points(level, node)
         si = _union([self.pivots[level + 1][c]["so"] for c in far_kids] +
-                    [self.pivots[level][a]["so"] for a in far_leaves])
+                    [self.pivots[level][a]["so"] for a in far_leaves] + parent_far)
         to = _union([self.pivots[level + 1][c]["ti"] for c in far_kids] +
-                    [self.pivots[level][a]["ti"] for a in far_leaves])
+                    [self.pivots[level][a]["ti"] for a in far_leaves] + parent_far)
         return dict(ti=ti, si=si, to=to, so=so)
 
     def parent_far_points(self, level, node):
-        """Reading R16 (adaptive trees): a leaf whose LFR parent P has a leaf among its
+        """Reading R16 (adaptive trees): an LFR node whose LFR parent P has a leaf among its
         neighbours gets no interaction-list boxes in that direction (IL(B) is made of the children
         of P's neighbours), although sources there reach it through P's local expansion.  Its
-        far-field search sets then also take the points of IL(P), so the leaf's bases see every
+        far-field search sets then also take the points of IL(P), so its bases see every
         direction its far field arrives from.  Never triggers on a uniform tree."""
         tree, lists = self.tree, self.lists
         if level < 2 or tree.is_hfr(level - 1):

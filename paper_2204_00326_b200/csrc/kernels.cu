@@ -177,23 +177,50 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // IndexStager: the M2L stream is a flat list of multipole slots (idx), so every thread finds
 // its source directly.  RunStager: the near-field stream is a few runs of consecutive points
 // (the neighbour leaves), walked with a cursor that every thread advances identically.
+template <int STAGE, int NT>
 struct IndexStager {
+  // idx of the chunk after the one being staged is prefetched into registers one chunk ahead,
+  // so issuing its copies never waits on the index load
+  static constexpr int kSlots = (STAGE + NT - 1) / NT;
   const int32_t* idx;
   int64_t base;
   int total;
   const double2* xy;
   const double2* val;
-  template <int STAGE>
-  __device__ __forceinline__ int stage(double4* buf, int c0) {
-    const int fill = min(STAGE, total - c0);
-    for (int q = threadIdx.x; q < fill; q += blockDim.x) {
-      const int k = __ldg(idx + base + c0 + q);
-      double2* d = reinterpret_cast<double2*>(buf + q);
-      cp_async16(d, xy + k);
-      cp_async16(d + 1, val + k);
+  int kreg[kSlots];
+  __device__ __forceinline__ void prefetch(int c0) {
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      const int q = threadIdx.x + s * NT;
+      kreg[s] = (q < STAGE && c0 + q < total) ? __ldg(idx + base + c0 + q) : 0;
+    }
+  }
+  __device__ __forceinline__ int issue(double4* buf, int c0) {
+    const int fill = max(0, min(STAGE, total - c0));
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+      const int q = threadIdx.x + s * NT;
+      if (q < fill) {
+        double2* d = reinterpret_cast<double2*>(buf + q);
+        cp_async16(d, xy + kreg[s]);
+        cp_async16(d + 1, val + kreg[s]);
+      }
     }
     cp_async_commit();
-    return max(fill, 0);
+    return fill;
+  }
+  template <int S>
+  __device__ __forceinline__ int first(double4* buf) {
+    prefetch(0);
+    const int fill = issue(buf, 0);
+    prefetch(fill);
+    return fill;
+  }
+  template <int S>
+  __device__ __forceinline__ int next(double4* buf, int c0) {
+    const int fill = issue(buf, c0);  // indices prefetched during the previous chunk
+    prefetch(c0 + fill);
+    return fill;
   }
 };
 struct RunStager {
@@ -223,6 +250,14 @@ struct RunStager {
     }
     cp_async_commit();
     return fill;
+  }
+  template <int S>
+  __device__ __forceinline__ int first(double4* buf) {
+    return stage<S>(buf, 0);
+  }
+  template <int S>
+  __device__ __forceinline__ int next(double4* buf, int c0) {
+    return stage<S>(buf, c0);
   }
 };
 
@@ -356,11 +391,11 @@ __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, cons
                                                   int slice, int nsl, double& ar, double& ai, const PolyTable& T,
                                                   const FarBand* bands) {
   int c0 = 0, which = 0, it0 = items.is;
-  int fill = st.template stage<STAGE>(buf, 0);
+  int fill = st.template first<STAGE>(buf);
   while (fill > 0) {
     cp_async_wait_all();
     __syncthreads();  // chunk `which` visible to all; everyone is done with the other buffer
-    const int next = st.template stage<STAGE>(buf + (which ^ 1) * STAGE, c0 + fill);
+    const int next = st.template next<STAGE>(buf + (which ^ 1) * STAGE, c0 + fill);
     const int c1 = c0 + fill;
     while (it0 < items.ie && items.pe(it0) <= c0) ++it0;
     if (active) {
@@ -414,7 +449,8 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
       const bool active = slice < nsl;
       double2 xt = ld2(ti_xy + lo + t0 + t);
       double ar = 0.0, ai = 0.0;
-      IndexStager st{stream_idx, stream_ptr[tgt], (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]), so_xy, mult};
+      IndexStager<kM2LStage, kM2LThreads> st{stream_idx, stream_ptr[tgt], (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]),
+                                              so_xy, mult, {}};
       stream_accumulate<kM2LStage>(buf, st, items, xt, active, slice, nsl, ar, ai, T, bands);
       red[threadIdx.x] = make_double2(ar, ai);
       __syncthreads();

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <sys/stat.h>
@@ -597,6 +598,20 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
               si.insert(si.end(), pc.so.begin(), pc.so.end());
               to.insert(to.end(), pc.ti.begin(), pc.ti.end());
             }
+          }
+          // reading R16 for non-leaf nodes: the points of IL(parent) when the LFR parent has a
+          // leaf neighbour (the directions its own interaction list does not reach)
+          if (!lv.hfr && l >= 2 && !pv.hfr) {
+            const Box& B = lv.boxes[b];
+            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+            bool leaf_nb = false;
+            for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
+            if (leaf_nb)
+              for (int a : pv.IL[pb])
+                for (int32_t t = pv.boxes[a].begin; t < pv.boxes[a].end; ++t) {
+                  si.push_back(P.perm[t]);
+                  to.push_back(P.perm[t]);
+                }
           }
           sorted_union(ti);
           sorted_union(so);
