@@ -9,7 +9,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "_lib", "libdafmm.so")
+_LIB_PATH = os.path.join(_HERE, "_lib", os.environ.get("DAFMM_LIB_NAME") or "libdafmm.so")
 _lib = None
 
 EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_matvec", "dafmm_matvec_parts",

@@ -13,6 +13,11 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "libdafmm.so")
+# experiments: DAFMM_NVCC_FLAGS adds nvcc flags, DAFMM_LIB_NAME builds a differently named library
+# (the binding loads DAFMM_LIB_NAME too when it is set)
+EXTRA = os.environ.get("DAFMM_NVCC_FLAGS", "").split()
+if os.environ.get("DAFMM_LIB_NAME"):
+    LIB = os.path.join(OUT_DIR, os.environ["DAFMM_LIB_NAME"])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["kernels.cu"]
@@ -34,7 +39,8 @@ def build(verbose=False, force=False, ptxas_verbose=False):
     objs = []
     for f in CU_SOURCES:
         o = os.path.join(OUT_DIR, f + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *inc, "-c",
+        o = os.path.join(OUT_DIR, os.path.basename(LIB) + "." + f + ".o")
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *EXTRA, *inc, "-c",
                os.path.join(CSRC, f), "-o", o]
         if ptxas_verbose:
             cmd += ["-Xptxas", "-v"]

@@ -73,6 +73,31 @@ DAFMM_HD void horner2(const Pair* c, const double* x, double* a, double* b) {
   }
 }
 
+// Fixed-degree polynomials: immediates (DAFMM_POLY_IMM, the default) or the shared-memory table.
+#ifndef DAFMM_POLY_IMM
+#define DAFMM_POLY_IMM 1
+#endif
+template <int TB>
+DAFMM_HD void poly_log1p(const PolyTable& T, const double* x, double* a, double* b) {
+  if (DAFMM_POLY_IMM) dafmm_fit::log1p_imm<TB>(x, a, b);
+  else horner2<dafmm_fit::LOG1P_N, TB>(T.log1p, x, a, b);
+}
+template <int TB>
+DAFMM_HD void poly_sincos(const PolyTable& T, const double* x, double* a, double* b) {
+  if (DAFMM_POLY_IMM) dafmm_fit::sincos_imm<TB>(x, a, b);
+  else horner2<dafmm_fit::SC_N, TB>(T.sincos, x, a, b);
+}
+template <int ZN, int TB>
+DAFMM_HD void poly_near(const PolyTable& T, const double* x, double* a, double* b) {
+  if (DAFMM_POLY_IMM) {
+    if (ZN == 8) dafmm_fit::near8_imm<TB>(x, a, b);
+    else dafmm_fit::near12_imm<TB>(x, a, b);
+  } else {
+    if (ZN == 8) horner2<dafmm_fit::NEAR8_N, TB>(T.near8, x, a, b);
+    else horner2<dafmm_fit::NEAR12_N, TB>(T.near12, x, a, b);
+  }
+}
+
 // ln(z2 / 4) for TB positive normal z2.
 template <int TB>
 DAFMM_HD void log_quarter_vec(const double* z2, double* out, const PolyTable& T) {
@@ -90,7 +115,7 @@ DAFMM_HD void log_quarter_vec(const double* z2, double* out, const PolyTable& T)
     lc[i] = tb.b;
     r2[i] = r[i] * r[i];
   }
-  horner2<dafmm_fit::LOG1P_N, TB>(T.log1p, r2, qe, qo);
+  poly_log1p<TB>(T, r2, qe, qo);
 #pragma unroll
   for (int i = 0; i < TB; ++i)
     out[i] = fma((double)e[i], dafmm_fit::LN2, lc[i] + fma(r2[i], fma(r[i], qo[i], qe[i]), r[i]));
@@ -112,7 +137,7 @@ DAFMM_HD void h0_near_vec(const double* z2, double* re, double* im, const PolyTa
 #pragma unroll
   for (int i = 0; i < TB; ++i) t[i] = fma(z2[i], ts, -1.0);
   if constexpr (IMM) dafmm_fit::near8_imm<TB>(t, j0, rr);
-  else horner2<n, TB>(ZN == 8 ? T.near8 : T.near12, t, j0, rr);
+  else poly_near<ZN, TB>(T, t, j0, rr);
   log_quarter_vec<TB>(z2, lu, T);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
@@ -168,7 +193,7 @@ DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, dou
     rh2[i] = rho[i] * rho[i];
     quad[i] = (int)qf;
   }
-  horner2<dafmm_fit::SC_N, TB>(T.sincos, rh2, sp, c);
+  poly_sincos<TB>(T, rh2, sp, c);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
     const double s = rho[i] * sp[i];
@@ -190,7 +215,8 @@ template <int TB>
 struct GenericFarPQ {
   const PolyTable& T;
   DAFMM_HD void operator()(const double* x, double* P, double* Q) const {
-    horner2<dafmm_fit::GENERIC_FAR_N, TB>(T.generic_far, x, P, Q);
+    if (DAFMM_POLY_IMM) dafmm_fit::generic_far_imm<TB>(x, P, Q);
+    else horner2<dafmm_fit::GENERIC_FAR_N, TB>(T.generic_far, x, P, Q);
   }
 };
 

@@ -27,7 +27,16 @@ constexpr int kM2LThreads = 128;
 constexpr int kM2LStage = 320;   // M2L: staged source pivots per chunk (32 B each, double-buffered)
 constexpr int kNearStage = 320;  // near field: staged source points per chunk
 constexpr int kCombineThreads = 64;
-constexpr int kTB = 4;
+// kernel entries evaluated in lockstep per thread (each coefficient shared by TB FMAs); measured
+// best: 8 for P2P, 4 for M2L (whose far-type evaluator needs more registers per entry)
+#ifndef DAFMM_TB_P2P
+#define DAFMM_TB_P2P 8
+#endif
+#ifndef DAFMM_TB_M2L
+#define DAFMM_TB_M2L 4
+#endif
+constexpr int kTBP2P = DAFMM_TB_P2P;
+constexpr int kTBM2L = DAFMM_TB_M2L;
 constexpr int kBandNear8Imm = -1;  // kernel-internal: band near-8 with immediate coefficients (P2P)       // kernel entries evaluated in lockstep per thread (shared coefficients)
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
@@ -263,19 +272,19 @@ struct RunStager {
 
 // Items of an M2L target: band code and stream range, from the packed plan.
 struct M2LItems {
+  static constexpr int kTB = kTBM2L;
   static constexpr bool kGuarded = false;  // no i == j pairs
   static constexpr bool kNearOnly = false;
-  const int32_t* code_;
-  const int32_t* pb_;
-  const int32_t* pe_;
+  const int4* it_;  // (code, pb, pe, -) in shared memory: read once per chunk by every thread
   int is, ie;
-  __device__ __forceinline__ int code(int i) const { return code_[i]; }
+  __device__ __forceinline__ int code(int i) const { return it_[i].x; }
   __device__ __forceinline__ bool guard(int) const { return false; }
-  __device__ __forceinline__ int pb(int i) const { return pb_[i]; }
-  __device__ __forceinline__ int pe(int i) const { return pe_[i]; }
+  __device__ __forceinline__ int pb(int i) const { return it_[i].y; }
+  __device__ __forceinline__ int pe(int i) const { return it_[i].z; }
 };
 // Items of a near-field leaf: its own block [0, own) (contains i == j) and the rest.
 struct NearItems {
+  static constexpr int kTB = kTBP2P;
   static constexpr bool kGuarded = true;   // item 0 holds the i == j pairs
   static constexpr bool kNearOnly = true;  // bands: near-8, near-12 or generic
   int band, own, total, is, ie;
@@ -286,26 +295,26 @@ struct NearItems {
 };
 
 // Band evaluator by code (compile time): generic, near 8, near 12, or a data band.
-template <int CODE>
+template <int CODE, int TB>
 __device__ __forceinline__ void eval_band(const double* z2, double* re, double* im, const PolyTable& T,
                                           const FarBand* band) {
-  if constexpr (CODE == kBandGeneric) h0_generic_vec<kTB>(z2, re, im, T);
-  else if constexpr (CODE == kBandNear8) h0_near_vec<8, kTB>(z2, re, im, T);
-  else if constexpr (CODE == kBandNear8Imm) h0_near_vec<8, kTB, true>(z2, re, im, T);
-  else if constexpr (CODE == kBandNear12) h0_near_vec<12, kTB>(z2, re, im, T);
-  else h0_far_vec<kTB>(z2, re, im, band->A, band->B, DataFarPQ<kTB>{band}, T);
+  if constexpr (CODE == kBandGeneric) h0_generic_vec<TB>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear8) h0_near_vec<8, TB>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear8Imm) h0_near_vec<8, TB, true>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear12) h0_near_vec<12, TB>(z2, re, im, T);
+  else h0_far_vec<TB>(z2, re, im, band->A, band->B, DataFarPQ<TB>{band}, T);
 }
 
 // One lockstep block of kTB staged sources p[0], p[stride], ...: acc += sum_q H0(|xt - s_q|) v_q.
 // MASK: only the first `valid` sources count (tail block); GUARD: the pair i == j (own leaf of
 // the near field; its value is the self term D_i) is excluded.  Excluded lanes get a safe z^2
 // and a zero weight so the evaluator stays branch-free.
-template <int CODE, bool GUARD, bool MASK>
+template <int CODE, int TB, bool GUARD, bool MASK>
 __device__ __forceinline__ void consume_block(const double4* p, int stride, int valid, double2 xt, double& ar, double& ai,
                                               const PolyTable& T, const FarBand* band) {
   if constexpr (CODE == kBandGeneric) {  // rare (straddling segments): one lane at a time
 #pragma unroll 1
-    for (int q = 0; q < (MASK ? valid : kTB); ++q) {
+    for (int q = 0; q < (MASK ? valid : TB); ++q) {
       const double4 sv = p[q * stride];
       const double dx = xt.x - sv.x, dy = xt.y - sv.y;
       const double d2 = fma(dx, dx, dy * dy);
@@ -317,10 +326,10 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
     }
     return;
   }
-  double z2[kTB], hr[kTB], hi[kTB];
-  bool use[kTB];
+  double z2[TB], hr[TB], hi[TB];
+  bool use[TB];
 #pragma unroll
-  for (int q = 0; q < kTB; ++q) {
+  for (int q = 0; q < TB; ++q) {
     const bool ok = !MASK || q < valid;
     const double2 sp = *reinterpret_cast<const double2*>(p + ((MASK && !ok) ? 0 : q * stride));
     const double dx = xt.x - sp.x, dy = xt.y - sp.y;
@@ -328,11 +337,11 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
     use[q] = ok && (!GUARD || d2 > 0.0);
     z2[q] = (MASK || GUARD) ? (use[q] ? d2 : kZ2Safe) : d2;
   }
-  eval_band<CODE>(z2, hr, hi, T, band);
+  eval_band<CODE, TB>(z2, hr, hi, T, band);
   // the weights are re-read from shared memory after the evaluation (not held in registers
   // across it: the evaluator needs every register it can get)
 #pragma unroll
-  for (int q = 0; q < kTB; ++q) {
+  for (int q = 0; q < TB; ++q) {
     double2 v = reinterpret_cast<const double2*>(p + ((MASK && q >= valid) ? 0 : q * stride))[1];
     if (MASK || GUARD) {
       v.x = use[q] ? v.x : 0.0;
@@ -346,39 +355,39 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
 // acc += sum_{j in [a, b)} H0(|xt - s_j|) v_j over staged sources (kappa-scaled coordinates).
 // The range is cut into blocks of kTB consecutive sources, dealt to the slices cyclically
 // (block k to slice k mod nsl); only the last block of the range can be partial (masked).
-template <int CODE, bool GUARD>
+template <int CODE, int TB, bool GUARD>
 __device__ __forceinline__ void consume(const double4* sb, int a, int b, double2 xt, int slice, int nsl, double& ar,
                                         double& ai, const PolyTable& T, const FarBand* band) {
   const int n = b - a;
-  const int full = n / kTB;
+  const int full = n / TB;
   for (int k = slice; k < full; k += nsl)
-    consume_block<CODE, GUARD, false>(sb + a + k * kTB, 1, kTB, xt, ar, ai, T, band);
-  if ((n % kTB) && slice == full % nsl)
-    consume_block<CODE, GUARD, true>(sb + a + full * kTB, 1, n % kTB, xt, ar, ai, T, band);
+    consume_block<CODE, TB, GUARD, false>(sb + a + k * TB, 1, TB, xt, ar, ai, T, band);
+  if ((n % TB) && slice == full % nsl)
+    consume_block<CODE, TB, GUARD, true>(sb + a + full * TB, 1, n % TB, xt, ar, ai, T, band);
 }
 
 // Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only near-8, near-12 and
 // generic occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
-template <bool GUARD, bool NEAR_ONLY>
+template <int TB, bool GUARD, bool NEAR_ONLY>
 __device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
                                              double& ar, double& ai, const PolyTable& T, const FarBand* bands) {
   if constexpr (NEAR_ONLY) {
-    if (code == kBandNear8) consume<kBandNear8Imm, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
-    else if (code == kBandNear12) consume<kBandNear12, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
-    else consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    if (code == kBandNear8) consume<kBandNear8Imm, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    else if (code == kBandNear12) consume<kBandNear12, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    else consume<kBandGeneric, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
   } else {
     switch (code) {
       case kBandNear8:
-        consume<kBandNear8, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        consume<kBandNear8, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
         break;
       case kBandNear12:
-        consume<kBandNear12, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        consume<kBandNear12, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
         break;
       case kBandGeneric:
-        consume<kBandGeneric, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        consume<kBandGeneric, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
         break;
       default:
-        consume<kBandFarData, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands + (code - kBandFarData));
+        consume<kBandFarData, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands + (code - kBandFarData));
     }
   }
 }
@@ -403,9 +412,10 @@ __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, cons
       for (int it = it0; it < items.ie && items.pb(it) < c1; ++it) {
         const int a = max(items.pb(it), c0) - c0, b = min(items.pe(it), c1) - c0;
         if (Items::kGuarded && items.guard(it))
-          consume_code<Items::kGuarded, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+          consume_code<Items::kTB, Items::kGuarded, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar,
+                                                                      ai, T, bands);
         else
-          consume_code<false, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+          consume_code<Items::kTB, false, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
       }
     }
     c0 = c1;
@@ -417,7 +427,10 @@ __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, cons
 
 // ---- M2L: u[t] = sum_{src nodes} sum_k H0(kappa |t - s_k|) m_k --------------------
 // One CTA per target node; its source stream is cut into band-uniform items.
-__global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
+#ifndef DAFMM_M2L_MINB
+#define DAFMM_M2L_MINB 6
+#endif
+__global__ void __launch_bounds__(kM2LThreads, DAFMM_M2L_MINB) m2l_kernel(
     int ntargets, int* __restrict__ ticket, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
     const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx, const int32_t* __restrict__ item_ptr,
     const int32_t* __restrict__ item_code, const int32_t* __restrict__ item_pb, const int32_t* __restrict__ item_pe,
@@ -427,6 +440,7 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
   __shared__ double2 red[kM2LThreads];
   __shared__ PolyTable T;
   __shared__ FarBand bands[dafmm_fit::NUM_FAR];
+  __shared__ int4 sitems[kNumBandCodes];
   __shared__ int next;
   load_poly_table(T);
   load_far_bands(bands);
@@ -440,7 +454,12 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
     if (tgt >= ntargets) break;
     const int r = rows[tgt];
     const int64_t lo = loc_off[tgt];
-    const M2LItems items{item_code, item_pb, item_pe, item_ptr[tgt], item_ptr[tgt + 1]};
+    // the target's items (at most kNumBandCodes) into shared memory
+    const int i0 = item_ptr[tgt], ni = item_ptr[tgt + 1] - i0;
+    for (int i = threadIdx.x; i < ni; i += blockDim.x)
+      sitems[i] = make_int4(item_code[i0 + i], item_pb[i0 + i], item_pe[i0 + i], 0);
+    __syncthreads();
+    const M2LItems items{sitems, 0, ni};
     for (int t0 = 0; t0 < r; t0 += kM2LThreads) {
       const int rc = min(kM2LThreads, r - t0);
       const int nsl = kM2LThreads / rc;
@@ -471,7 +490,10 @@ __global__ void __launch_bounds__(kM2LThreads, 6) m2l_kernel(
 // ---- near field P2P ------------------------------------------------------------
 // phi_t = sum_{j in N(leaf), j != t} H0(kappa |x_t - x_j|) v_j   (H0 units, tree order).
 // The leaf's own block is the first near entry (the only one with i == j pairs).
-__global__ void __launch_bounds__(kNearThreads, 3) p2p_kernel(
+#ifndef DAFMM_P2P_MINB
+#define DAFMM_P2P_MINB 3
+#endif
+__global__ void __launch_bounds__(kNearThreads, DAFMM_P2P_MINB) p2p_kernel(
     const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end, const int32_t* __restrict__ near_ptr,
     const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int32_t* __restrict__ leaf_band,
     const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi) {

@@ -268,9 +268,14 @@ def main(out_path):
     w("    a[i] = fma(a[i], x[i], ca);               \\")
     w("    b[i] = fma(b[i], x[i], cb);               \\")
     w("  }")
-    w(h2_function("near8_imm", nears[0][0], nears[0][1],
-                  "(J0, R) of the near band z <= 8 with the coefficients as immediates (the P2P kernel: "
-                  "fp64-pipe-bound, it prefers issue slots to shared-memory latency)"))
+    w("// The same fixed-degree polynomials with their coefficients as immediates (uniform-register")
+    w("// operands of DFMA, shared by the TB lanes of a block); measured faster than shared-memory")
+    w("// coefficients for both the P2P and the M2L kernel (DESIGN.md §6).")
+    w(h2_function("near8_imm", nears[0][0], nears[0][1], "(J0, R), z <= 8"))
+    w(h2_function("near12_imm", nears[1][0], nears[1][1], "(J0, R), z <= 12"))
+    w(h2_function("generic_far_imm", gfar[0], gfar[1], "(P, Q) of the generic far band [8, inf)"))
+    w(h2_function("sincos_imm", cs, cc, "(sin(rho)/rho, cos(rho)) in rho^2"))
+    w(h2_function("log1p_imm", qe, qo, "(qe, qo) in r^2"))
     w("// Coefficient pairs of every fixed-degree polynomial and the log table.  The kernels copy it")
     w("// to shared memory once per CTA; one 128-bit broadcast load then feeds the 2 x TB FMAs of a")
     w("// lane-blocked Horner step (64-bit immediates would cost two UMOVs each on sm_100a).")
