@@ -23,8 +23,17 @@ namespace dafmm {
 namespace {
 
 constexpr int kNearThreads = 256;
-constexpr int kM2LThreads = 128;
-constexpr int kM2LStage = 320;   // M2L: staged source pivots per chunk (32 B each, double-buffered)
+#ifndef DAFMM_M2L_THREADS
+#define DAFMM_M2L_THREADS 128
+#endif
+#ifndef DAFMM_M2L_STAGE
+#define DAFMM_M2L_STAGE 320
+#endif
+#ifndef DAFMM_BANDS_CONST
+#define DAFMM_BANDS_CONST 0
+#endif
+constexpr int kM2LThreads = DAFMM_M2L_THREADS;
+constexpr int kM2LStage = DAFMM_M2L_STAGE;  // M2L: staged source pivots per chunk (32 B each, double-buffered)
 constexpr int kNearStage = 320;  // near field: staged source points per chunk
 constexpr int kCombineThreads = 64;
 // kernel entries evaluated in lockstep per thread (each coefficient shared by TB FMAs); measured
@@ -439,11 +448,17 @@ __global__ void __launch_bounds__(kM2LThreads, DAFMM_M2L_MINB) m2l_kernel(
   __shared__ __align__(16) double4 buf[2 * kM2LStage];
   __shared__ double2 red[kM2LThreads];
   __shared__ PolyTable T;
+#if DAFMM_BANDS_CONST
+  const FarBand* bands = dafmm_fit::kFarBandsDev;  // uniform constant-bank loads per coefficient pair
+#else
   __shared__ FarBand bands[dafmm_fit::NUM_FAR];
+#endif
   __shared__ int4 sitems[kNumBandCodes];
   __shared__ int next;
   load_poly_table(T);
+#if !DAFMM_BANDS_CONST
   load_far_bands(bands);
+#endif
   // persistent CTAs take target nodes from a ticket counter (targets are packed by
   // decreasing cost, so the dynamic order balances the tail)
   while (true) {
