@@ -216,7 +216,8 @@ def oracle_rows_sample(P, target_s, max_rows=4096):
     prob = oracle.Problem(P["points"], P["weights"], P["q"], P["kappa"])
     n = prob.n
     rng = np.random.default_rng(12345)
-    probe = np.sort(rng.choice(n, size=min(16, n), replace=False))
+    oracle.dense_matvec_rows(prob, P["x"], np.arange(min(2, n)))  # load the library, start the threads
+    probe = np.sort(rng.choice(n, size=min(64, n), replace=False))
     t0 = time.perf_counter()
     oracle.dense_matvec_rows(prob, P["x"], probe)
     dt = time.perf_counter() - t0

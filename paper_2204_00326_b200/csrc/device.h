@@ -13,7 +13,10 @@ namespace dafmm {
 // gather, p2m, m2m, m2l, l2l, near (P2P, side stream), combine (L2P + identity + scatter), and the
 // span of the concurrent part (from the fork to the later of P2P and L2L)
 constexpr int kNumPasses = 8;
-enum ProfEvent { EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_NEAR0, EV_NEAR1, EV_JOIN, EV_END, EV_COUNT };
+// marks recorded before the pass they name (EV_FAR_END after L2L); see harvest_profile
+enum ProfEvent {
+  EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_FAR_END, EV_NEAR0, EV_NEAR1, EV_JOIN, EV_END, EV_COUNT
+};
 
 struct DevBatch {
   int items = 0;

@@ -895,9 +895,10 @@ int harvest_profile(DevPlan& d, std::string& err) {
     return true;
   };
   double t[kNumPasses], near_end = 0.0, far_end = 0.0;
-  if (!el(EV_START, EV_FORK, t[0]) || !el(EV_FORK, EV_P2M, t[1]) || !el(EV_P2M, EV_M2M, t[2]) ||
-      !el(EV_M2M, EV_M2L, t[3]) || !el(EV_M2L, EV_L2L, t[4]) || !el(EV_NEAR0, EV_NEAR1, t[5]) ||
-      !el(EV_JOIN, EV_END, t[6]) || !el(EV_FORK, EV_NEAR1, near_end) || !el(EV_FORK, EV_L2L, far_end))
+  // gather | memsets + P2M | M2M | M2L | L2L | P2P (side stream) | combine | fork-to-join span
+  if (!el(EV_START, EV_FORK, t[0]) || !el(EV_FORK, EV_M2M, t[1]) || !el(EV_M2M, EV_M2L, t[2]) ||
+      !el(EV_M2L, EV_L2L, t[3]) || !el(EV_L2L, EV_FAR_END, t[4]) || !el(EV_NEAR0, EV_NEAR1, t[5]) ||
+      !el(EV_JOIN, EV_END, t[6]) || !el(EV_FORK, EV_NEAR1, near_end) || !el(EV_FORK, EV_FAR_END, far_end))
     return DAFMM_ECUDA;
   t[7] = std::max(near_end, far_end);
   for (int p = 0; p < kNumPasses; ++p) d.prof_ms[p] += t[p];
@@ -949,9 +950,10 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
                                                     d.mult, d.loc);
     ++d.launches;
   }
+  mark(EV_L2L, fs);
   if (far)
     for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1, fs);  // L2L
-  mark(EV_L2L, fs);
+  mark(EV_FAR_END, fs);
   mark(EV_NEAR0, ns);
   if (near) {  // P2P
     p2p_kernel<<<d.nleaves, kNearThreads, 0, ns>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
