@@ -43,6 +43,7 @@ void dafmm_default_options(dafmm_options* opt) {
   opt->max_level = o.max_level;
   opt->num_threads = o.num_threads;
   opt->host_only = o.host_only;
+  opt->symmetric_pivots = o.symmetric_pivots;
 }
 
 int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
@@ -57,6 +58,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.max_level = opt->max_level;
     o.num_threads = opt->num_threads;
     o.host_only = opt->host_only;
+    o.symmetric_pivots = opt->symmetric_pivots;
   }
   std::unique_ptr<dafmm_plan> h;
   try {

@@ -621,7 +621,15 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
         NodePivots& np = P.piv[l][nd];
         int64_t ent = 0;
         aca(cx, ti, si, eps, np.ti, np.si, ent);
-        aca(cx, to, so, eps, np.to, np.so, ent);
+        if (P.opt.symmetric_pivots) {
+          // reading R19: G is symmetric, and the outgoing search sets equal the incoming ones
+          // with rows and columns swapped, so the incoming skeleton (t^{B,i}, s^{B,i}) also serves
+          // as the outgoing one (s^{B,o} = t^{B,i}, t^{B,o} = s^{B,i}): one ACA per node
+          np.so = np.ti;
+          np.to = np.si;
+        } else {
+          aca(cx, to, so, eps, np.to, np.so, ent);
+        }
         level_entries += ent;
       }
     }

@@ -63,6 +63,21 @@ def test_host_setup_matches_oracle_lists_and_pivots(name, n, kappa, tmp_path):
     assert np.array_equal(np.sort(plan["perm"]), np.arange(P["points"].shape[0]))
 
 
+def test_host_setup_symmetric_pivots(tmp_path):
+    """R19: with symmetric_pivots (default) the outgoing skeleton is the incoming one swapped;
+    with 0 the two ACAs run separately.  Both pass the oracle's validation."""
+    P = make_problem("c1")
+    plan, _ = _host_plan(P, tmp_path)
+    for piv in plan["levels"][3]["pivots"].values():
+        assert np.array_equal(piv["so"], piv["ti"]) and np.array_equal(piv["to"], piv["si"])
+    plan2, _ = _host_plan(P, tmp_path / "b", symmetric_pivots=0)
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    piv = [dict()] + [plan2["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    validate_pivots(NCA(prob, tree, lists, P["nca_tol"], pivots=piv), piv)
+
+
 def test_host_setup_ragged_points(tmp_path):
     rng = np.random.default_rng(7)
     pts = rng.uniform(-1, 1, size=(3000, 2))

@@ -67,6 +67,19 @@ def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     assert _rel(near - x, nca.matvec(x, parts=("near",)) - x) <= 1e-12
 
 
+def test_gpu_two_aca_pivots_paper_form(tmp_path):
+    """symmetric_pivots=0: separate incoming and outgoing ACAs per node (P:597-634 as written)."""
+    P = make_problem("c2", n=128, kappa=20.0)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], symmetric_pivots=0)
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path)
+    x = P["x"]
+    y_gpu = _gpu_matvec(op, x)
+    assert _rel(y_gpu - x, nca.matvec(x) - x) <= 1e-11
+    rows = np.arange(0, prob.n, 3)
+    yd = oracle.dense_matvec_rows(prob, x, rows)
+    assert _rel(y_gpu[rows] - x[rows], yd - x[rows]) <= 10 * P["nca_tol"]
+
+
 def test_gpu_zero_contrast_identity_and_linearity():
     P = make_problem("c1")
     op = _prod().DAFMM(P["points"], P["weights"], np.zeros(4096), P["kappa"], 64, P["nca_tol"])
