@@ -1059,7 +1059,8 @@ bool write_npy(const std::string& path, const char* descr, const std::vector<T>&
 }  // namespace
 
 int export_plan(const Plan& P, const std::string& dir, std::string& err) {
-  mkdir(dir.c_str(), 0755);
+  for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
   bool ok = true;
   std::vector<double> meta = {(double)P.n, (double)P.L, P.W, P.x0, P.y0, P.kappa, P.opt.T, P.nca_tol};
   ok &= write_npy(dir + "/meta.npy", "<f8", meta, {(int64_t)meta.size()});
