@@ -64,9 +64,10 @@ typedef struct {
   int host_only;       /* 1: build the host plan only (no device upload; for inspection and
                           dafmm_export_plan on machines without a GPU); matvec / GMRES then
                           return DAFMM_EINVAL.  Default 0. */
-  int symmetric_pivots; /* 1 (default): one ACA per node; the outgoing skeleton is the incoming one
-                           with rows and columns swapped (reading R19, G symmetric).  0: two ACAs
-                           per node (incoming and outgoing), as P:597-634 write them. */
+  int symmetric_pivots; /* 0 (default): two ACAs per node (incoming and outgoing), as P:597-634
+                           write them.  1: one ACA per node; the outgoing skeleton is the incoming
+                           one with rows and columns swapped (reading R19, G symmetric): half the
+                           ACA setup time, 3% more M2L work at C4. */
 } dafmm_options;
 
 /* Statistics of a plan (sizes, ranks, setup times). */

@@ -24,7 +24,7 @@ struct Options {
   int max_level = 20;
   int num_threads = 0;     // host setup threads (0: OpenMP default)
   int host_only = 0;       // skip the device upload
-  int symmetric_pivots = 1;  // reading R19: one ACA per node, outgoing skeleton = incoming
+  int symmetric_pivots = 0;  // reading R19 (option): one ACA per node, outgoing skeleton = incoming
 };
 
 struct Box {

@@ -64,13 +64,13 @@ def test_host_setup_matches_oracle_lists_and_pivots(name, n, kappa, tmp_path):
 
 
 def test_host_setup_symmetric_pivots(tmp_path):
-    """R19: with symmetric_pivots (default) the outgoing skeleton is the incoming one swapped;
-    with 0 the two ACAs run separately.  Both pass the oracle's validation."""
+    """R19: with symmetric_pivots=1 the outgoing skeleton is the incoming one swapped; with 0
+    (default) the two ACAs run separately.  Both pass the oracle's validation."""
     P = make_problem("c1")
-    plan, _ = _host_plan(P, tmp_path)
+    plan, _ = _host_plan(P, tmp_path, symmetric_pivots=1)
     for piv in plan["levels"][3]["pivots"].values():
         assert np.array_equal(piv["so"], piv["ti"]) and np.array_equal(piv["to"], piv["si"])
-    plan2, _ = _host_plan(P, tmp_path / "b", symmetric_pivots=0)
+    plan2, _ = _host_plan(P, tmp_path / "b")
     tree = Tree(P["points"], P["weights"], P["kappa"], 64)
     lists = Lists(tree)
     piv = [dict()] + [plan2["levels"][l]["pivots"] for l in range(1, tree.L + 1)]

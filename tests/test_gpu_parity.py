@@ -67,10 +67,10 @@ def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     assert _rel(near - x, nca.matvec(x, parts=("near",)) - x) <= 1e-12
 
 
-def test_gpu_two_aca_pivots_paper_form(tmp_path):
-    """symmetric_pivots=0: separate incoming and outgoing ACAs per node (P:597-634 as written)."""
+def test_gpu_symmetric_pivots(tmp_path):
+    """symmetric_pivots=1 (R19): one ACA per node, the outgoing skeleton is the incoming one."""
     P = make_problem("c2", n=128, kappa=20.0)
-    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], symmetric_pivots=0)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], symmetric_pivots=1)
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
     x = P["x"]
     y_gpu = _gpu_matvec(op, x)
