@@ -12,11 +12,11 @@
 //       generic band [8, inf) in PolyTable; 29 narrower bands in the FarBand table
 //   generic (any z > 0): per-lane choice of near band 8 or the generic far band.
 //
-// Evaluators are lane-blocked: one call evaluates TB independent entries in lockstep.  Every
-// coefficient is data: a pair of doubles (two polynomials at the same argument) read with one
-// 128-bit broadcast shared-memory load that feeds 2 x TB FMAs.  Device callers pass the
-// tables' shared-memory copies (load_poly_table / load_far_bands); host callers kPolyHost /
-// kFarBandsHost.  Kernels pick one band per CTA-uniform work segment (setup classifies every
+// Evaluators are lane-blocked: one call evaluates TB independent entries in lockstep, so each
+// coefficient of a fixed-degree polynomial (an immediate: a uniform-register DFMA operand) is
+// shared by TB FMAs.  Data chosen at run time lives in tables that device callers pass as their
+// shared-memory copies (load_poly_table: the log table; load_far_bands: the data bands) and host
+// callers as kPolyHost / kFarBandsHost.  Kernels pick one band per CTA-uniform work segment (setup classifies every
 // interaction by the exact [z_min, z_max] of its point pairs), so the band never diverges
 // inside a warp.
 #pragma once
@@ -32,70 +32,21 @@ using dafmm_fit::FarBand;
 using dafmm_fit::Pair;
 using dafmm_fit::PolyTable;
 
-// Band codes of a work segment: 0 generic, 1 near z <= 8, 2 near z <= 12, 3 + b data band b.
+// Band codes of a work segment: 0 generic, 1 near z <= 8, 2 near z <= 12, 3 near z <= 7,
+// 4 + b data band b.
 constexpr int kBandGeneric = 0;
 constexpr int kBandNear8 = 1;
 constexpr int kBandNear12 = 2;
-constexpr int kBandFarData = 3;
+constexpr int kBandNear7 = 3;
+constexpr int kBandFarData = 4;
 constexpr int kNumBandCodes = kBandFarData + dafmm_fit::NUM_FAR;
 
-// One coefficient pair.  On the device the tables live in shared memory and the load is a
-// volatile 128-bit LDS: otherwise the compiler hoists the loop-invariant coefficients of all
-// polynomials into registers (far more than a thread has) and spills.
-DAFMM_HD Pair ldp(const Pair* p) {
-#ifdef __CUDA_ARCH__
-  Pair r;
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(p);
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.a), "=d"(r.b) : "r"(sa));
-  return r;
-#else
-  return *p;
-#endif
-}
-
-// Two polynomials of N coefficients (pairs c[k] = (a_k, b_k)) at x[i], i < TB.
-template <int N, int TB>
-DAFMM_HD void horner2(const Pair* c, const double* x, double* a, double* b) {
-  Pair t = ldp(c + N - 1);
-#pragma unroll
-  for (int i = 0; i < TB; ++i) {
-    a[i] = t.a;
-    b[i] = t.b;
-  }
-#pragma unroll
-  for (int k = N - 2; k >= 0; --k) {
-    t = ldp(c + k);
-#pragma unroll
-    for (int i = 0; i < TB; ++i) {
-      a[i] = fma(a[i], x[i], t.a);
-      b[i] = fma(b[i], x[i], t.b);
-    }
-  }
-}
-
-// Fixed-degree polynomials: immediates (DAFMM_POLY_IMM, the default) or the shared-memory table.
-#ifndef DAFMM_POLY_IMM
-#define DAFMM_POLY_IMM 1
-#endif
-template <int TB>
-DAFMM_HD void poly_log1p(const PolyTable& T, const double* x, double* a, double* b) {
-  if (DAFMM_POLY_IMM) dafmm_fit::log1p_imm<TB>(x, a, b);
-  else horner2<dafmm_fit::LOG1P_N, TB>(T.log1p, x, a, b);
-}
-template <int TB>
-DAFMM_HD void poly_sincos(const PolyTable& T, const double* x, double* a, double* b) {
-  if (DAFMM_POLY_IMM) dafmm_fit::sincos_imm<TB>(x, a, b);
-  else horner2<dafmm_fit::SC_N, TB>(T.sincos, x, a, b);
-}
+// Fixed-degree polynomials: lane-blocked Horner with immediate coefficients (hankel_coeffs.h).
 template <int ZN, int TB>
-DAFMM_HD void poly_near(const PolyTable& T, const double* x, double* a, double* b) {
-  if (DAFMM_POLY_IMM) {
-    if (ZN == 8) dafmm_fit::near8_imm<TB>(x, a, b);
-    else dafmm_fit::near12_imm<TB>(x, a, b);
-  } else {
-    if (ZN == 8) horner2<dafmm_fit::NEAR8_N, TB>(T.near8, x, a, b);
-    else horner2<dafmm_fit::NEAR12_N, TB>(T.near12, x, a, b);
-  }
+DAFMM_HD void poly_near(const double* x, double* a, double* b) {
+  if constexpr (ZN == 7) dafmm_fit::near7_imm<TB>(x, a, b);
+  else if constexpr (ZN == 8) dafmm_fit::near8_imm<TB>(x, a, b);
+  else dafmm_fit::near12_imm<TB>(x, a, b);
 }
 
 // ln(z2 / 4) for TB positive normal z2.
@@ -115,7 +66,7 @@ DAFMM_HD void log_quarter_vec(const double* z2, double* out, const PolyTable& T)
     lc[i] = tb.b;
     r2[i] = r[i] * r[i];
   }
-  poly_log1p<TB>(T, r2, qe, qo);
+  dafmm_fit::log1p_imm<TB>(r2, qe, qo);
 #pragma unroll
   for (int i = 0; i < TB; ++i)
     out[i] = fma((double)e[i], dafmm_fit::LN2, lc[i] + fma(r2[i], fma(r[i], qo[i], qe[i]), r[i]));
@@ -125,19 +76,16 @@ DAFMM_HD void log_quarter_vec(const double* z2, double* out, const PolyTable& T)
 #endif
 }
 
-// Near-type band: z <= 8 (ZN = 8) or z <= 12 (ZN = 12).  IMM: the (J0, R) coefficients of
-// band 8 as immediates instead of shared-memory loads.
-template <int ZN, int TB, bool IMM = false>
+// Near-type band: z <= ZN for ZN in {7, 8, 12}.
+template <int ZN, int TB>
 DAFMM_HD void h0_near_vec(const double* z2, double* re, double* im, const PolyTable& T) {
-  static_assert(ZN == 8 || ZN == 12, "near bands are z <= 8 and z <= 12");
-  static_assert(!IMM || ZN == 8, "immediates exist for band 8 only");
-  constexpr double ts = ZN == 8 ? dafmm_fit::NEAR8_T_SCALE : dafmm_fit::NEAR12_T_SCALE;
-  constexpr int n = ZN == 8 ? dafmm_fit::NEAR8_N : dafmm_fit::NEAR12_N;
+  static_assert(ZN == 7 || ZN == 8 || ZN == 12, "near bands are z <= 7, 8 and 12");
+  constexpr double ts = ZN == 7 ? dafmm_fit::NEAR7_T_SCALE : ZN == 8 ? dafmm_fit::NEAR8_T_SCALE
+                                                                     : dafmm_fit::NEAR12_T_SCALE;
   double t[TB], j0[TB], rr[TB], lu[TB];
 #pragma unroll
   for (int i = 0; i < TB; ++i) t[i] = fma(z2[i], ts, -1.0);
-  if constexpr (IMM) dafmm_fit::near8_imm<TB>(t, j0, rr);
-  else poly_near<ZN, TB>(T, t, j0, rr);
+  poly_near<ZN, TB>(t, j0, rr);
   log_quarter_vec<TB>(z2, lu, T);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
@@ -193,7 +141,7 @@ DAFMM_HD void h0_far_vec(const double* z2, double* re, double* im, double A, dou
     rh2[i] = rho[i] * rho[i];
     quad[i] = (int)qf;
   }
-  poly_sincos<TB>(T, rh2, sp, c);
+  dafmm_fit::sincos_imm<TB>(rh2, sp, c);
 #pragma unroll
   for (int i = 0; i < TB; ++i) {
     const double s = rho[i] * sp[i];
@@ -215,8 +163,7 @@ template <int TB>
 struct GenericFarPQ {
   const PolyTable& T;
   DAFMM_HD void operator()(const double* x, double* P, double* Q) const {
-    if (DAFMM_POLY_IMM) dafmm_fit::generic_far_imm<TB>(x, P, Q);
-    else horner2<dafmm_fit::GENERIC_FAR_N, TB>(T.generic_far, x, P, Q);
+    dafmm_fit::generic_far_imm<TB>(x, P, Q);
   }
 };
 
@@ -274,13 +221,17 @@ inline cplx h0(double z2) {
 }
 
 // Setup-side band choice for a segment whose point pairs have z in [zmin, zmax]: the
-// cheapest band (estimated fp64 operations per entry) that covers the whole range.
-inline int choose_band(double zmin, double zmax) {
+// cheapest band (estimated fp64 operations per entry) that covers the whole range.  The M2L
+// stream passes allow_near7 = false: one band fewer keeps the persistent kernel free of spills.
+inline int choose_band(double zmin, double zmax, bool allow_near7) {
   int best = kBandGeneric;
   double cost = 1e30;
-  if (zmax <= 8.0) {
+  if (allow_near7 && zmax <= 7.0) {
+    best = kBandNear7;
+    cost = 47.0;
+  } else if (zmax <= 8.0) {
     best = kBandNear8;
-    cost = 51.0;
+    cost = 49.0;
   } else if (zmax <= 12.0) {
     best = kBandNear12;
     cost = 59.0;

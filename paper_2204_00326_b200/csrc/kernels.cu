@@ -46,7 +46,6 @@ constexpr int kCombineThreads = 64;
 #endif
 constexpr int kTBP2P = DAFMM_TB_P2P;
 constexpr int kTBM2L = DAFMM_TB_M2L;
-constexpr int kBandNear8Imm = -1;  // kernel-internal: band near-8 with immediate coefficients (P2P)       // kernel entries evaluated in lockstep per thread (shared coefficients)
 
 __device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
@@ -295,7 +294,7 @@ struct M2LItems {
 struct NearItems {
   static constexpr int kTB = kTBP2P;
   static constexpr bool kGuarded = true;   // item 0 holds the i == j pairs
-  static constexpr bool kNearOnly = true;  // bands: near-8, near-12 or generic
+  static constexpr bool kNearOnly = true;  // bands: near-7, near-8, near-12 or generic
   int band, own, total, is, ie;
   __device__ __forceinline__ int code(int) const { return band; }
   __device__ __forceinline__ bool guard(int i) const { return i == 0; }
@@ -309,7 +308,7 @@ __device__ __forceinline__ void eval_band(const double* z2, double* re, double* 
                                           const FarBand* band) {
   if constexpr (CODE == kBandGeneric) h0_generic_vec<TB>(z2, re, im, T);
   else if constexpr (CODE == kBandNear8) h0_near_vec<8, TB>(z2, re, im, T);
-  else if constexpr (CODE == kBandNear8Imm) h0_near_vec<8, TB, true>(z2, re, im, T);
+  else if constexpr (CODE == kBandNear7) h0_near_vec<7, TB>(z2, re, im, T);
   else if constexpr (CODE == kBandNear12) h0_near_vec<12, TB>(z2, re, im, T);
   else h0_far_vec<TB>(z2, re, im, band->A, band->B, DataFarPQ<TB>{band}, T);
 }
@@ -375,17 +374,18 @@ __device__ __forceinline__ void consume(const double4* sb, int a, int b, double2
     consume_block<CODE, TB, GUARD, true>(sb + a + full * TB, 1, n % TB, xt, ar, ai, T, band);
 }
 
-// Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only near-8, near-12 and
-// generic occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
+// Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only the near bands and generic
+// occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
 template <int TB, bool GUARD, bool NEAR_ONLY>
 __device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
                                              double& ar, double& ai, const PolyTable& T, const FarBand* bands) {
   if constexpr (NEAR_ONLY) {
-    if (code == kBandNear8) consume<kBandNear8Imm, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    if (code == kBandNear7) consume<kBandNear7, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    else if (code == kBandNear8) consume<kBandNear8, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
     else if (code == kBandNear12) consume<kBandNear12, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
     else consume<kBandGeneric, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
   } else {
-    switch (code) {
+    switch (code) {  // the M2L stream: choose_band(.., allow_near7 = false) never yields near-7
       case kBandNear8:
         consume<kBandNear8, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
         break;

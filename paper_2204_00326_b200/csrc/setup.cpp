@@ -844,7 +844,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
           lo = std::min(lo, r2);
           hi = std::max(hi, r2);
         }
-      codes[i][e] = choose_band(P.kappa * std::sqrt(lo), P.kappa * std::sqrt(hi));
+      codes[i][e] = choose_band(P.kappa * std::sqrt(lo), P.kappa * std::sqrt(hi), false);
     }
   }
   // targets in order of decreasing work (the persistent M2L kernel takes them in this order)
@@ -937,7 +937,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       }
       pairs -= (B.end - B.begin);
       pk.p2p_pairs += pairs;
-      int band = zmax <= 8.0 ? kBandNear8 : zmax <= 12.0 ? kBandNear12 : kBandGeneric;
+      int band = zmax <= 7.0 ? kBandNear7 : zmax <= 8.0 ? kBandNear8 : zmax <= 12.0 ? kBandNear12 : kBandGeneric;
       pk.leaf_band.push_back(band);
       pk.p2p_band_entries[band] += pairs;
       pk.near_ptr.push_back((int32_t)pk.near_begin.size());

@@ -14,14 +14,15 @@ All evaluators take z2 = (kappa r)^2 (the kernels store kappa-scaled coordinates
         P, Q polynomials in x = A s + B, s = 1/z mapped from [1/zhi, 1/zlo] onto [-1, 1].
         The generic band [8, inf) sits in PolyTable; 29 narrower bands form the FarBand table.
   sincos on |rho| <= pi/4: sin(rho)/rho and cos(rho) polynomials in rho^2.
-  ln u = e ln2 + ln c_i + log1p(m/c_i - 1), u = 2^e m, with a 2^7-entry table (rcp_i, ln c_i)
-        indexed by the top mantissa bits and a degree-9 log1p.
+  ln u = e ln2 + ln c_i + log1p(m/c_i - 1), u = 2^e m, with a 2^8-entry table (rcp_i, ln c_i)
+        indexed by the top mantissa bits and a degree-6 log1p.
 
-All coefficients are data: pairs of doubles (two polynomials evaluated at the same argument)
-in PolyTable (fixed-degree polynomials and the log table) and in the FarBand table (data
-bands, padded to an odd coefficient count).  The kernels copy them to shared memory; one
-128-bit broadcast load then feeds the 2 x TB FMAs of a lane-blocked Horner step (on sm_100a
-DFMA takes no constant-bank operand and a 64-bit immediate costs two UMOVs).
+Fixed-degree polynomials (near bands, generic far band, sincos, log1p) are emitted as lane-
+blocked Horner evaluators with literal coefficients: each literal becomes a uniform-register
+immediate shared by the TB lanes of a block (on sm_100a DFMA takes no constant-bank operand).
+Data that is selected at run time is emitted as tables the kernels copy to shared memory: the
+log table (PolyTable) and the FarBand table of data bands (coefficient pairs, padded to an odd
+count so the Horner loop runs in pairs).
 """
 import math
 import os
@@ -31,7 +32,7 @@ import mpmath as mp
 import numpy as np
 
 mp.mp.dps = 32
-NEAR_BANDS = [8.0, 12.0]            # near-type bands z <= Zn (code)
+NEAR_BANDS = [7.0, 8.0, 12.0]       # near-type bands z <= Zn
 GENERIC_FAR = (8.0, float("inf"))   # far-type band emitted as code (generic per-lane path)
 TOL_FAR = 3.0e-16                   # max abs error of P, Q (|P| ~ 1)
 TOL_NEAR = 3.2e-15                  # max abs error of J0, R
@@ -178,7 +179,7 @@ def cody_waite():
     return float(c1), float(half_pi - c1)
 
 
-def log_table(bits=7):
+def log_table(bits=8):
     """(rcp_i, ln c_i) with rcp_i = fp64(1 / (1 + (i + 1/2) / 2^bits)) and ln c_i = -ln(rcp_i)
     exactly for the stored rcp_i, so ln(m) = log1p(m rcp_i - 1) + ln c_i is an identity."""
     out = []
@@ -190,8 +191,8 @@ def log_table(bits=7):
 
 def log1p_coeffs():
     """log1p(r) = r + r^2 q(r), q(r) = sum_{k>=0} (-1)^(k+1) r^k / (k+2), split into even and odd
-    parts q = qe(r^2) + r qo(r^2) (degree 9 overall: |r| <= 2^-8 leaves a relative tail < 1e-20)."""
-    q = [mp.mpf((-1) ** (k + 1)) / (k + 2) for k in range(8)]
+    parts q = qe(r^2) + r qo(r^2) (degree 6 overall: |r| <= 2^-9 leaves a tail < 2e-19)."""
+    q = [mp.mpf((-1) ** (k + 1)) / (k + 2) for k in range(5)]
     return q[0::2], q[1::2]
 
 
@@ -236,7 +237,7 @@ def main(out_path):
     w("constexpr double SQRT_2_OVER_PI = %.17e;" % float(mp.sqrt(2 / mp.pi)))
     w("constexpr double LN2 = %.17e;" % float(mp.log(2)))
     w("constexpr double PIO2_1 = %.17e;\nconstexpr double PIO2_2 = %.17e;" % (c1, c2))
-    w("constexpr int LOG_BITS = 7;")
+    w("constexpr int LOG_BITS = 8;")
     w("struct alignas(16) Pair {\n  double a, b;\n};")
     # fixed-degree polynomials: pairs in one table (copied to shared memory by the kernels)
     def pairlist(ca, cb):
@@ -244,13 +245,14 @@ def main(out_path):
         ca = [float(v) for v in ca] + [0.0] * (n - len(ca))
         cb = [float(v) for v in cb] + [0.0] * (n - len(cb))
         return n, "{" + ", ".join("{%.17e, %.17e}" % (x, y) for x, y in zip(ca, cb)) + "}"
-    n8, near8 = pairlist(nears[0][0], nears[0][1])
-    n12, near12 = pairlist(nears[1][0], nears[1][1])
+    n7, near7 = pairlist(nears[0][0], nears[0][1])
+    n8, near8 = pairlist(nears[1][0], nears[1][1])
+    n12, near12 = pairlist(nears[2][0], nears[2][1])
     ngf, gf = pairlist(gfar[0], gfar[1])
     nsc, sc = pairlist(cs, cc)
     nlp, lp = pairlist(qe, qo)
     w("// near-type bands: (J0, R) polynomials in t = z2 * T_SCALE - 1")
-    for zn, n in zip(NEAR_BANDS, (n8, n12)):
+    for zn, n in zip(NEAR_BANDS, (n7, n8, n12)):
         U = zn * zn / 4
         w("constexpr double NEAR%d_Z2_MAX = %.17g;  // z^2 <= Z2_MAX" % (int(zn), zn * zn))
         w("constexpr double NEAR%d_T_SCALE = %.17g;  // t = z2 * T_SCALE - 1 = 2 (z2/4) / U - 1" % (int(zn), 0.5 / U))
@@ -268,27 +270,21 @@ def main(out_path):
     w("    a[i] = fma(a[i], x[i], ca);               \\")
     w("    b[i] = fma(b[i], x[i], cb);               \\")
     w("  }")
-    w("// The same fixed-degree polynomials with their coefficients as immediates (uniform-register")
-    w("// operands of DFMA, shared by the TB lanes of a block); measured faster than shared-memory")
-    w("// coefficients for both the P2P and the M2L kernel (DESIGN.md §6).")
-    w(h2_function("near8_imm", nears[0][0], nears[0][1], "(J0, R), z <= 8"))
-    w(h2_function("near12_imm", nears[1][0], nears[1][1], "(J0, R), z <= 12"))
+    w("// Fixed-degree polynomials with their coefficients as immediates (uniform-register operands")
+    w("// of DFMA, shared by the TB lanes of a block); measured faster than shared-memory coefficient")
+    w("// tables for both the P2P and the M2L kernel (DESIGN.md §6, profiles/ab_r20_*).")
+    w(h2_function("near7_imm", nears[0][0], nears[0][1], "(J0, R), z <= 7"))
+    w(h2_function("near8_imm", nears[1][0], nears[1][1], "(J0, R), z <= 8"))
+    w(h2_function("near12_imm", nears[2][0], nears[2][1], "(J0, R), z <= 12"))
     w(h2_function("generic_far_imm", gfar[0], gfar[1], "(P, Q) of the generic far band [8, inf)"))
     w(h2_function("sincos_imm", cs, cc, "(sin(rho)/rho, cos(rho)) in rho^2"))
     w(h2_function("log1p_imm", qe, qo, "(qe, qo) in r^2"))
-    w("// Coefficient pairs of every fixed-degree polynomial and the log table.  The kernels copy it")
-    w("// to shared memory once per CTA; one 128-bit broadcast load then feeds the 2 x TB FMAs of a")
-    w("// lane-blocked Horner step (64-bit immediates would cost two UMOVs each on sm_100a).")
+    w("// The log table (per-lane indexed: data, copied to shared memory by the kernels).")
     w("struct PolyTable {")
-    w("  Pair near8[NEAR8_N];            // (J0_k, R_k), z <= 8")
-    w("  Pair near12[NEAR12_N];          // (J0_k, R_k), z <= 12")
-    w("  Pair generic_far[GENERIC_FAR_N];  // (P_k, Q_k), z >= 8")
-    w("  Pair sincos[SC_N];              // (sin(rho)/rho, cos(rho)) in rho^2")
-    w("  Pair log1p[LOG1P_N];            // (qe_k, qo_k): log1p(r) = r + r^2 (qe(r^2) + r qo(r^2))")
     w("  Pair log_tab[1 << LOG_BITS];    // (rcp_i, ln c_i), i = top LOG_BITS mantissa bits")
     w("};")
     lt_init = "{" + ", ".join("{%.17e, %.17e}" % t for t in lt) + "}"
-    init = "{\n%s,\n%s,\n%s,\n%s,\n%s,\n%s}" % (near8, near12, gf, sc, lp, lt_init)
+    init = "{\n%s}" % lt_init
     w("#if defined(__CUDACC__)")
     w("static __constant__ PolyTable kPolyDev = %s;" % init)
     w("#endif")
