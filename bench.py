@@ -95,25 +95,78 @@ def whole_job_value(n_unknowns, world, ms_per_step_max):
     return n_unknowns * world / (ms_per_step_max * 1e-3)
 
 
-def roofline_entry(pass_ms, matvecs, stats, inputs):
-    """Roofline object of the fp64-ALU-bound part of the step.
+def _fp64_peak(inputs):
+    peak = inputs.get("fp64_tflops_measured")
+    if peak:
+        return peak, "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/)"
+    return FP64_NOMINAL_TFLOPS, "nominal 148 SM x 64 DFMA/clk x 1.965 GHz"
 
-    P2P (side stream) and M2L (with the translations, handle stream) run concurrently, so the
-    dominant unit is their overlap: achieved = (P2P point pairs x fp64 flops per pair + M2L
-    pivot pairs x fp64 flops per pair) / the span from the fork to the later of the two
-    (CUDA events, dafmm_pass_times).  Flops per entry are the counted fp64 work of the shipped
-    evaluator (ncu dfma/dadd/dmul, profiles/roofline_inputs.json); traffic = the two kernels'
-    DRAM bytes per launch from the same ncu capture."""
+
+def _hbm_peak():
+    mp = load_json(MEASURED_PEAKS)
+    if mp.get("hbm_gbs"):
+        return float(mp["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy bandwidth, burst)"
+    return 7700.0, "B200_PROFILING.md nominal HBM3e 7.7 TB/s (MEASURED_PEAKS.json absent)"
+
+
+def m2l_stored_bytes(stats):
+    """Algorithmic DRAM bytes of one stored-M2L launch: every block entry once
+    (16 B), every source-stream index (4 B) and gathered multipole (16 B), every output (16 B)."""
+    return 16 * stats["m2l_entries"] + 20 * stats["m2l_stream_len"] + 16 * stats["n_loc"]
+
+
+def roofline_entry(pass_ms, matvecs, stats, inputs, ms_per_step=None):
+    """Roofline object of the dominant kernel.
+
+    M2L blocks stored (the default when they fit): the dominant kernel is m2l_stored_kernel, HBM
+    bound: achieved = its algorithmic bytes per launch / its launch duration, measured live with
+    CUDA events on its stream (dafmm_pass_times) while P2P runs beside it.  The concurrent P2P
+    (fp64-ALU bound) and the whole step's bound, max(fp64 work / fp64 peak, DRAM bytes / HBM
+    peak), are reported beside it.
+    M2L on the fly: P2P and M2L are both fp64-ALU bound and the unit is their overlap: achieved
+    = (P2P pairs x fp64 flops per pair + M2L pairs x fp64 flops per pair) / the span from the fork
+    to the later of the two.  Flops per entry are the counted fp64 work of the shipped kernels
+    (ncu dfma/dadd/dmul, profiles/roofline_inputs.json); traffic = DRAM bytes per launch from
+    the same ncu capture."""
     mv = max(matvecs, 1)
     kin = inputs.get("kernels", {})
-    e = {"p2p": stats["p2p_pairs"], "m2l": stats["m2l_entries"]}
-    ms = {"p2p": pass_ms.get("near", 0.0) / mv, "m2l": pass_ms.get("m2l", 0.0) / mv}
+    fpk, fpk_src = _fp64_peak(inputs)
     span = pass_ms.get("overlap_span", 0.0) / mv
+    ms_p2p = pass_ms.get("near", 0.0) / mv
+    ms_m2l = pass_ms.get("m2l", 0.0) / mv
+    fpe_p2p = kin.get("p2p", {}).get("fp64_flops_per_entry")
+    p2p = {"kernel": "p2p_kernel", "bound": "alu", "launch_ms_concurrent": ms_p2p, "entries_per_launch": stats["p2p_pairs"],
+           "fp64_flops_per_entry": fpe_p2p, "ncu_fp64_pipe_pct": kin.get("p2p", {}).get("fp64_pipe_pct"),
+           "ncu_time_ms_isolated": kin.get("p2p", {}).get("ncu_time_ms")}
+    if fpe_p2p and ms_p2p > 0:
+        p2p["achieved"] = stats["p2p_pairs"] * fpe_p2p / (ms_p2p * 1e-3) / 1e12
+        p2p["frac"] = p2p["achieved"] / fpk
+    if stats.get("m2l_stored"):
+        hpk, hpk_src = _hbm_peak()
+        nbytes = m2l_stored_bytes(stats)
+        achieved = nbytes / (ms_m2l * 1e-3) / 1e9 if ms_m2l > 0 else None
+        ki = kin.get("m2l_stored", {})
+        # the step's bound: fp64 work (P2P + the stored M2L's complex MACs, 8 flops per entry)
+        # against fp64 peak, DRAM bytes (stored blocks, translation operators, ~10 vector passes)
+        # against HBM peak; the two resources overlap
+        flops = stats["p2p_pairs"] * (fpe_p2p or 0.0) + 8.0 * stats["m2l_entries"]
+        dram = nbytes + stats["operator_bytes"] + 10 * 16 * stats["n"]
+        t_alu, t_hbm = flops / (fpk * 1e12) * 1e3, dram / (hpk * 1e9) * 1e3
+        step = {"bound_ms": max(t_alu, t_hbm), "alu_ms": t_alu, "hbm_ms": t_hbm, "dram_bytes": dram,
+                "fp64_flops": flops}
+        if ms_per_step:
+            step["ms"] = ms_per_step
+            step["frac"] = step["bound_ms"] / ms_per_step
+        return {"kernel": "m2l_stored_kernel (M2L blocks streamed from HBM by TMA; concurrent with p2p_kernel)",
+                "bound": "hbm", "achieved": achieved, "peak": hpk, "unit": "GB/s",
+                "frac": (achieved / hpk) if achieved else None, "traffic": ki.get("dram_bytes_per_launch"),
+                "algorithmic_bytes_per_launch": nbytes, "launch_ms_concurrent": ms_m2l,
+                "ncu_time_ms_isolated": ki.get("ncu_time_ms"), "peak_source": hpk_src,
+                "concurrent": {"p2p": p2p, "span_ms": span}, "step": step, "fp64_peak": fpk,
+                "fp64_peak_source": fpk_src, "ncu_source": inputs.get("source")}
+    e = {"p2p": stats["p2p_pairs"], "m2l": stats["m2l_entries"]}
+    ms = {"p2p": ms_p2p, "m2l": ms_m2l}
     fpe = {k: kin.get(k, {}).get("fp64_flops_per_entry") for k in e}
-    peak = inputs.get("fp64_tflops_measured")
-    peak_src = "measured DFMA microbenchmark (tools/fp64_peak.cu, profiles/)"
-    if not peak:
-        peak, peak_src = FP64_NOMINAL_TFLOPS, "nominal 148 SM x 64 DFMA/clk x 1.965 GHz"
     achieved = None
     if all(fpe.values()) and span > 0:
         achieved = sum(e[k] * fpe[k] for k in e) / (span * 1e-3) / 1e12
@@ -125,9 +178,9 @@ def roofline_entry(pass_ms, matvecs, stats, inputs):
                    "ncu_fp64_pipe_pct": kin.get(k, {}).get("fp64_pipe_pct"),
                    "ncu_time_ms_isolated": kin.get(k, {}).get("ncu_time_ms")} for k in e}
     return {"kernel": "p2p_kernel || m2l_kernel (concurrent streams, fork to join)", "bound": "alu",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": (achieved / peak) if achieved else None,
+            "achieved": achieved, "peak": fpk, "unit": "TFLOP/s", "frac": (achieved / fpk) if achieved else None,
             "traffic": traffic, "span_ms": span, "entries_per_s": sum(e.values()) / (span * 1e-3) if span else None,
-            "kernels": kernels, "peak_source": peak_src, "ncu_source": inputs.get("source")}
+            "kernels": kernels, "peak_source": fpk_src, "ncu_source": inputs.get("source")}
 
 
 def summarize_clocks(rows):
@@ -368,7 +421,7 @@ def run_ours(args):
     line = None
     if rank == 0:
         inputs = load_json(PROFILE_SUMMARY)
-        roof = roofline_entry(pass_ms, matvecs, stats, inputs)
+        roof = roofline_entry(pass_ms, matvecs, stats, inputs, ms_max)
         line = {"metric": "DAFMM matvec unknowns/s", "value": value, "unit": "unknowns/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
                 "ms_per_step_min": min(times), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -385,7 +438,8 @@ def run_ours(args):
                                                            "setup_ops_s", "setup_upload_s")},
                 "plan": {k: stats[k] for k in ("levels", "n_nodes", "p2p_pairs", "m2l_entries", "m2l_pairs",
                                                "operator_bytes", "device_bytes", "mean_rank_leaf_in",
-                                               "mean_rank_leaf_out", "max_rank")}}
+                                               "mean_rank_leaf_out", "max_rank", "m2l_stored", "m2l_store_bytes",
+                                               "m2l_stream_len", "n_loc")}}
         if world == 1 and not args.no_cpu_baseline:
             rate, rows, secs, y_rows = oracle_rows_sample(P, 15.0)
             op.matvec(x, y)

@@ -68,6 +68,13 @@ typedef struct {
                            write them.  1: one ACA per node; the outgoing skeleton is the incoming
                            one with rows and columns swapped (reading R19, G symmetric): half the
                            ACA setup time, 3% more M2L work at C4. */
+  int m2l_store;       /* M2L blocks A_{t s}: 0 evaluate the kernel entries on the fly in
+                          every matvec (fp64-ALU bound); 1 evaluate them once at create time on the
+                          device and keep them in HBM (16 B per entry; every matvec then streams
+                          them: HBM bound), DAFMM_ENOMEM if they do not fit, DAFMM_EINVAL if a
+                          node has more than 128 pivots; -1 (default) auto: store when the blocks
+                          take at most half of the free device memory and every node has at most
+                          128 pivots, else on the fly.  dafmm_stats reports the choice. */
 } dafmm_options;
 
 /* Statistics of a plan (sizes, ranks, setup times). */
@@ -84,8 +91,13 @@ typedef struct {
   int32_t max_rank;
   double setup_tree_s, setup_lists_s, setup_nca_s, setup_ops_s, setup_pack_s, setup_upload_s;
   int64_t aca_entries;       /* kernel entries evaluated by ACA during setup */
-  int64_t m2l_band_entries[48]; /* M2L entries per H0 band code (hankel.cuh: 0 generic, 1 near z<=8, 2 near z<=12, 3+b data band b) */
+  int64_t m2l_band_entries[48]; /* M2L entries per H0 band code (0 generic, 1 near z<=8, 2 near z<=12,
+                                    3 near z<=7, 4+b data band b; dafmm_h0_bands) */
   int64_t p2p_band_entries[48]; /* P2P point pairs per band code */
+  int32_t m2l_stored;           /* 1: M2L blocks stored in HBM (dafmm_options.m2l_store) */
+  int64_t m2l_store_bytes;      /* their bytes (0 when evaluated on the fly) */
+  int64_t m2l_stream_len;       /* source pivots over all M2L target nodes (multipole gathers per matvec) */
+  int64_t n_loc;                /* local-expansion coefficients (M2L outputs) */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);
@@ -153,6 +165,23 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out);
 #define DAFMM_NUM_PASSES 8
 int dafmm_set_profiling(dafmm_handle h, int enable);
 int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64_t* launches_out);
+
+/* The product's H0^(1) evaluator, exposed band by band for the parity tests (DESIGN.md section 6,
+ * "H0 evaluator"; the kernel G = (i/4) H0^(1)(kappa |x - y|) is P:70-72, and the paper leaves
+ * the evaluation method open).
+ * dafmm_h0_bands writes, for every band code c < min(cap, return value), the z = kappa r
+ * interval the band is valid on: zlo[c] < z <= zhi[c] for the near bands (1: z <= 8,
+ * 2: z <= 12, 3: z <= 7; zlo = 0), zlo[c] <= z <= zhi[c] for the data bands c >= 4, and
+ * (0, inf) for code 0 (generic: near-8 or the asymptotic form, chosen per element).  Either
+ * pointer may be NULL.  Returns the number of band codes.  Host only, no GPU needed.
+ * dafmm_h0_eval: h0[i] = H0^(1)(sqrt(z2[i])) = J0 + i Y0 (complex128 interleaved), z2 =
+ * (kappa r)^2 > 0, by band `band`'s evaluator, in the same lane-blocked code as the P2P and M2L
+ * kernels.  z2, h0: DEVICE pointers (n doubles / n complex128, caller-owned); enqueued on
+ * `stream` (a cudaStream_t; NULL = the legacy default stream), asynchronous.  Arguments
+ * outside the band's interval give unspecified (finite) values.  Errors: DAFMM_EINVAL
+ * (n < 0, null pointer with n > 0, band code out of range), DAFMM_ECUDA (launch). */
+int dafmm_h0_bands(double* zlo, double* zhi, int cap);
+int dafmm_h0_eval(const void* z2, void* h0, int64_t n, int band, void* stream);
 
 /* Write the tree, lists, cones and pivot index sets as .npy files into directory `path`
  * (created if missing) for the independent CPU oracle.  Synchronous, host only. */

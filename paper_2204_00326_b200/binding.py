@@ -14,7 +14,8 @@ _lib = None
 
 EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_matvec", "dafmm_matvec_parts",
             "dafmm_matvec_host", "ls_gmres_solve", "dafmm_set_stream", "dafmm_stats", "dafmm_export_plan",
-            "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times"]
+            "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times", "dafmm_h0_bands",
+            "dafmm_h0_eval"]
 
 NUM_PASSES = 8
 PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near", "combine", "overlap_span"]
@@ -32,7 +33,7 @@ class DAFMMError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("T", ctypes.c_double), ("self_term", ctypes.c_int), ("kernel_mode", ctypes.c_int),
                 ("max_level", ctypes.c_int), ("num_threads", ctypes.c_int), ("host_only", ctypes.c_int),
-                ("symmetric_pivots", ctypes.c_int)]
+                ("symmetric_pivots", ctypes.c_int), ("m2l_store", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -45,7 +46,8 @@ class Stats(ctypes.Structure):
                 ("setup_nca_s", ctypes.c_double), ("setup_ops_s", ctypes.c_double),
                 ("setup_pack_s", ctypes.c_double), ("setup_upload_s", ctypes.c_double),
                 ("aca_entries", ctypes.c_int64), ("m2l_band_entries", ctypes.c_int64 * 48),
-                ("p2p_band_entries", ctypes.c_int64 * 48)]
+                ("p2p_band_entries", ctypes.c_int64 * 48), ("m2l_stored", ctypes.c_int32),
+                ("m2l_store_bytes", ctypes.c_int64), ("m2l_stream_len", ctypes.c_int64), ("n_loc", ctypes.c_int64)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -79,6 +81,8 @@ def load():
     lib.dafmm_export_plan.argtypes = [vp, ctypes.c_char_p]
     lib.dafmm_set_profiling.argtypes = [vp, i32]
     lib.dafmm_pass_times.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    lib.dafmm_h0_bands.argtypes = [vp, vp, i32]
+    lib.dafmm_h0_eval.argtypes = [vp, vp, i64, i32, vp]
     lib.dafmm_destroy.argtypes = [vp]
     lib.dafmm_destroy.restype = None
     lib.dafmm_last_error.restype = ctypes.c_char_p
@@ -191,6 +195,26 @@ def dafmm_pass_times(h):
 
 def dafmm_export_plan(h, path):
     return _check(load().dafmm_export_plan(h, str(path).encode()))
+
+
+def dafmm_h0_bands():
+    """[(zlo, zhi)] per band code: the z = kappa r interval each evaluator band is valid on."""
+    lib = load()
+    nb = _check(lib.dafmm_h0_bands(None, None, 0))
+    lo, hi = (ctypes.c_double * nb)(), (ctypes.c_double * nb)()
+    lib.dafmm_h0_bands(ctypes.cast(lo, ctypes.c_void_p), ctypes.cast(hi, ctypes.c_void_p), nb)
+    return list(zip(list(lo), list(hi)))
+
+
+def dafmm_h0_eval(z2, out, band, stream=None):
+    """out = H0^(1)(sqrt(z2)) by band `band`: z2 a CUDA float64 tensor, out CUDA complex128 (same n)."""
+    if not (z2.is_cuda and z2.is_contiguous() and str(z2.dtype) == "torch.float64"):
+        raise ValueError("z2 must be a contiguous CUDA float64 tensor")
+    if out.numel() != z2.numel():
+        raise ValueError("out must have z2's length")
+    ptr = 0 if stream is None else (stream if isinstance(stream, int) else stream.cuda_stream)
+    return _check(load().dafmm_h0_eval(ctypes.c_void_p(z2.data_ptr()), _dev(out), z2.numel(), int(band),
+                                       ctypes.c_void_p(ptr)))
 
 
 def dafmm_destroy(h):

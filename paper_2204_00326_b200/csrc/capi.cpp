@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -9,13 +10,14 @@
 
 #include "dafmm.h"
 #include "device.h"
+#include "hankel.cuh"
 #include "plan.h"
 
 struct dafmm_plan {
   dafmm::Plan plan;
   dafmm::DevPlan dev;
   int64_t operator_bytes = 0;
-  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;
+  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0, m2l_stream_len = 0, n_loc = 0;
   std::vector<int64_t> m2l_band, p2p_band;
 };
 
@@ -44,6 +46,7 @@ void dafmm_default_options(dafmm_options* opt) {
   opt->num_threads = o.num_threads;
   opt->host_only = o.host_only;
   opt->symmetric_pivots = o.symmetric_pivots;
+  opt->m2l_store = o.m2l_store;
 }
 
 int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
@@ -59,6 +62,8 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.num_threads = opt->num_threads;
     o.host_only = opt->host_only;
     o.symmetric_pivots = opt->symmetric_pivots;
+    o.m2l_store = opt->m2l_store;
+    if (o.m2l_store < -1 || o.m2l_store > 1) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0 or 1");
   }
   std::unique_ptr<dafmm_plan> h;
   try {
@@ -89,6 +94,8 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     h->p2p_pairs = pk.p2p_pairs;
     h->m2l_entries = pk.m2l_entries;
     h->m2l_pairs = pk.m2l_pairs;
+    h->m2l_stream_len = (int64_t)pk.m2l_stream_idx.size();
+    h->n_loc = pk.n_loc;
     h->m2l_band = pk.m2l_band_entries;
     h->p2p_band = pk.p2p_band_entries;
   } catch (const std::bad_alloc&) {
@@ -210,6 +217,10 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->setup_pack_s = P.t_pack;
   out->setup_upload_s = P.t_upload;
   out->aca_entries = P.aca_entries;
+  out->m2l_stored = h->dev.m2l_mat != nullptr ? 1 : 0;
+  out->m2l_store_bytes = h->dev.m2l_mat != nullptr ? h->m2l_entries * 16 : 0;
+  out->m2l_stream_len = h->m2l_stream_len;
+  out->n_loc = h->n_loc;
   for (size_t b = 0; b < h->m2l_band.size() && b < 48; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
   for (size_t b = 0; b < h->p2p_band.size() && b < 48; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
   return DAFMM_OK;
@@ -233,5 +244,31 @@ void dafmm_destroy(dafmm_handle h) {
 }
 
 const char* dafmm_last_error(void) { return g_last_error.c_str(); }
+
+int dafmm_h0_bands(double* zlo, double* zhi, int cap) {
+  const int nb = dafmm::kNumBandCodes;
+  for (int c = 0; c < nb && c < cap; ++c) {
+    double lo = 0.0, hi = INFINITY;
+    if (c == dafmm::kBandNear7) hi = std::sqrt(dafmm_fit::NEAR7_Z2_MAX);
+    else if (c == dafmm::kBandNear8) hi = std::sqrt(dafmm_fit::NEAR8_Z2_MAX);
+    else if (c == dafmm::kBandNear12) hi = std::sqrt(dafmm_fit::NEAR12_Z2_MAX);
+    else if (c >= dafmm::kBandFarData) {
+      lo = dafmm_fit::kFarBandsHost[c - dafmm::kBandFarData].zlo;
+      hi = dafmm_fit::kFarBandsHost[c - dafmm::kBandFarData].zhi;
+    }
+    if (zlo) zlo[c] = lo;
+    if (zhi) zhi[c] = hi;
+  }
+  return nb;
+}
+
+int dafmm_h0_eval(const void* z2, void* h0, int64_t n, int band, void* stream) {
+  if (n < 0) return fail(DAFMM_EINVAL, "n must be >= 0");
+  if (n > 0 && (!z2 || !h0)) return fail(DAFMM_EINVAL, "null argument");
+  if (band < 0 || band >= dafmm::kNumBandCodes) return fail(DAFMM_EINVAL, "band code out of range");
+  std::string err;
+  int rc = dafmm::h0_eval((const double*)z2, (double2*)h0, n, band, (cudaStream_t)stream, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
 
 }  // extern "C"

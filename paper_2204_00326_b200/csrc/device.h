@@ -63,6 +63,11 @@ struct DevPlan {
   int32_t* m2l_item_code = nullptr;
   int32_t* m2l_item_begin = nullptr;
   int32_t* m2l_item_end = nullptr;
+  // stored M2L blocks (dafmm_options.m2l_store): per target node, column-major r x L block
+  // (entry (t, s) at m2l_mat_off[target] + s * r + t), H0 units
+  int64_t* m2l_mat_off = nullptr;
+  double2* m2l_mat = nullptr;
+  int m2l_store_grid = 0;
   // leaves
   int nleaves = 0, max_leaf = 0;
   int32_t* leaf_begin = nullptr;
@@ -112,5 +117,7 @@ void free_plan(DevPlan& d);
 int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::string& err);
 int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit, int restart, int* iters,
               double* relres, double* history, std::string& err);
+// out[i] = H0^(1)(sqrt(z2[i])) by band `code` (device pointers, enqueued on s)
+int h0_eval(const double* z2, double2* out, int64_t n, int code, cudaStream_t s, std::string& err);
 
 }  // namespace dafmm

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <string>
 #include <cstdio>
 #include <vector>
 
@@ -332,8 +333,7 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
       ar = fma(hr, sv.z, fma(-hi, sv.w, ar));
       ai = fma(hr, sv.w, fma(hi, sv.z, ai));
     }
-    return;
-  }
+  } else {
   double z2[TB], hr[TB], hi[TB];
   bool use[TB];
 #pragma unroll
@@ -357,6 +357,7 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
     }
     ar = fma(hr[q], v.x, fma(-hi[q], v.y, ar));
     ai = fma(hr[q], v.y, fma(hi[q], v.x, ai));
+  }
   }
 }
 
@@ -500,6 +501,307 @@ __global__ void __launch_bounds__(kM2LThreads, DAFMM_M2L_MINB) m2l_kernel(
       __syncthreads();
     }
   }
+}
+
+// ---- stored M2L blocks (dafmm_options.m2l_store) ------------------------------------------
+// The M2L operator of a target node is the block A_{t s} of kernel entries between its
+// incoming pivots t and the outgoing pivots s of every node in its interaction lists (
+// the kappa^2 q and w scalings are folded into the stored operators and multipoles, so the block
+// is pure H0).  It depends only on the plan, so it can be evaluated once and kept in HBM: the
+// matvec then streams 16 B per entry instead of evaluating ~100 fp64 flops per entry, and the
+// M2L turns from fp64-ALU bound into HBM bound -- the other resource than the concurrent P2P's.
+//
+// Layout: per target node (r rows, L source columns in its source-stream order), column-major:
+// entry (t, s) at m2l_mat_off[target] + s * r + t.  A CTA whose threads are mapped as
+// (row t, slice sl) with nsl = floor(NT / r) slices, thread j = sl * r + t, touches entries
+// e = j + k * nsl * r: one contiguous run per step, and every thread keeps one row.
+//
+constexpr int kMSConsumers = 128;  // consumer threads (4 warps); a node may have at most this many rows
+constexpr int kMSThreads = kMSConsumers + 32;  // + one producer warp (one elected lane issues TMA)
+#ifndef DAFMM_MS_STAGES
+#define DAFMM_MS_STAGES 4
+#endif
+#ifndef DAFMM_MS_COLS
+#define DAFMM_MS_COLS 512
+#endif
+#ifndef DAFMM_NEAR_HIGH
+#define DAFMM_NEAR_HIGH 0  // 1: the near-field stream gets the high priority instead of the far field
+#endif
+#ifndef DAFMM_MS_PER_SM
+#define DAFMM_MS_PER_SM 2  // persistent stored-M2L CTAs per SM (they share the SMs with P2P CTAs)
+#endif
+#ifndef DAFMM_MS_MINB
+#define DAFMM_MS_MINB 6  // register cap (<= 64): room for P2P CTAs beside the stored-M2L CTAs
+#endif
+constexpr int kMSStageE = 1024;                 // entries per TMA bulk copy (16 KB)
+constexpr int kMSStages = DAFMM_MS_STAGES;      // ring depth (x 16 KB in flight per CTA)
+constexpr int kMSCols = DAFMM_MS_COLS;          // source columns per work unit (multipoles double-buffered)
+constexpr int kMaxStoredRows = kMSConsumers;
+constexpr int kMSFormThreads = 128;
+constexpr size_t kMSDynSmem = sizeof(double2) * kMSStages * kMSStageE;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+// wait until the phase with parity `parity` of barrier b has completed.  The suspend-time hint
+// lets the waiting warp sleep until the phase completes (woken by the barrier) instead of
+// re-polling: spinning waiters would take issue slots from the P2P warps sharing the SM.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity), "r"(0x989680u)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMSConsumers) : "memory"); }
+// TMA 1-D bulk copy global -> shared, completion counted in bytes on barrier b
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
+}
+
+// Evaluate the blocks once (at create time): one CTA per target node.
+__global__ void __launch_bounds__(kMSFormThreads) m2l_form_kernel(const int64_t* __restrict__ loc_off,
+                                                                const int32_t* __restrict__ rows,
+                                                                const int64_t* __restrict__ stream_ptr,
+                                                                const int32_t* __restrict__ stream_idx,
+                                                                const int64_t* __restrict__ mat_off,
+                                                                const double2* __restrict__ ti_xy,
+                                                                const double2* __restrict__ so_xy,
+                                                                double2* __restrict__ mat) {
+  __shared__ PolyTable T;
+  load_poly_table(T);
+  const int tgt = blockIdx.x;
+  const int r = rows[tgt];
+  if (r <= 0) return;
+  const int nsl = kMSFormThreads / r, t = threadIdx.x % r, sl = threadIdx.x / r;
+  if (sl >= nsl) return;
+  const double2 xt = ld2(ti_xy + loc_off[tgt] + t);
+  const int64_t sp = stream_ptr[tgt];
+  const int L = (int)(stream_ptr[tgt + 1] - sp);
+  double2* M = mat + mat_off[tgt];
+  for (int c = sl; c < L; c += nsl) {
+    const double2 sv = ld2(so_xy + stream_idx[sp + c]);
+    const double dx = xt.x - sv.x, dy = xt.y - sv.y;
+    const double d2 = fma(dx, dx, dy * dy);
+    double hr, hi;
+    h0_generic_vec<1>(&d2, &hr, &hi, T);
+    M[(int64_t)c * r + t] = make_double2(hr, hi);
+  }
+}
+
+// Apply the stored blocks: u[t] = sum_s A_{t s} m_s.  Persistent CTAs take target nodes from a
+// ticket counter (nodes packed by decreasing work).  Warp-specialised: one lane of the producer
+// warp cuts each node into work units of at most kMSCols source columns, publishes the unit
+// descriptors one unit ahead (a kMSUnits-slot ring), and streams each unit's entries through a
+// kMSStages-deep ring of shared-memory stages with TMA bulk copies (mbarrier full/empty
+// handshakes).  The 4 consumer warps accumulate their row over the staged entries; while they
+// consume unit i they gather unit i+1's multipoles into the other half of a double buffer with
+// cp.async (indices loaded one stage earlier), so the gather latency hides behind the stream.
+// At a node's last unit the slices of each row are reduced and u is written.
+struct MSUnit {
+  int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
+};
+constexpr int kMSUnits = 4;
+constexpr int kMSIdx = kMSCols / kMSConsumers;  // multipole indices per consumer thread per unit
+__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
+    int ntargets, int* __restrict__ ticket, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
+    double2* __restrict__ loc) {
+  extern __shared__ __align__(128) double2 ms_dyn[];  // the TMA ring: kMSStages x kMSStageE entries
+  double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
+  __shared__ __align__(16) double2 mb[2][kMSCols];
+  __shared__ double2 red[kMSConsumers];
+  __shared__ __align__(8) uint64_t full[kMSStages], empty[kMSStages], ufull[kMSUnits], uempty[kMSUnits];
+  __shared__ MSUnit units[kMSUnits];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMSStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kMSConsumers / 32);
+    }
+    for (int i = 0; i < kMSUnits; ++i) {
+      mbar_init(&ufull[i], 1);
+      mbar_init(&uempty[i], kMSConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kMSConsumers / 32) {  // ---- producer
+    if (lane != 0) return;
+    int stage = 0, uslot = 0;
+    uint32_t sphase = 0, uphase = 0;
+    // the unit sequence: (tgt, c0, c1); next_unit() advances it, fetching tickets as needed
+    int tgt = -2, L = 0, c0 = 0;
+    auto next_unit = [&](MSUnit& u) {
+      if (tgt == -1) {
+        u = MSUnit{-1, 0, 0, 0};
+        return;
+      }
+      if (tgt == -2 || c0 >= L) {  // next node
+        tgt = atomicAdd(ticket, 1);
+        if (tgt >= ntargets) {
+          tgt = -1;
+          u = MSUnit{-1, 0, 0, 0};
+          return;
+        }
+        L = (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]);
+        c0 = 0;
+      }
+      const int c1 = min(L, c0 + kMSCols);
+      u = MSUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0)};
+      c0 = c1;
+    };
+    auto publish = [&](const MSUnit& u) {
+      mbar_wait(&uempty[uslot], uphase ^ 1);
+      units[uslot] = u;
+      mbar_arrive(&ufull[uslot]);
+      if (++uslot == kMSUnits) {
+        uslot = 0;
+        uphase ^= 1;
+      }
+    };
+    MSUnit cur, nxt;
+    next_unit(cur);
+    publish(cur);
+    while (cur.tgt >= 0) {
+      next_unit(nxt);
+      publish(nxt);  // one unit ahead: the consumers prefetch its multipoles
+      const int r = rows[cur.tgt];
+      const double2* src = mat + mat_off[cur.tgt] + (int64_t)cur.c0 * r;
+      const int ne = (cur.c1 - cur.c0) * r;
+      for (int e0 = 0; e0 < ne; e0 += kMSStageE) {
+        const int cnt = min(kMSStageE, ne - e0);
+        mbar_wait(&empty[stage], sphase ^ 1);
+        mbar_arrive_tx(&full[stage], (uint32_t)cnt * 16u);
+        bulk_load(ring[stage], src + e0, (uint32_t)cnt * 16u, &full[stage]);
+        if (++stage == kMSStages) {
+          stage = 0;
+          sphase ^= 1;
+        }
+      }
+      cur = nxt;
+    }
+    return;
+  }
+  // ---- consumers (threads 0 .. kMSConsumers-1)
+  const int j = threadIdx.x;
+  int stage = 0, uslot = 0;
+  uint32_t sphase = 0, uphase = 0;
+  auto take = [&]() {
+    mbar_wait(&ufull[uslot], uphase);
+    const MSUnit u = units[uslot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&uempty[uslot]);
+    if (++uslot == kMSUnits) {
+      uslot = 0;
+      uphase ^= 1;
+    }
+    return u;
+  };
+  auto gather_idx = [&](const MSUnit& u, int* kidx) {
+    const int64_t sp = u.tgt >= 0 ? stream_ptr[u.tgt] + u.c0 : 0;
+#pragma unroll
+    for (int k = 0; k < kMSIdx; ++k) {
+      const int c = j + k * kMSConsumers;
+      kidx[k] = (u.tgt >= 0 && c < u.c1 - u.c0) ? __ldg(stream_idx + sp + c) : -1;
+    }
+  };
+  auto gather_issue = [&](const int* kidx, double2* dst) {
+#pragma unroll
+    for (int k = 0; k < kMSIdx; ++k)
+      if (kidx[k] >= 0) cp_async16(dst + j + k * kMSConsumers, mult + kidx[k]);
+    cp_async_commit();
+  };
+  int r = 1, nsl = 0, t = 0, P = 1, buf = 0;
+  bool act = false;
+  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+  int kidx[kMSIdx];
+  MSUnit u = take();
+  gather_idx(u, kidx);
+  gather_issue(kidx, mb[0]);
+  while (u.tgt >= 0) {
+    const MSUnit un = take();  // published before u's stages were issued
+    gather_idx(un, kidx);      // loads in flight while the first stage is consumed
+    if (u.flags & 1) {
+      r = rows[u.tgt];
+      nsl = r > 0 ? kMSConsumers / r : 0;
+      P = max(1, nsl * r);
+      t = r > 0 ? j % r : 0;
+      act = j < P;
+      ar0 = ai0 = ar1 = ai1 = 0.0;
+    }
+    cp_async_wait_all();
+    consumers_sync();  // u's multipoles (mb[buf]) complete; everyone is done with mb[buf ^ 1]
+    const double2* mv = mb[buf];
+    const int ne = (u.c1 - u.c0) * r;
+    for (int e0 = 0; e0 < ne; e0 += kMSStageE) {
+      const int e1 = min(ne, e0 + kMSStageE);
+      mbar_wait(&full[stage], sphase);
+      if (act) {
+        // this thread's entries e = j (mod P) in [e0, e1); entry e is (row t, column (e - t) / r)
+        int e = e0 + ((j - e0) % P + P) % P;
+        int c = (e - t) / r;
+        const double2* R = ring[stage] - e0;
+        for (; e + 3 * P < e1; e += 4 * P, c += 4 * nsl) {
+          const double2 m0 = R[e], v0 = mv[c];
+          const double2 m1 = R[e + P], v1 = mv[c + nsl];
+          const double2 m2 = R[e + 2 * P], v2 = mv[c + 2 * nsl];
+          const double2 m3 = R[e + 3 * P], v3 = mv[c + 3 * nsl];
+          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
+          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
+          ar1 = fma(m1.x, v1.x, fma(-m1.y, v1.y, ar1));
+          ai1 = fma(m1.x, v1.y, fma(m1.y, v1.x, ai1));
+          ar0 = fma(m2.x, v2.x, fma(-m2.y, v2.y, ar0));
+          ai0 = fma(m2.x, v2.y, fma(m2.y, v2.x, ai0));
+          ar1 = fma(m3.x, v3.x, fma(-m3.y, v3.y, ar1));
+          ai1 = fma(m3.x, v3.y, fma(m3.y, v3.x, ai1));
+        }
+        for (; e < e1; e += P, c += nsl) {
+          const double2 m0 = R[e], v0 = mv[c];
+          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
+          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kMSStages) {
+        stage = 0;
+        sphase ^= 1;
+      }
+      if (e0 == 0) gather_issue(kidx, mb[buf ^ 1]);  // next unit's multipoles
+    }
+    if (ne == 0) gather_issue(kidx, mb[buf ^ 1]);
+    if (u.flags & 2) {  // reduce the slices of each row, write u
+      red[j] = make_double2(ar0 + ar1, ai0 + ai1);
+      consumers_sync();
+      if (j < r) {
+        double sr = 0.0, si = 0.0;
+        for (int q = j; q < P; q += r) {
+          sr += red[q].x;
+          si += red[q].y;
+        }
+        loc[loc_off[u.tgt] + j] = make_double2(sr, si);
+      }
+    }
+    u = un;
+    buf ^= 1;
+  }
+  cp_async_wait_all();
 }
 
 // ---- near field P2P ------------------------------------------------------------
@@ -732,6 +1034,40 @@ __global__ void norm2_kernel(int64_t n, const double2* __restrict__ w, double2* 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// ---- H0 evaluator probe (dafmm_h0_eval) ------------------------------------------------------
+// out[i] = H0^(1)(sqrt(z2[i])) by the band `code`'s evaluator, lane-blocked exactly as in P2P /
+// M2L (kH0EvalTB entries per thread, coefficient tables in shared memory): it exposes the
+// product's inner evaluator to the parity tests, band by band.
+constexpr int kH0EvalTB = 4;
+template <int CODE>
+__device__ __forceinline__ void h0_eval_block(const double* z2, double* re, double* im, const PolyTable& T,
+                                              const FarBand* band) {
+  eval_band<CODE, kH0EvalTB>(z2, re, im, T, band);
+}
+__global__ void __launch_bounds__(128) h0_eval_kernel(const double* __restrict__ z2, double2* __restrict__ out,
+                                                      int64_t n, int code) {
+  __shared__ PolyTable T;
+  __shared__ FarBand bands[dafmm_fit::NUM_FAR];
+  load_poly_table(T);
+  load_far_bands(bands);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kH0EvalTB;
+  for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kH0EvalTB; i0 < n; i0 += stride) {
+    double z[kH0EvalTB], re[kH0EvalTB], im[kH0EvalTB];
+#pragma unroll
+    for (int q = 0; q < kH0EvalTB; ++q) z[q] = z2[i0 + q < n ? i0 + q : i0];
+    switch (code) {
+      case kBandGeneric: h0_eval_block<kBandGeneric>(z, re, im, T, nullptr); break;
+      case kBandNear7: h0_eval_block<kBandNear7>(z, re, im, T, nullptr); break;
+      case kBandNear8: h0_eval_block<kBandNear8>(z, re, im, T, nullptr); break;
+      case kBandNear12: h0_eval_block<kBandNear12>(z, re, im, T, nullptr); break;
+      default: h0_eval_block<kBandFarData>(z, re, im, T, bands + (code - kBandFarData));
+    }
+#pragma unroll
+    for (int q = 0; q < kH0EvalTB; ++q)
+      if (i0 + q < n) out[i0 + q] = make_double2(re[q], im[q]);
+  }
+}
+
 int grid_for(int64_t n, int threads, int cap) {
   int64_t g = (n + threads - 1) / threads;
   if (g > cap) g = cap;
@@ -831,17 +1167,61 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
        upload(d, &d.near_end, pk.near_end, err) && upload(d, &d.leaf_loc_off, pk.leaf_loc_off, err) &&
        upload(d, &d.leaf_rank, pk.leaf_rank, err) && upload(d, &d.leaf_U_off, pk.leaf_U_off, err) &&
        upload(d, &d.leaf_band, pk.leaf_band, err);
+  if (ok && d.m2l_targets > 0 && plan.opt.m2l_store != 0) {  // stored M2L blocks
+    std::vector<int64_t> moff(d.m2l_targets);
+    int64_t tot = 0;
+    int maxr = 0;
+    for (int t = 0; t < d.m2l_targets; ++t) {
+      moff[t] = tot;
+      maxr = std::max(maxr, pk.m2l_rows[t]);
+      tot += (int64_t)pk.m2l_rows[t] * (pk.m2l_stream_ptr[t + 1] - pk.m2l_stream_ptr[t]);
+    }
+    size_t free_b = 0, total_b = 0;
+    if (!ck(cudaMemGetInfo(&free_b, &total_b), err, "cudaMemGetInfo")) return DAFMM_ECUDA;
+    const size_t bytes = (size_t)tot * sizeof(double2);
+    if (plan.opt.m2l_store == 1 && maxr > kMaxStoredRows) {
+      err = "m2l_store=1: a node has " + std::to_string(maxr) + " pivots (at most " +
+            std::to_string(kMaxStoredRows) + " supported)";
+      return DAFMM_EINVAL;
+    }
+    if (plan.opt.m2l_store == 1 && bytes > free_b) {
+      err = "m2l_store=1: the M2L blocks need " + std::to_string(bytes) + " bytes, " + std::to_string(free_b) +
+            " free";
+      return DAFMM_ENOMEM;
+    }
+    if (tot > 0 && maxr <= kMaxStoredRows && (plan.opt.m2l_store == 1 || bytes <= free_b / 2)) {
+      ok = upload(d, &d.m2l_mat_off, moff, err) && alloc(d, &d.m2l_mat, (size_t)tot, err);
+      if (ok) {
+        m2l_form_kernel<<<d.m2l_targets, kMSFormThreads>>>(d.m2l_loc_off, d.m2l_rows, d.m2l_stream_ptr,
+                                                         d.m2l_stream_idx, d.m2l_mat_off, d.ti_xy, d.so_xy,
+                                                         d.m2l_mat);
+        ok = ck(cudaGetLastError(), err, "m2l_form_kernel") && ck(cudaDeviceSynchronize(), err, "m2l_form_kernel");
+      }
+      if (!ok) return DAFMM_ECUDA;
+    }
+  }
   if (ok) {
     int per_sm = 0, sms = 0, dev = 0;
     ok = ck(cudaGetDevice(&dev), err, "cudaGetDevice") &&
          ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), err, "SM count") &&
          ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
     d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
+    d.m2l_store_grid = std::max(1, std::min(d.m2l_targets, DAFMM_MS_PER_SM * sms));
+    if (d.m2l_mat)
+      ok = ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
+              err, "stored M2L shared memory") &&
+           ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
+              "carveout") &&
+           // the largest shared-memory carveout for P2P too, so an SM running three P2P CTAs has
+           // room for the stored-M2L CTA beside them
+           ck(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err, "carveout");
   }
   int prio_lo = 0, prio_hi = 0;
   ok = ok && ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), err, "stream priorities") &&
-       ck(cudaStreamCreateWithPriority(&d.s_far, cudaStreamNonBlocking, prio_hi), err, "far stream") &&
-       ck(cudaStreamCreateWithPriority(&d.s_near, cudaStreamNonBlocking, prio_lo), err, "near stream") &&
+       ck(cudaStreamCreateWithPriority(&d.s_far, cudaStreamNonBlocking, DAFMM_NEAR_HIGH ? prio_lo : prio_hi), err,
+          "far stream") &&
+       ck(cudaStreamCreateWithPriority(&d.s_near, cudaStreamNonBlocking, DAFMM_NEAR_HIGH ? prio_hi : prio_lo), err,
+          "near stream") &&
        ck(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming), err, "fork event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_far, cudaEventDisableTiming), err, "join event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_near, cudaEventDisableTiming), err, "join event") &&
@@ -943,7 +1323,12 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   if (far)
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
   mark(EV_M2L, fs);
-  if (far && d.m2l_targets > 0) {  // M2L, persistent CTAs
+  if (far && d.m2l_targets > 0 && d.m2l_mat) {  // M2L from the stored blocks
+    m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, fs>>>(d.m2l_targets, d.m2l_ticket,
+                                                               d.m2l_loc_off, d.m2l_rows, d.m2l_stream_ptr, d.m2l_stream_idx,
+                                                               d.m2l_mat_off, d.m2l_mat, d.mult, d.loc);
+    ++d.launches;
+  } else if (far && d.m2l_targets > 0) {  // M2L, kernel entries on the fly, persistent CTAs
     m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, fs>>>(d.m2l_targets, d.m2l_ticket, d.m2l_loc_off, d.m2l_rows,
                                                     d.m2l_stream_ptr, d.m2l_stream_idx, d.m2l_item_ptr, d.m2l_item_code,
                                                     d.m2l_item_begin, d.m2l_item_end, d.ti_xy, d.so_xy,
@@ -1102,6 +1487,18 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
   *iters_out = iters;
   *relres_out = rn / bnorm;
   return converged ? DAFMM_OK : DAFMM_NOT_CONVERGED;
+}
+
+int h0_eval(const double* z2, double2* out, int64_t n, int code, cudaStream_t s, std::string& err) {
+  if (n == 0) return DAFMM_OK;
+  const int64_t blocks = std::min<int64_t>((n + 128 * kH0EvalTB - 1) / (128 * kH0EvalTB), 148 * 16);
+  h0_eval_kernel<<<(int)blocks, 128, 0, s>>>(z2, out, n, code);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    err = std::string("h0_eval_kernel: ") + cudaGetErrorString(e);
+    return DAFMM_ECUDA;
+  }
+  return DAFMM_OK;
 }
 
 }  // namespace dafmm

@@ -25,6 +25,7 @@ struct Options {
   int num_threads = 0;     // host setup threads (0: OpenMP default)
   int host_only = 0;       // skip the device upload
   int symmetric_pivots = 0;  // reading R19 (option): one ACA per node, outgoing skeleton = incoming
+  int m2l_store = -1;        // M2L blocks: -1 auto, 0 evaluated on the fly every matvec, 1 stored in HBM
 };
 
 struct Box {

@@ -67,3 +67,22 @@ def test_roofline_entry_overlap_span():
     assert r["achieved"] == pytest.approx((4000 * 100.0 + 1000 * 50.0) / 2.5e-3 / 1e12)
     assert r["frac"] == pytest.approx(r["achieved"] / 34.0) and r["traffic"] == 130
     assert r["kernels"]["m2l"]["launch_ms_concurrent"] == 2.0
+
+
+def test_roofline_entry_stored_m2l():
+    """Stored M2L blocks: the dominant kernel is the HBM stream; achieved = algorithmic bytes
+    (16 B per entry + 20 B per source-stream element + 16 B per output) / its launch time."""
+    stats = {"p2p_pairs": 1000, "m2l_entries": 4000, "m2l_stored": 1, "m2l_stream_len": 100, "n_loc": 50,
+             "operator_bytes": 10000, "n": 64}
+    inputs = {"fp64_tflops_measured": 34.0,
+              "kernels": {"m2l_stored": {"dram_bytes_per_launch": 70000, "ncu_time_ms": 0.5},
+                          "p2p": {"fp64_flops_per_entry": 50.0, "dram_bytes_per_launch": 7}}}
+    r = bench.roofline_entry({"near": 2.0, "m2l": 1.0, "overlap_span": 3.0}, 2, stats, inputs, ms_per_step=2.0)
+    nbytes = 16 * 4000 + 20 * 100 + 16 * 50
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s"
+    assert r["algorithmic_bytes_per_launch"] == nbytes
+    assert r["achieved"] == pytest.approx(nbytes / 0.5e-3 / 1e9)
+    assert r["frac"] == pytest.approx(r["achieved"] / r["peak"]) and r["traffic"] == 70000
+    assert r["concurrent"]["p2p"]["achieved"] == pytest.approx(1000 * 50.0 / 1e-3 / 1e12)
+    st = r["step"]
+    assert st["bound_ms"] == max(st["alu_ms"], st["hbm_ms"]) and st["frac"] == pytest.approx(st["bound_ms"] / 2.0)

@@ -119,3 +119,34 @@ def test_host_only_plan_refuses_device_calls():
     with pytest.raises(prod.DAFMMError):
         op.set_profiling(True)
     op.close()
+
+
+def test_h0_band_table():
+    """dafmm_h0_bands (host only): the near bands are (0, 7], (0, 8], (0, 12]; the data bands are
+    finite positive intervals inside the generic band's (0, inf) and overlap so that every z
+    beyond the near bands is covered by some data band up to the largest one's end."""
+    from paper_2204_00326_b200 import binding
+    bands = binding.dafmm_h0_bands()
+    assert bands[0] == (0.0, float("inf"))
+    assert bands[1] == (0.0, 8.0) and bands[2] == (0.0, 12.0) and bands[3] == (0.0, 7.0)
+    data = sorted(bands[4:])
+    assert len(data) >= 1
+    for lo, hi in data:
+        assert 0.0 < lo < hi < float("inf")
+    reach = 12.0
+    for lo, hi in data:
+        if lo <= reach:
+            reach = max(reach, hi)
+    assert reach >= max(hi for _, hi in data) * 0.999
+
+
+def test_m2l_store_option_validated():
+    """dafmm_options.m2l_store takes -1 (auto), 0 or 1; anything else is DAFMM_EINVAL."""
+    from paper_2204_00326_b200 import binding
+    P = make_problem("c1", n=16)
+    assert binding.default_options().m2l_store == -1
+    with pytest.raises(binding.DAFMMError):
+        binding.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1e-8, host_only=1, m2l_store=2)
+    op = binding.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1e-8, host_only=1, m2l_store=1)
+    st = op.stats()
+    assert st["m2l_stored"] == 0 and st["m2l_store_bytes"] == 0  # host-only plan: nothing on a device

@@ -50,13 +50,20 @@ def _oracle_on_product_plan(P, op, tmp_path):
 @pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0),
                                           ("c1", 128, 4.0), ("c1", 40, 7.0), ("c5", 5, 12.0), ("c5", 5, 8.0)])
 def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
+    """Both M2L modes: the blocks stored in HBM (m2l_store=1) and evaluated on the fly (0)."""
     P = make_problem(name, n=n, kappa=kappa)
-    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=1)
+    assert op.stats()["m2l_stored"] == 1
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
     x = P["x"]
     y_gpu = _gpu_matvec(op, x)
     y_cpu = nca.matvec(x)
     assert _rel(y_gpu - x, y_cpu - x) <= 1e-11
+    op_fly = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=0)
+    assert op_fly.stats()["m2l_stored"] == 0 and op_fly.stats()["m2l_store_bytes"] == 0
+    y_fly = _gpu_matvec(op_fly, x)
+    assert _rel(y_fly - x, y_cpu - x) <= 1e-11
+    assert _rel(y_fly - x, y_gpu - x) <= 1e-13
     rows = np.arange(0, prob.n, 3)
     yd = oracle.dense_matvec_rows(prob, x, rows)
     assert _rel(y_gpu[rows] - x[rows], yd - x[rows]) <= 10 * P["nca_tol"]

@@ -14,7 +14,7 @@ python - "$TAG" <<'PY'
 import json, sys
 tag = sys.argv[1]
 b = json.loads(open('gpurun_out/bench_%s.json' % tag).read().strip().splitlines()[-1])
-E = {'near_kernel': b['plan']['p2p_pairs'], 'p2p_kernel': b['plan']['p2p_pairs'], 'm2l_kernel': b['plan']['m2l_entries']}
+E = {'near_kernel': b['plan']['p2p_pairs'], 'p2p_kernel': b['plan']['p2p_pairs'], 'm2l_kernel': b['plan']['m2l_entries'], 'm2l_stored_kernel': b['plan']['m2l_entries']}
 for d in json.load(open('profiles/%s_ncu_summary.json' % tag)):
     if d['kernel'] in E:
         e = E[d['kernel']]
@@ -23,7 +23,12 @@ for d in json.load(open('profiles/%s_ncu_summary.json' % tag)):
               'inst/entry %.1f' % (d['warp_inst'] * 32 / e),
               'pipe %.1f issue %.1f warps %.1f regs %d' % (d['fp64_pipe_pct'], d['issue_pct'], d['warps_active_pct'], d['regs']))
 PY
-for k in m2l p2p near; do
-  ncu -i gpurun_out/prof_$TAG.ncu-rep --page source --csv --kernel-name ${k}_kernel --launch-skip 0 --launch-count 1 2>/dev/null > /tmp/src_${k}_$TAG.csv
-  echo "== $k"; python tools/stalls.py /tmp/src_${k}_$TAG.csv 6 | tee profiles/${TAG}_${k}_stalls.txt
+for k in m2l_stored p2p; do
+  ncu -i gpurun_out/prof_$TAG.ncu-rep --page source --csv --kernel-name ${k}_kernel --launch-skip 0 --launch-count 1 2>/dev/null > gpurun_out/src_${k}_$TAG.csv
+  echo "== $k"; python tools/stalls.py gpurun_out/src_${k}_$TAG.csv 6 | tee profiles/${TAG}_${k}_stalls.txt
 done
+if [ -f gpurun_out/prof_${TAG}_fly.ncu-rep ]; then
+  python tools/ncu_summary.py gpurun_out/prof_${TAG}_fly.ncu-rep > profiles/${TAG}_fly_ncu_summary.json
+  ncu -i gpurun_out/prof_${TAG}_fly.ncu-rep --page source --csv --kernel-name m2l_kernel --launch-skip 0 --launch-count 1 2>/dev/null > gpurun_out/src_m2l_$TAG.csv
+  echo "== m2l (on the fly)"; python tools/stalls.py gpurun_out/src_m2l_$TAG.csv 6 | tee profiles/${TAG}_m2l_stalls.txt
+fi

@@ -17,5 +17,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
     python tools/ncu_target.py $CFG 3 > gpurun_out/ncu_launches_$TAG.log 2>&1; echo "launches rc=$?"
 ncu --set full --clock-control none --import-source on \
     --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active \
-    -k regex:"p2p_kernel|m2l_kernel|translate|combine_kernel" -s 0 -c 20 -o gpurun_out/prof_$TAG -f \
+    -k regex:"p2p_kernel|m2l_kernel|m2l_stored|translate|combine_kernel" -s 0 -c 20 -o gpurun_out/prof_$TAG -f \
     python tools/ncu_target.py $CFG 1 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
+# the on-the-fly M2L kernel (dafmm_options.m2l_store = 0) for comparison
+ncu --set full --clock-control none --import-source on \
+    --metrics sm__sass_thread_inst_executed_op_dfma_pred_on.sum,sm__sass_thread_inst_executed_op_dadd_pred_on.sum,sm__sass_thread_inst_executed_op_dmul_pred_on.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active \
+    -k regex:"m2l_kernel" -s 0 -c 1 -o gpurun_out/prof_${TAG}_fly -f \
+    python tools/ncu_target.py $CFG 1 0 > gpurun_out/ncu_fly_$TAG.log 2>&1; echo "ncu fly rc=$?"

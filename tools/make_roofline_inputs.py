@@ -7,9 +7,10 @@ import json
 import sys
 
 summary, bench, tag = sys.argv[1], sys.argv[2], sys.argv[3]
-S = json.load(open(summary))
+S = [d for path in summary.split(",") for d in json.load(open(path))]  # comma-separated summaries
 B = json.loads(open(bench).read().strip().splitlines()[-1])
-entries = {"p2p_kernel": B["plan"]["p2p_pairs"], "near_kernel": B["plan"]["p2p_pairs"], "m2l_kernel": B["plan"]["m2l_entries"]}
+entries = {"p2p_kernel": B["plan"]["p2p_pairs"], "near_kernel": B["plan"]["p2p_pairs"],
+           "m2l_kernel": B["plan"]["m2l_entries"], "m2l_stored_kernel": B["plan"]["m2l_entries"]}
 out = {"source": "profiles/%s_ncu_summary.json (ncu --set full, config %s)" % (tag, B["config"]["workload"][:2]),
        "fp64_tflops_measured": 34.157,
        "fp64_peak_source": "tools/fp64_peak.cu DFMA chains, 148 SM x 8 CTA x 256 thr, 1965 MHz, "
@@ -20,6 +21,7 @@ for d in S:
     if k in entries:
         e = entries[k]
         out["kernels"][{"near_kernel": "p2p"}.get(k, k.replace("_kernel", ""))] = {
+            "entries_per_launch": e,
             "fp64_flops_per_entry": (2 * d["dfma"] + d["dadd"] + d["dmul"]) / e,
             "fp64_inst_per_entry": (d["dfma"] + d["dadd"] + d["dmul"]) / e,
             "inst_per_entry": d["warp_inst"] * 32 / e,

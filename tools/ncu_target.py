@@ -11,7 +11,8 @@ from synth.configs import make_problem  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 P = make_problem(name)
-op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+mode = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # dafmm_options.m2l_store
+op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=mode)
 x = torch.from_numpy(P["x"]).cuda()
 y = torch.empty_like(x)
 for _ in range(reps):
