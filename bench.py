@@ -354,10 +354,12 @@ def gmres_case(name, prod, torch):
     t0 = time.perf_counter()
     rc, iters, relres = op.gmres(f, psi, P["gmres_tol"], maxit, restart)
     solve = time.perf_counter() - t0
+    st = op.stats()
     op.close()
     return {"config": name, "N": int(P["points"].shape[0]), "kappa": P["kappa"], "tol": P["gmres_tol"],
             "restart": restart, "status": "converged" if rc == 0 else "not_converged", "iterations": iters,
-            "true_relres": relres, "solve_s": solve, "setup_s": setup}
+            "true_relres": relres, "solve_s": solve, "ms_per_iteration": 1e3 * solve / max(iters, 1),
+            "reorthogonalisations": st["gmres_reorth"], "m2l_stored": st["m2l_stored"], "setup_s": setup}
 
 
 def run_ours(args):

@@ -221,6 +221,7 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->m2l_store_bytes = h->dev.m2l_mat != nullptr ? h->m2l_entries * 16 : 0;
   out->m2l_stream_len = h->m2l_stream_len;
   out->n_loc = h->n_loc;
+  out->gmres_reorth = h->dev.gm_reorth;
   for (size_t b = 0; b < h->m2l_band.size() && b < 48; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
   for (size_t b = 0; b < h->p2p_band.size() && b < 48; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
   return DAFMM_OK;

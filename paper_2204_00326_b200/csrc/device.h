@@ -95,6 +95,7 @@ struct DevPlan {
   double2* gm_part = nullptr;  // partial sums
   double* gm_hostbuf = nullptr;  // pinned
   int gm_part_blocks = 0;
+  int64_t gm_reorth = 0;       // reorthogonalisation passes in the last ls_gmres_solve
   size_t device_bytes = 0;
   std::vector<void*> allocations;
   // per-pass CUDA-event profiling (dafmm_set_profiling / dafmm_pass_times)

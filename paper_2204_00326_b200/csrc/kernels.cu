@@ -603,8 +603,8 @@ __global__ void __launch_bounds__(kMSFormThreads) m2l_form_kernel(const int64_t*
   }
 }
 
-// Apply the stored blocks: u[t] = sum_s A_{t s} m_s.  Persistent CTAs take target nodes from a
-// ticket counter (nodes packed by decreasing work).  Warp-specialised: one lane of the producer
+// Apply the stored blocks: u[t] = sum_s A_{t s} m_s.  Persistent CTAs; CTA b takes target nodes
+// b, b + G, b + 2G, ... (packed by decreasing work).  Warp-specialised: one lane of the producer
 // warp cuts each node into work units of at most kMSCols source columns, publishes the unit
 // descriptors one unit ahead (a kMSUnits-slot ring), and streams each unit's entries through a
 // kMSStages-deep ring of shared-memory stages with TMA bulk copies (mbarrier full/empty
@@ -614,11 +614,13 @@ __global__ void __launch_bounds__(kMSFormThreads) m2l_form_kernel(const int64_t*
 // At a node's last unit the slices of each row are reduced and u is written.
 struct MSUnit {
   int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
+  int r, pad;              // the node's rows
+  int64_t sp, lo;          // its source stream offset and output offset
 };
 constexpr int kMSUnits = 4;
 constexpr int kMSIdx = kMSCols / kMSConsumers;  // multipole indices per consumer thread per unit
 __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
-    int ntargets, int* __restrict__ ticket, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
     const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
     const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
     double2* __restrict__ loc) {
@@ -646,24 +648,46 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     int stage = 0, uslot = 0;
     uint32_t sphase = 0, uphase = 0;
     // the unit sequence: (tgt, c0, c1); next_unit() advances it, fetching tickets as needed
-    int tgt = -2, L = 0, c0 = 0;
+    // static schedule: this CTA's nodes are blockIdx.x + k gridDim.x (the list is sorted by
+    // decreasing work, so round-robin balances to within one node); the metadata of node k+1
+    // is loaded while node k streams (independent addresses: the loads do not stall the lane)
+    int tgt = -2, L = 0, c0 = 0, r = 0;
+    int64_t sp = 0, lo = 0, moff = 0;
+    int ntgt = blockIdx.x, nr = 0;
+    int64_t nsp = 0, nsp1 = 0, nlo = 0, nmoff = 0;
+    auto prefetch_node = [&]() {
+      if (ntgt < ntargets) {
+        nr = rows[ntgt];
+        nsp = stream_ptr[ntgt];
+        nsp1 = stream_ptr[ntgt + 1];
+        nlo = loc_off[ntgt];
+        nmoff = mat_off[ntgt];
+      }
+    };
+    prefetch_node();
     auto next_unit = [&](MSUnit& u) {
       if (tgt == -1) {
-        u = MSUnit{-1, 0, 0, 0};
+        u = MSUnit{-1, 0, 0, 0, 0, 0, 0, 0};
         return;
       }
       if (tgt == -2 || c0 >= L) {  // next node
-        tgt = atomicAdd(ticket, 1);
-        if (tgt >= ntargets) {
+        if (ntgt >= ntargets) {
           tgt = -1;
-          u = MSUnit{-1, 0, 0, 0};
+          u = MSUnit{-1, 0, 0, 0, 0, 0, 0, 0};
           return;
         }
-        L = (int)(stream_ptr[tgt + 1] - stream_ptr[tgt]);
+        tgt = ntgt;
+        r = nr;
+        sp = nsp;
+        L = (int)(nsp1 - nsp);
+        lo = nlo;
+        moff = nmoff;
         c0 = 0;
+        ntgt += gridDim.x;
+        prefetch_node();
       }
       const int c1 = min(L, c0 + kMSCols);
-      u = MSUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0)};
+      u = MSUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0), r, 0, sp, lo};
       c0 = c1;
     };
     auto publish = [&](const MSUnit& u) {
@@ -677,13 +701,14 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     };
     MSUnit cur, nxt;
     next_unit(cur);
+    int64_t cur_moff = moff;
     publish(cur);
     while (cur.tgt >= 0) {
       next_unit(nxt);
+      const int64_t nxt_moff = moff;
       publish(nxt);  // one unit ahead: the consumers prefetch its multipoles
-      const int r = rows[cur.tgt];
-      const double2* src = mat + mat_off[cur.tgt] + (int64_t)cur.c0 * r;
-      const int ne = (cur.c1 - cur.c0) * r;
+      const double2* src = mat + cur_moff + (int64_t)cur.c0 * cur.r;
+      const int ne = (cur.c1 - cur.c0) * cur.r;
       for (int e0 = 0; e0 < ne; e0 += kMSStageE) {
         const int cnt = min(kMSStageE, ne - e0);
         mbar_wait(&empty[stage], sphase ^ 1);
@@ -695,6 +720,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
         }
       }
       cur = nxt;
+      cur_moff = nxt_moff;
     }
     return;
   }
@@ -714,7 +740,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     return u;
   };
   auto gather_idx = [&](const MSUnit& u, int* kidx) {
-    const int64_t sp = u.tgt >= 0 ? stream_ptr[u.tgt] + u.c0 : 0;
+    const int64_t sp = u.sp + u.c0;
 #pragma unroll
     for (int k = 0; k < kMSIdx; ++k) {
       const int c = j + k * kMSConsumers;
@@ -727,7 +753,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
       if (kidx[k] >= 0) cp_async16(dst + j + k * kMSConsumers, mult + kidx[k]);
     cp_async_commit();
   };
-  int r = 1, nsl = 0, t = 0, P = 1, buf = 0;
+  int nsl = 0, P = 1, buf = 0, sl = 0;
   bool act = false;
   double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
   int kidx[kMSIdx];
@@ -736,12 +762,12 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
   gather_issue(kidx, mb[0]);
   while (u.tgt >= 0) {
     const MSUnit un = take();  // published before u's stages were issued
-    gather_idx(un, kidx);      // loads in flight while the first stage is consumed
+    gather_idx(un, kidx);      // in flight while the first half of u is consumed
+    const int r = u.r;
     if (u.flags & 1) {
-      r = rows[u.tgt];
       nsl = r > 0 ? kMSConsumers / r : 0;
       P = max(1, nsl * r);
-      t = r > 0 ? j % r : 0;
+      sl = r > 0 ? j / r : 0;
       act = j < P;
       ar0 = ai0 = ar1 = ai1 = 0.0;
     }
@@ -749,13 +775,14 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     consumers_sync();  // u's multipoles (mb[buf]) complete; everyone is done with mb[buf ^ 1]
     const double2* mv = mb[buf];
     const int ne = (u.c1 - u.c0) * r;
-    for (int e0 = 0; e0 < ne; e0 += kMSStageE) {
-      const int e1 = min(ne, e0 + kMSStageE);
+    const int nst = (ne + kMSStageE - 1) / kMSStageE;
+    // this thread's entries in the unit: e = j + k P (row t = j mod r, column c = sl + k nsl);
+    // e and c run on across the stages
+    int e = j, c = sl;
+    for (int st = 0; st < nst; ++st) {
+      const int e0 = st * kMSStageE, e1 = min(ne, e0 + kMSStageE);
       mbar_wait(&full[stage], sphase);
       if (act) {
-        // this thread's entries e = j (mod P) in [e0, e1); entry e is (row t, column (e - t) / r)
-        int e = e0 + ((j - e0) % P + P) % P;
-        int c = (e - t) / r;
         const double2* R = ring[stage] - e0;
         for (; e + 3 * P < e1; e += 4 * P, c += 4 * nsl) {
           const double2 m0 = R[e], v0 = mv[c];
@@ -783,9 +810,9 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
         stage = 0;
         sphase ^= 1;
       }
-      if (e0 == 0) gather_issue(kidx, mb[buf ^ 1]);  // next unit's multipoles
+      if (st == nst / 2) gather_issue(kidx, mb[buf ^ 1]);  // next unit's multipoles (indices have landed)
     }
-    if (ne == 0) gather_issue(kidx, mb[buf ^ 1]);
+    if (nst == 0) gather_issue(kidx, mb[buf ^ 1]);
     if (u.flags & 2) {  // reduce the slices of each row, write u
       red[j] = make_double2(ar0 + ar1, ai0 + ai1);
       consumers_sync();
@@ -795,7 +822,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
           sr += red[q].x;
           si += red[q].y;
         }
-        loc[loc_off[u.tgt] + j] = make_double2(sr, si);
+        loc[u.lo + j] = make_double2(sr, si);
       }
     }
     u = un;
@@ -810,7 +837,12 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
 #ifndef DAFMM_P2P_MINB
 #define DAFMM_P2P_MINB 3
 #endif
-__global__ void __launch_bounds__(kNearThreads, DAFMM_P2P_MINB) p2p_kernel(
+#ifdef DAFMM_P2P_MAXREG
+#define DAFMM_P2P_REGCAP __maxnreg__(DAFMM_P2P_MAXREG)
+#else
+#define DAFMM_P2P_REGCAP __launch_bounds__(kNearThreads, DAFMM_P2P_MINB)
+#endif
+__global__ void DAFMM_P2P_REGCAP p2p_kernel(
     const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end, const int32_t* __restrict__ near_ptr,
     const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int32_t* __restrict__ leaf_band,
     const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi) {
@@ -1315,7 +1347,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   if (far) {
     cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, fs);
     cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, fs);
-    if (d.m2l_targets > 0) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), fs);
+    if (d.m2l_targets > 0 && !d.m2l_mat) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), fs);
   }
   mark(EV_P2M, fs);
   if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0, fs);  // P2M
@@ -1324,8 +1356,8 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
   mark(EV_M2L, fs);
   if (far && d.m2l_targets > 0 && d.m2l_mat) {  // M2L from the stored blocks
-    m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, fs>>>(d.m2l_targets, d.m2l_ticket,
-                                                               d.m2l_loc_off, d.m2l_rows, d.m2l_stream_ptr, d.m2l_stream_idx,
+    m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, fs>>>(d.m2l_targets, d.m2l_loc_off,
+                                                               d.m2l_rows, d.m2l_stream_ptr, d.m2l_stream_idx,
                                                                d.m2l_mat_off, d.m2l_mat, d.mult, d.loc);
     ++d.launches;
   } else if (far && d.m2l_targets > 0) {  // M2L, kernel entries on the fly, persistent CTAs
@@ -1363,7 +1395,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
 }
 
 // ============================================================================================
-// Restarted GMRES (reading R14) with CGS2 orthogonalisation on the device.
+// Restarted GMRES (reading R14) with CGS + DGKS reorthogonalisation (R20) on the device.
 int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit, int restart, int* iters_out,
               double* relres_out, double* history, std::string& err) {
   const int64_t n = d.n;
@@ -1403,6 +1435,7 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
   std::vector<std::complex<double>> H((size_t)(m + 1) * m), g(m + 1), sn(m);
   std::vector<double> cs(m);
   int iters = 0;
+  d.gm_reorth = 0;
   bool converged = false;
   // r = f (psi0 = 0)
   cudaMemcpyAsync(d.gm_r, f, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s);
@@ -1420,22 +1453,38 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
       double2* vj1 = d.gm_V + (int64_t)(j + 1) * n;
       if (run_matvec(d, vj, d.gm_w, 3u, err) != DAFMM_OK) return DAFMM_ECUDA;
       ++iters;
-      // CGS2: two passes of h = V^H w, w -= V h
-      for (int pass = 0; pass < 2; ++pass) {
+      // CGS with DGKS reorthogonalisation (reading R20): one pass h = V^H w, w -= V h; a second
+      // pass only when the projection cancelled ||w|| below 1/sqrt(2) of its value before it
+      double2* seg2 = d.gm_h + 2 * (m + 2);  // [0] |w|^2 after the projection, [1] before
+      norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
+      reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, seg2 + 1);
+      auto project = [&](int pass) {
         multidot_kernel<<<dim3(nb, (j + 1 + kMD - 1) / kMD), kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_w, d.gm_part,
                                                                                  stride);
         reduce_parts_kernel<<<1, 256, 0, s>>>(nb, j + 1, d.gm_part, stride, d.gm_h + pass * (m + 2));
         combine_kernel<<<nb, kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_h + pass * (m + 2), -1.0, d.gm_w);
-      }
-      norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
-      reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, d.gm_h + 2 * (m + 2));
-      if (!ck(cudaMemcpyAsync(d.gm_hostbuf, d.gm_h, sizeof(double2) * (2 * (m + 2) + 1), cudaMemcpyDeviceToHost, s),
-              err, "D2H") ||
-          !ck(cudaStreamSynchronize(s), err, "sync"))
-        return DAFMM_ECUDA;
+        norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
+        reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, seg2);
+        return ck(cudaMemcpyAsync(d.gm_hostbuf, d.gm_h, sizeof(double2) * 3 * (m + 2), cudaMemcpyDeviceToHost, s),
+                  err, "D2H") &&
+               ck(cudaStreamSynchronize(s), err, "sync");
+      };
+      if (!project(0)) return DAFMM_ECUDA;
       const double* hb = d.gm_hostbuf;
-      for (int i = 0; i <= j; ++i)
-        H[(size_t)i * m + j] = std::complex<double>(hb[2 * i] + hb[2 * ((m + 2) + i)], hb[2 * i + 1] + hb[2 * ((m + 2) + i) + 1]);
+      const double before = hb[2 * (2 * (m + 2) + 1)];
+      bool reorth = hb[2 * 2 * (m + 2)] < 0.5 * before;  // ||w'||^2 < ||w||^2 / 2
+      if (reorth) {
+        ++d.gm_reorth;
+        if (!project(1)) return DAFMM_ECUDA;
+      }
+      for (int i = 0; i <= j; ++i) {
+        double hr = hb[2 * i], hi = hb[2 * i + 1];
+        if (reorth) {
+          hr += hb[2 * ((m + 2) + i)];
+          hi += hb[2 * ((m + 2) + i) + 1];
+        }
+        H[(size_t)i * m + j] = std::complex<double>(hr, hi);
+      }
       double hnext = std::sqrt(hb[2 * 2 * (m + 2)]);
       H[(size_t)(j + 1) * m + j] = hnext;
       if (hnext != 0.0) axpby_kernel<<<nb, kVecThreads, 0, s>>>(n, 1.0 / hnext, d.gm_w, 0.0, d.gm_w, vj1);
