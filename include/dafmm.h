@@ -98,7 +98,7 @@ typedef struct {
   int64_t m2l_store_bytes;      /* their bytes (0 when evaluated on the fly) */
   int64_t m2l_stream_len;       /* source pivots over all M2L target nodes (multipole gathers per matvec) */
   int64_t n_loc;                /* local-expansion coefficients (M2L outputs) */
-  int64_t gmres_reorth;         /* reorthogonalisation passes (DGKS) in the last ls_gmres_solve */
+  int64_t gmres_reorth;         /* second Gram-Schmidt passes (CGS2) in the last ls_gmres_solve */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);

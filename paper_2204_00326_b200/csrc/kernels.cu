@@ -68,6 +68,10 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ perm, const
 // row (all 32 lanes busy) and a warp reduction.  Items wider than 32 kTCK columns are handled
 // in column blocks.  HBM-bound: every operator element is read once per matvec.
 constexpr int kTCK = 8;
+#ifndef DAFMM_TRB
+#define DAFMM_TRB 1  // measured: 1 row per step is fastest (profiles/README.md, r34)
+#endif
+constexpr int kTRB = DAFMM_TRB;  // rows per step in translate_kernel
 __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
                                  const int64_t* __restrict__ item_mat_off, const int32_t* __restrict__ item_cols,
                                  const int32_t* __restrict__ term_ptr, const int64_t* __restrict__ src_off,
@@ -98,30 +102,45 @@ __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off,
       cs = ce;
     }
     const int kmax = min(kTCK, (C - cb + 31) / 32);
-    for (int r = 0; r < R; ++r) {
-      const double2* row = M + (int64_t)r * C + cb + lane;
-      double ar = 0.0, ai = 0.0;
+    // kTRB rows per step: their loads are all in flight together and their warp reductions
+    // interleave (one row at a time left the warp waiting on each shuffle tree)
+    for (int r0 = 0; r0 < R; r0 += kTRB) {
+      double ar[kTRB], ai[kTRB];
 #pragma unroll
-      for (int k = 0; k < kTCK; ++k) {
-        if (k < kmax && cb + lane + 32 * k < C) {
-          const double2 m = ld2(row + 32 * k);
-          ar = fma(m.x, v[k].x, fma(-m.y, v[k].y, ar));
-          ai = fma(m.x, v[k].y, fma(m.y, v[k].x, ai));
+      for (int q = 0; q < kTRB; ++q) ar[q] = ai[q] = 0.0;
+#pragma unroll
+      for (int q = 0; q < kTRB; ++q) {
+        if (r0 + q < R) {
+          const double2* row = M + (int64_t)(r0 + q) * C + cb + lane;
+#pragma unroll
+          for (int k = 0; k < kTCK; ++k) {
+            if (k < kmax && cb + lane + 32 * k < C) {
+              const double2 m = ld2(row + 32 * k);
+              ar[q] = fma(m.x, v[k].x, fma(-m.y, v[k].y, ar[q]));
+              ai[q] = fma(m.x, v[k].y, fma(m.y, v[k].x, ai[q]));
+            }
+          }
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        ar += __shfl_xor_sync(0xffffffffu, ar, o);
-        ai += __shfl_xor_sync(0xffffffffu, ai, o);
-      }
-      if (lane == (r & 31)) {
-        double2 o = make_double2(ar, ai);
-        if (accumulate || cb > 0) {
-          const double2 p = dst[doff + r];
-          o.x += p.x;
-          o.y += p.y;
+#pragma unroll
+        for (int q = 0; q < kTRB; ++q) {
+          ar[q] += __shfl_xor_sync(0xffffffffu, ar[q], o);
+          ai[q] += __shfl_xor_sync(0xffffffffu, ai[q], o);
         }
-        dst[doff + r] = o;
+      }
+#pragma unroll
+      for (int q = 0; q < kTRB; ++q) {
+        if (lane == q && r0 + q < R) {
+          double2 o = make_double2(ar[q], ai[q]);
+          if (accumulate || cb > 0) {
+            const double2 p = dst[doff + r0 + q];
+            o.x += p.x;
+            o.y += p.y;
+          }
+          dst[doff + r0 + q] = o;
+        }
       }
     }
   }
@@ -974,6 +993,9 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* sh) {
 // i = blockIdx.y * kMD + g of this block: w is read once per group of kMD basis vectors and
 // each thread keeps kMD complex partial sums (one pass, no per-vector barriers).
 constexpr int kMD = 8;
+#ifndef DAFMM_MD_BLOCKS
+#define DAFMM_MD_BLOCKS 148
+#endif
 __global__ void multidot_kernel(int64_t n, int k, const double2* __restrict__ V, const double2* __restrict__ w,
                                 double2* __restrict__ part, int stride) {
   __shared__ double2 sh[kMD][kVecThreads / 32];
@@ -1013,18 +1035,26 @@ __global__ void multidot_kernel(int64_t n, int k, const double2* __restrict__ V,
   }
 }
 
-// out[i] = sum_b part[b * stride + i]  (deterministic order)
+// out[i] = sum_b part[b * stride + i]: one warp per output, lanes over the blocks, then a fixed
+// shuffle tree (deterministic order).  Launch with reduce_launch().
 __global__ void reduce_parts_kernel(int nblocks, int k, const double2* __restrict__ part, int stride,
                                     double2* __restrict__ out) {
-  int i = threadIdx.x;
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (i >= k) return;
   double sr = 0.0, si = 0.0;
-  for (int b = 0; b < nblocks; ++b) {
-    double2 v = part[(int64_t)b * stride + i];
+  for (int b = lane; b < nblocks; b += 32) {
+    const double2 v = part[(int64_t)b * stride + i];
     sr += v.x;
     si += v.y;
   }
-  out[i] = make_double2(sr, si);
+  for (int o = 16; o > 0; o >>= 1) {
+    sr += __shfl_down_sync(0xffffffffu, sr, o);
+    si += __shfl_down_sync(0xffffffffu, si, o);
+  }
+  if (lane == 0) out[i] = make_double2(sr, si);
+}
+void reduce_launch(int nblocks, int k, const double2* part, int stride, double2* out, cudaStream_t s) {
+  reduce_parts_kernel<<<(k + 7) / 8, 256, 0, s>>>(nblocks, k, part, stride, out);
 }
 
 // w += sign * sum_{i<k} h_i V_i
@@ -1395,7 +1425,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
 }
 
 // ============================================================================================
-// Restarted GMRES (reading R14) with CGS + DGKS reorthogonalisation (R20) on the device.
+// Restarted GMRES (reading R14) with CGS2 orthogonalisation (R20) on the device.
 int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit, int restart, int* iters_out,
               double* relres_out, double* history, std::string& err) {
   const int64_t n = d.n;
@@ -1414,9 +1444,12 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
     d.gm_part_blocks = nb;
   }
   const int stride = m + 2;
+  // multi-dot blocks per vector group: fewer, longer blocks (their 2-D grid already has a
+  // block row per group of kMD basis vectors)
+  const int nb_md = std::min(nb, DAFMM_MD_BLOCKS);
   auto norm = [&](const double2* v, double& out) -> bool {
     norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, v, d.gm_part);
-    reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, d.gm_h);
+    reduce_launch(nb, 1, d.gm_part, 1, d.gm_h, s);
     if (!ck(cudaMemcpyAsync(d.gm_hostbuf, d.gm_h, sizeof(double2), cudaMemcpyDeviceToHost, s), err, "D2H") ||
         !ck(cudaStreamSynchronize(s), err, "sync"))
       return false;
@@ -1453,38 +1486,25 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
       double2* vj1 = d.gm_V + (int64_t)(j + 1) * n;
       if (run_matvec(d, vj, d.gm_w, 3u, err) != DAFMM_OK) return DAFMM_ECUDA;
       ++iters;
-      // CGS with DGKS reorthogonalisation (reading R20): one pass h = V^H w, w -= V h; a second
-      // pass only when the projection cancelled ||w|| below 1/sqrt(2) of its value before it
-      double2* seg2 = d.gm_h + 2 * (m + 2);  // [0] |w|^2 after the projection, [1] before
-      norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
-      reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, seg2 + 1);
-      auto project = [&](int pass) {
-        multidot_kernel<<<dim3(nb, (j + 1 + kMD - 1) / kMD), kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_w, d.gm_part,
-                                                                                 stride);
-        reduce_parts_kernel<<<1, 256, 0, s>>>(nb, j + 1, d.gm_part, stride, d.gm_h + pass * (m + 2));
+      // CGS2 (reading R20): two passes of h = V^H w, w -= V h, one host synchronisation.  (A DGKS
+      // test that skips the second pass was measured: the projection cancels ||w|| below 1/sqrt(2)
+      // in 98% of the C3 iterations, so it only added a synchronisation; profiles/README.md.)
+      for (int pass = 0; pass < 2; ++pass) {
+        multidot_kernel<<<dim3(nb_md, (j + 1 + kMD - 1) / kMD), kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_w,
+                                                                                    d.gm_part, stride);
+        reduce_launch(nb_md, j + 1, d.gm_part, stride, d.gm_h + pass * (m + 2), s);
         combine_kernel<<<nb, kVecThreads, 0, s>>>(n, j + 1, d.gm_V, d.gm_h + pass * (m + 2), -1.0, d.gm_w);
-        norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
-        reduce_parts_kernel<<<1, 32, 0, s>>>(nb, 1, d.gm_part, 1, seg2);
-        return ck(cudaMemcpyAsync(d.gm_hostbuf, d.gm_h, sizeof(double2) * 3 * (m + 2), cudaMemcpyDeviceToHost, s),
-                  err, "D2H") &&
-               ck(cudaStreamSynchronize(s), err, "sync");
-      };
-      if (!project(0)) return DAFMM_ECUDA;
+      }
+      ++d.gm_reorth;
+      norm2_kernel<<<nb, kVecThreads, 0, s>>>(n, d.gm_w, d.gm_part);
+      reduce_launch(nb, 1, d.gm_part, 1, d.gm_h + 2 * (m + 2), s);
+      if (!ck(cudaMemcpyAsync(d.gm_hostbuf, d.gm_h, sizeof(double2) * (2 * (m + 2) + 1), cudaMemcpyDeviceToHost, s),
+              err, "D2H") ||
+          !ck(cudaStreamSynchronize(s), err, "sync"))
+        return DAFMM_ECUDA;
       const double* hb = d.gm_hostbuf;
-      const double before = hb[2 * (2 * (m + 2) + 1)];
-      bool reorth = hb[2 * 2 * (m + 2)] < 0.5 * before;  // ||w'||^2 < ||w||^2 / 2
-      if (reorth) {
-        ++d.gm_reorth;
-        if (!project(1)) return DAFMM_ECUDA;
-      }
-      for (int i = 0; i <= j; ++i) {
-        double hr = hb[2 * i], hi = hb[2 * i + 1];
-        if (reorth) {
-          hr += hb[2 * ((m + 2) + i)];
-          hi += hb[2 * ((m + 2) + i) + 1];
-        }
-        H[(size_t)i * m + j] = std::complex<double>(hr, hi);
-      }
+      for (int i = 0; i <= j; ++i)
+        H[(size_t)i * m + j] = std::complex<double>(hb[2 * i] + hb[2 * ((m + 2) + i)], hb[2 * i + 1] + hb[2 * ((m + 2) + i) + 1]);
       double hnext = std::sqrt(hb[2 * 2 * (m + 2)]);
       H[(size_t)(j + 1) * m + j] = hnext;
       if (hnext != 0.0) axpby_kernel<<<nb, kVecThreads, 0, s>>>(n, 1.0 / hnext, d.gm_w, 0.0, d.gm_w, vj1);
