@@ -155,15 +155,18 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out);
  * milliseconds per pass into ms_out[DAFMM_NUM_PASSES], in the order
  *   0 gather (caller order -> tree order, w scaling)
  *   1 P2M (plus the memsets of the expansion buffers)
- *   2 M2M, all levels     3 M2L, all levels     4 L2L, all levels
+ *   2 M2M, all levels     3 M2L, all levels but the deepest
+ *   4 L2L, all levels
  *   5 near field P2P (on the handle's internal side stream, concurrent with 1-4)
  *   6 combine: L2P + identity + self term + scatter
  *   7 span of the concurrent part: from the fork after the gather to the later of 4 and 5
+ *   8 M2L of the deepest level when it runs on a third internal stream from the end of P2M
+ *     (build option DAFMM_LEAF_SPLIT; 0 otherwise, the deepest level then being part of 3)
  * plus the number of profiled matvecs and the number of kernels launched by the library since
  * the last reset (either pointer may be NULL).  Passes 1-4 and 5 overlap in time, so their sum
  * exceeds the matvec time; 0 + 7 + 6 is the matvec time.  Errors: DAFMM_EINVAL (null handle /
  * host-only plan), DAFMM_ECUDA. */
-#define DAFMM_NUM_PASSES 8
+#define DAFMM_NUM_PASSES 9
 int dafmm_set_profiling(dafmm_handle h, int enable);
 int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64_t* launches_out);
 

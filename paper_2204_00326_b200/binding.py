@@ -17,8 +17,8 @@ EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_m
             "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times", "dafmm_h0_bands",
             "dafmm_h0_eval"]
 
-NUM_PASSES = 8
-PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near", "combine", "overlap_span"]
+NUM_PASSES = 9
+PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near", "combine", "overlap_span", "m2l_leaf"]
 
 DAFMM_OK, DAFMM_NOT_CONVERGED = 0, 1
 ERRORS = {-1: "DAFMM_EINVAL", -2: "DAFMM_ECUDA", -3: "DAFMM_ENOMEM", -4: "DAFMM_ESETUP"}

@@ -12,10 +12,11 @@ namespace dafmm {
 // Passes timed by the profiler, in launch order (DAFMM_PASS_* of dafmm.h).
 // gather, p2m, m2m, m2l, l2l, near (P2P, side stream), combine (L2P + identity + scatter), and the
 // span of the concurrent part (from the fork to the later of P2P and L2L)
-constexpr int kNumPasses = 8;
+constexpr int kNumPasses = 9;
 // marks recorded before the pass they name (EV_FAR_END after L2L); see harvest_profile
 enum ProfEvent {
-  EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_FAR_END, EV_NEAR0, EV_NEAR1, EV_JOIN, EV_END, EV_COUNT
+  EV_START, EV_FORK, EV_P2M, EV_M2M, EV_M2L, EV_L2L, EV_FAR_END, EV_NEAR0, EV_NEAR1, EV_JOIN, EV_END,
+  EV_LEAF0, EV_LEAF1, EV_COUNT
 };
 
 struct DevBatch {
@@ -37,6 +38,10 @@ struct DevPlan {
   cudaStream_t s_far = nullptr;    // internal high-priority stream: far field (P2M ... L2L)
   cudaStream_t s_near = nullptr;   // internal low-priority stream: P2P, concurrent with the far field
   cudaEvent_t ev_fork = nullptr, ev_join_far = nullptr, ev_join_near = nullptr;
+  // leaf-level M2L on its own stream: it needs only the leaves' multipoles (P2M), so it runs
+  // beside M2M and the coarse-level M2L / L2L, and joins before the L2L into the leaf level
+  cudaStream_t s_leaf = nullptr;
+  cudaEvent_t ev_p2m = nullptr, ev_leaf = nullptr;
   // per tree point
   double2* pts_t = nullptr;  // kappa-scaled coordinates
   double* w_t = nullptr;
@@ -53,8 +58,9 @@ struct DevPlan {
   std::vector<DevBatch> m2m, l2l;
   // M2L
   int m2l_targets = 0;
+  int m2l_leaf_targets = 0;       // the first m2l_leaf_targets targets are at the deepest level
   int m2l_grid = 1;               // persistent CTAs (SMs x resident CTAs per SM)
-  int* m2l_ticket = nullptr;      // work counter, reset per matvec
+  int* m2l_ticket = nullptr;      // work counters (leaf-level part, rest), reset per matvec
   int64_t* m2l_loc_off = nullptr;
   int32_t* m2l_rows = nullptr;
   int64_t* m2l_stream_ptr = nullptr;  // per target: its source stream in m2l_stream_idx

@@ -67,7 +67,10 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ perm, const
 // c = lane + 32 k (k < kTCK) into registers, then each row is one coalesced pass over the
 // row (all 32 lanes busy) and a warp reduction.  Items wider than 32 kTCK columns are handled
 // in column blocks.  HBM-bound: every operator element is read once per matvec.
-constexpr int kTCK = 8;
+#ifndef DAFMM_TCK
+#define DAFMM_TCK 8
+#endif
+constexpr int kTCK = DAFMM_TCK;  // source columns per lane per pass (32 kTCK columns per pass)
 #ifndef DAFMM_TRB
 #define DAFMM_TRB 1  // measured: 1 row per step is fastest (profiles/README.md, r34)
 #endif
@@ -542,6 +545,9 @@ constexpr int kMSThreads = kMSConsumers + 32;  // + one producer warp (one elect
 #endif
 #ifndef DAFMM_MS_COLS
 #define DAFMM_MS_COLS 512
+#endif
+#ifndef DAFMM_LEAF_SPLIT
+#define DAFMM_LEAF_SPLIT 0  // 1: the deepest level's M2L on its own stream from the end of P2M
 #endif
 #ifndef DAFMM_NEAR_HIGH
 #define DAFMM_NEAR_HIGH 0  // 1: the near-field stream gets the high priority instead of the far field
@@ -1217,6 +1223,7 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   d.l2l.assign(pk.l2l.size(), DevBatch());
   for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err);
   d.m2l_targets = (int)pk.m2l_loc_off.size();
+  d.m2l_leaf_targets = pk.m2l_leaf_targets;
   ok = ok && upload(d, &d.m2l_loc_off, pk.m2l_loc_off, err) && upload(d, &d.m2l_rows, pk.m2l_rows, err) &&
        upload(d, &d.m2l_stream_ptr, pk.m2l_stream_ptr, err) && upload(d, &d.m2l_stream_idx, pk.m2l_stream_idx, err) &&
        upload(d, &d.m2l_item_ptr, pk.m2l_item_ptr, err) &&
@@ -1284,22 +1291,26 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
           "far stream") &&
        ck(cudaStreamCreateWithPriority(&d.s_near, cudaStreamNonBlocking, DAFMM_NEAR_HIGH ? prio_hi : prio_lo), err,
           "near stream") &&
+       ck(cudaStreamCreateWithPriority(&d.s_leaf, cudaStreamNonBlocking, DAFMM_NEAR_HIGH ? prio_lo : prio_hi), err,
+          "leaf M2L stream") &&
+       ck(cudaEventCreateWithFlags(&d.ev_p2m, cudaEventDisableTiming), err, "P2M event") &&
+       ck(cudaEventCreateWithFlags(&d.ev_leaf, cudaEventDisableTiming), err, "leaf M2L event") &&
        ck(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming), err, "fork event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_far, cudaEventDisableTiming), err, "join event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_near, cudaEventDisableTiming), err, "join event") &&
-       alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 1, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
+       alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 2, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
        alloc(d, &d.loc, pk.n_loc, err) && alloc(d, &d.host_stage, 2 * plan.n, err);
   if (!ok) return DAFMM_ECUDA;
   return DAFMM_OK;
 }
 
 void free_plan(DevPlan& d) {
-  for (cudaEvent_t* e : {&d.ev_fork, &d.ev_join_far, &d.ev_join_near})
+  for (cudaEvent_t* e : {&d.ev_fork, &d.ev_join_far, &d.ev_join_near, &d.ev_p2m, &d.ev_leaf})
     if (*e) {
       cudaEventDestroy(*e);
       *e = nullptr;
     }
-  for (cudaStream_t* st : {&d.s_far, &d.s_near})
+  for (cudaStream_t* st : {&d.s_far, &d.s_near, &d.s_leaf})
     if (*st) {
       cudaStreamDestroy(*st);
       *st = nullptr;
@@ -1343,6 +1354,7 @@ int harvest_profile(DevPlan& d, std::string& err) {
       !el(EV_JOIN, EV_END, t[6]) || !el(EV_FORK, EV_NEAR1, near_end) || !el(EV_FORK, EV_FAR_END, far_end))
     return DAFMM_ECUDA;
   t[7] = std::max(near_end, far_end);
+  if (!el(EV_LEAF0, EV_LEAF1, t[8])) return DAFMM_ECUDA;
   for (int p = 0; p < kNumPasses; ++p) d.prof_ms[p] += t[p];
   ++d.prof_count;
   d.prof_pending = false;
@@ -1377,29 +1389,53 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   if (far) {
     cudaMemsetAsync(d.mult, 0, sizeof(double2) * d.n_mult, fs);
     cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, fs);
-    if (d.m2l_targets > 0 && !d.m2l_mat) cudaMemsetAsync(d.m2l_ticket, 0, sizeof(int), fs);
+    if (d.m2l_targets > 0 && !d.m2l_mat) cudaMemsetAsync(d.m2l_ticket, 0, 2 * sizeof(int), fs);
   }
   mark(EV_P2M, fs);
   if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0, fs);  // P2M
+  // M2L over targets [t0, t1) on stream st (ticket slot k for the on-the-fly kernel)
+  auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
+    if (t1 <= t0) return;
+    if (d.m2l_mat) {  // from the stored blocks
+      m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, st>>>(
+          t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
+          d.m2l_mat, d.mult, d.loc);
+    } else {  // kernel entries on the fly, persistent CTAs
+      m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, st>>>(t1 - t0, d.m2l_ticket + k, d.m2l_loc_off + t0, d.m2l_rows + t0,
+                                                      d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_item_ptr + t0,
+                                                      d.m2l_item_code, d.m2l_item_begin, d.m2l_item_end, d.ti_xy,
+                                                      d.so_xy, d.mult, d.loc);
+    }
+    ++d.launches;
+  };
+  // DAFMM_LEAF_SPLIT: the deepest level's M2L needs only the leaves' multipoles, so it can run
+  // on its own stream beside M2M and the coarser M2L / L2L, joining before the L2L into the
+  // deepest level (the only other kernel touching those local expansions).  Measured slower
+  // with stored blocks at C4 (4.18 vs 3.71 ms: two M2L launches crowd the P2P; profiles/README.md),
+  // so it is off by default.
+  const int nleaf = (DAFMM_LEAF_SPLIT && far && fork && d.l2l.size() > 0) ? d.m2l_leaf_targets : 0;
+  if (nleaf > 0) {
+    cudaEventRecord(d.ev_p2m, fs);
+    cudaStreamWaitEvent(d.s_leaf, d.ev_p2m, 0);
+    mark(EV_LEAF0, d.s_leaf);
+    m2l(0, nleaf, 0, d.s_leaf);
+    mark(EV_LEAF1, d.s_leaf);
+    cudaEventRecord(d.ev_leaf, d.s_leaf);
+  } else {
+    mark(EV_LEAF0, fs);
+    mark(EV_LEAF1, fs);
+  }
   mark(EV_M2M, fs);
   if (far)
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
   mark(EV_M2L, fs);
-  if (far && d.m2l_targets > 0 && d.m2l_mat) {  // M2L from the stored blocks
-    m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, fs>>>(d.m2l_targets, d.m2l_loc_off,
-                                                               d.m2l_rows, d.m2l_stream_ptr, d.m2l_stream_idx,
-                                                               d.m2l_mat_off, d.m2l_mat, d.mult, d.loc);
-    ++d.launches;
-  } else if (far && d.m2l_targets > 0) {  // M2L, kernel entries on the fly, persistent CTAs
-    m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, fs>>>(d.m2l_targets, d.m2l_ticket, d.m2l_loc_off, d.m2l_rows,
-                                                    d.m2l_stream_ptr, d.m2l_stream_idx, d.m2l_item_ptr, d.m2l_item_code,
-                                                    d.m2l_item_begin, d.m2l_item_end, d.ti_xy, d.so_xy,
-                                                    d.mult, d.loc);
-    ++d.launches;
-  }
+  if (far) m2l(nleaf, d.m2l_targets, 1, fs);  // M2L: all (remaining) levels
   mark(EV_L2L, fs);
   if (far)
-    for (auto& b : d.l2l) d.launches += launch_translate(d, b, d.loc, d.loc, 1, fs);  // L2L
+    for (size_t i = 0; i < d.l2l.size(); ++i) {  // L2L
+      if (nleaf > 0 && i + 1 == d.l2l.size()) cudaStreamWaitEvent(fs, d.ev_leaf, 0);
+      d.launches += launch_translate(d, d.l2l[i], d.loc, d.loc, 1, fs);
+    }
   mark(EV_FAR_END, fs);
   mark(EV_NEAR0, ns);
   if (near) {  // P2P

@@ -102,6 +102,7 @@ struct Packed {
   std::vector<Batch> m2m;            // per parent level, processed from fine to coarse
   std::vector<Batch> l2l;            // per parent level, processed from coarse to fine
   // M2L: target nodes with source node CSR
+  int m2l_leaf_targets = 0;          // targets [0, m2l_leaf_targets) are at the deepest level L
   std::vector<int64_t> m2l_loc_off;  // per target
   std::vector<int32_t> m2l_rows;     // r_i per target
   std::vector<int32_t> m2l_src_ptr;  // targets + 1

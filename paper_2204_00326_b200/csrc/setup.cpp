@@ -856,7 +856,15 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
   }
   std::vector<size_t> torder(tg.size());
   std::iota(torder.begin(), torder.end(), 0);
-  std::stable_sort(torder.begin(), torder.end(), [&](size_t a, size_t b) { return tcost[a] > tcost[b]; });
+  // the deepest level's targets first (their M2L needs only the leaves' multipoles and runs
+  // beside M2M), each part in order of decreasing work
+  std::stable_sort(torder.begin(), torder.end(), [&](size_t a, size_t b) {
+    const bool la = tg[a].level == L, lb = tg[b].level == L;
+    if (la != lb) return la;
+    return tcost[a] > tcost[b];
+  });
+  pk.m2l_leaf_targets = 0;
+  for (auto& t : tg) pk.m2l_leaf_targets += t.level == L ? 1 : 0;
   pk.m2l_src_ptr.push_back(0);
   pk.m2l_item_ptr.push_back(0);
   pk.m2l_stream_ptr.push_back(0);
