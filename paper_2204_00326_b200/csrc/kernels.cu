@@ -68,11 +68,11 @@ __global__ void gather_kernel(int64_t n, const int32_t* __restrict__ perm, const
 // row (all 32 lanes busy) and a warp reduction.  Items wider than 32 kTCK columns are handled
 // in column blocks.  HBM-bound: every operator element is read once per matvec.
 #ifndef DAFMM_TCK
-#define DAFMM_TCK 8
+#define DAFMM_TCK 4
 #endif
 constexpr int kTCK = DAFMM_TCK;  // source columns per lane per pass (32 kTCK columns per pass)
 #ifndef DAFMM_TRB
-#define DAFMM_TRB 1  // measured: 1 row per step is fastest (profiles/README.md, r34)
+#define DAFMM_TRB 2  // with DAFMM_TCK 4: measured best (profiles/README.md, r34 and r36)
 #endif
 constexpr int kTRB = DAFMM_TRB;  // rows per step in translate_kernel
 __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
