@@ -85,6 +85,13 @@ struct DevPlan {
   int32_t* leaf_rank = nullptr;
   int64_t* leaf_U_off = nullptr;
   int32_t* leaf_band = nullptr;
+  // symmetric near field (Packed::p2p_sym): slots of the column sums, two halves of slot_total
+  int p2p_sym = 0;
+  int64_t slot_total = 0;
+  int64_t* leaf_slot_base = nullptr;
+  int32_t* in_ptr = nullptr;
+  int64_t* in_off = nullptr;
+  double2* slots = nullptr;
   // scratch
   double2* x_t = nullptr;
   double2* v_t = nullptr;

@@ -302,10 +302,46 @@ struct RunStager {
 };
 
 // Items of an M2L target: band code and stream range, from the packed plan.
+// COLS (symmetric near field): the block's column sums sum_t H0(|x_t - s_q|) v_t over the
+// warp's 32 targets are written to cs.slots[cs.base + pos + q] (one warp-half of the slots).
+struct ColSink {
+  double2* slots;
+  int64_t base;
+  double2 vt;  // this thread's target weight w_t x_t
+};
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+// Reduce N values per lane (N a power of 2, <= 32) over the warp's 32 lanes, reduce-scatter
+// style: each halving step exchanges half of the values, N - 1 shuffles in all (instead of
+// 5 N).  Returns the full sum of value index (lane >> (5 - log2 N)) & (N - 1)... for N = 16:
+// value (lane >> 1), held by lanes 2k and 2k + 1.
+template <int N>
+__device__ __forceinline__ double warp_reduce_scatter(double* v) {
+  const int lane = threadIdx.x & 31;
+  int o = 16;
+#pragma unroll
+  for (int n = N; n > 1; n >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < n / 2; ++i) {
+      const double send = up ? v[i] : v[i + n / 2];
+      const double keep = up ? v[i + n / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double r = v[0];
+#pragma unroll
+  for (; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
 struct M2LItems {
   static constexpr int kTB = kTBM2L;
   static constexpr bool kGuarded = false;  // no i == j pairs
   static constexpr bool kNearOnly = false;
+  static constexpr bool kCols = false;
   const int4* it_;  // (code, pb, pe, -) in shared memory: read once per chunk by every thread
   int is, ie;
   __device__ __forceinline__ int code(int i) const { return it_[i].x; }
@@ -318,7 +354,14 @@ struct NearItems {
   static constexpr int kTB = kTBP2P;
   static constexpr bool kGuarded = true;   // item 0 holds the i == j pairs
   static constexpr bool kNearOnly = true;  // bands: near-7, near-8, near-12 or generic
+  static constexpr bool kCols = true;      // item 1 of a symmetric near field writes column sums
   int band, own, total, is, ie;
+  int sym;
+  double2* slots;     // this warp-half's slots
+  int64_t slot_base;  // slot of stream position `own`
+  double2 vt;
+  __device__ __forceinline__ bool cols(int i) const { return sym && i == 1; }
+  __device__ __forceinline__ ColSink sink(int c0) const { return ColSink{slots, slot_base - own + c0, vt}; }
   __device__ __forceinline__ int code(int) const { return band; }
   __device__ __forceinline__ bool guard(int i) const { return i == 0; }
   __device__ __forceinline__ int pb(int i) const { return i == 0 ? 0 : own; }
@@ -340,9 +383,9 @@ __device__ __forceinline__ void eval_band(const double* z2, double* re, double* 
 // MASK: only the first `valid` sources count (tail block); GUARD: the pair i == j (own leaf of
 // the near field; its value is the self term D_i) is excluded.  Excluded lanes get a safe z^2
 // and a zero weight so the evaluator stays branch-free.
-template <int CODE, int TB, bool GUARD, bool MASK>
+template <int CODE, int TB, bool GUARD, bool MASK, bool COLS = false>
 __device__ __forceinline__ void consume_block(const double4* p, int stride, int valid, double2 xt, double& ar, double& ai,
-                                              const PolyTable& T, const FarBand* band) {
+                                              const PolyTable& T, const FarBand* band, const ColSink& cs = {}, int pos = 0) {
   if constexpr (CODE == kBandGeneric) {  // rare (straddling segments): one lane at a time
 #pragma unroll 1
     for (int q = 0; q < (MASK ? valid : TB); ++q) {
@@ -354,6 +397,11 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
       h0_generic_vec<1>(&d2, &hr, &hi, T);
       ar = fma(hr, sv.z, fma(-hi, sv.w, ar));
       ai = fma(hr, sv.w, fma(hi, sv.z, ai));
+      if constexpr (COLS) {
+        const double cr = warp_sum(fma(hr, cs.vt.x, -hi * cs.vt.y));
+        const double ci = warp_sum(fma(hr, cs.vt.y, hi * cs.vt.x));
+        if ((threadIdx.x & 31) == 0) cs.slots[cs.base + pos + q] = make_double2(cr, ci);
+      }
     }
   } else {
   double z2[TB], hr[TB], hi[TB];
@@ -380,33 +428,48 @@ __device__ __forceinline__ void consume_block(const double4* p, int stride, int 
     ar = fma(hr[q], v.x, fma(-hi[q], v.y, ar));
     ai = fma(hr[q], v.y, fma(hi[q], v.x, ai));
   }
+  if constexpr (COLS) {  // the pairs' other direction: column sums over the warp's targets
+    static_assert(2 * TB == 16, "the column reduce-scatter is written for 8 sources per block");
+    double c[2 * TB];
+#pragma unroll
+    for (int q = 0; q < TB; ++q) {
+      const bool u = !MASK || q < valid;
+      c[2 * q] = u ? fma(hr[q], cs.vt.x, -hi[q] * cs.vt.y) : 0.0;
+      c[2 * q + 1] = u ? fma(hr[q], cs.vt.y, hi[q] * cs.vt.x) : 0.0;
+    }
+    const double r = warp_reduce_scatter<2 * TB>(c);
+    const int lane = threadIdx.x & 31, idx = lane >> 1, q = idx >> 1;
+    if (!(lane & 1) && (!MASK || q < valid))
+      reinterpret_cast<double*>(cs.slots + cs.base + pos + q)[idx & 1] = r;
+  }
   }
 }
 
 // acc += sum_{j in [a, b)} H0(|xt - s_j|) v_j over staged sources (kappa-scaled coordinates).
 // The range is cut into blocks of kTB consecutive sources, dealt to the slices cyclically
 // (block k to slice k mod nsl); only the last block of the range can be partial (masked).
-template <int CODE, int TB, bool GUARD>
+template <int CODE, int TB, bool GUARD, bool COLS = false>
 __device__ __forceinline__ void consume(const double4* sb, int a, int b, double2 xt, int slice, int nsl, double& ar,
-                                        double& ai, const PolyTable& T, const FarBand* band) {
+                                        double& ai, const PolyTable& T, const FarBand* band, const ColSink& cs = {}) {
   const int n = b - a;
   const int full = n / TB;
   for (int k = slice; k < full; k += nsl)
-    consume_block<CODE, TB, GUARD, false>(sb + a + k * TB, 1, TB, xt, ar, ai, T, band);
+    consume_block<CODE, TB, GUARD, false, COLS>(sb + a + k * TB, 1, TB, xt, ar, ai, T, band, cs, a + k * TB);
   if ((n % TB) && slice == full % nsl)
-    consume_block<CODE, TB, GUARD, true>(sb + a + full * TB, 1, n % TB, xt, ar, ai, T, band);
+    consume_block<CODE, TB, GUARD, true, COLS>(sb + a + full * TB, 1, n % TB, xt, ar, ai, T, band, cs, a + full * TB);
 }
 
 // Dispatch a CTA-uniform band code.  NEAR_ONLY (the P2P stream): only the near bands and generic
 // occur, so no other band is instantiated (code size: the kernel stays in the i-cache).
-template <int TB, bool GUARD, bool NEAR_ONLY>
+template <int TB, bool GUARD, bool NEAR_ONLY, bool COLS = false>
 __device__ __forceinline__ void consume_code(int code, const double4* sb, int a, int b, double2 xt, int slice, int nsl,
-                                             double& ar, double& ai, const PolyTable& T, const FarBand* bands) {
+                                             double& ar, double& ai, const PolyTable& T, const FarBand* bands,
+                                             const ColSink& cs = {}) {
   if constexpr (NEAR_ONLY) {
-    if (code == kBandNear7) consume<kBandNear7, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
-    else if (code == kBandNear8) consume<kBandNear8, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
-    else if (code == kBandNear12) consume<kBandNear12, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
-    else consume<kBandGeneric, TB, GUARD>(sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+    if (code == kBandNear7) consume<kBandNear7, TB, GUARD, COLS>(sb, a, b, xt, slice, nsl, ar, ai, T, bands, cs);
+    else if (code == kBandNear8) consume<kBandNear8, TB, GUARD, COLS>(sb, a, b, xt, slice, nsl, ar, ai, T, bands, cs);
+    else if (code == kBandNear12) consume<kBandNear12, TB, GUARD, COLS>(sb, a, b, xt, slice, nsl, ar, ai, T, bands, cs);
+    else consume<kBandGeneric, TB, GUARD, COLS>(sb, a, b, xt, slice, nsl, ar, ai, T, bands, cs);
   } else {
     switch (code) {  // the M2L stream: choose_band(.., allow_near7 = false) never yields near-7
       case kBandNear8:
@@ -446,8 +509,19 @@ __device__ __forceinline__ void stream_accumulate(double4* buf, Stager& st, cons
         if (Items::kGuarded && items.guard(it))
           consume_code<Items::kTB, Items::kGuarded, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar,
                                                                       ai, T, bands);
-        else
-          consume_code<Items::kTB, false, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T, bands);
+        else {
+          bool done = false;
+          if constexpr (Items::kCols) {
+            if (items.cols(it)) {  // symmetric near field: the column sums too
+              consume_code<Items::kTB, false, Items::kNearOnly, true>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai,
+                                                                      T, bands, items.sink(c0));
+              done = true;
+            }
+          }
+          if (!done)
+            consume_code<Items::kTB, false, Items::kNearOnly>(items.code(it), sb, a, b, xt, slice, nsl, ar, ai, T,
+                                                              bands);
+        }
       }
     }
     c0 = c1;
@@ -870,7 +944,8 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
 __global__ void DAFMM_P2P_REGCAP p2p_kernel(
     const int32_t* __restrict__ leaf_begin, const int32_t* __restrict__ leaf_end, const int32_t* __restrict__ near_ptr,
     const int32_t* __restrict__ near_begin, const int32_t* __restrict__ near_end, const int32_t* __restrict__ leaf_band,
-    const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi) {
+    const double2* __restrict__ pts_t, const double2* __restrict__ v_t, double2* __restrict__ phi, int sym,
+    const int64_t* __restrict__ leaf_slot_base, double2* __restrict__ slots, int64_t slot_total) {
   __shared__ __align__(16) double4 buf[2 * kNearStage];
   __shared__ double2 red[kNearThreads];
   __shared__ PolyTable T;
@@ -880,7 +955,6 @@ __global__ void DAFMM_P2P_REGCAP p2p_kernel(
   const int ps = near_ptr[leaf], pe = near_ptr[leaf + 1];
   int total = 0;
   for (int e = ps; e < pe; ++e) total += near_end[e] - near_begin[e];
-  const NearItems items{leaf_band[leaf], pe > ps ? near_end[ps] - near_begin[ps] : 0, total, 0, 2};
   for (int t0 = 0; t0 < m; t0 += kNearThreads) {
     const int rc = min(kNearThreads, m - t0);
     const int nsl = kNearThreads / rc;
@@ -888,6 +962,11 @@ __global__ void DAFMM_P2P_REGCAP p2p_kernel(
     const int slice = threadIdx.x / rc;
     const bool active = slice < nsl;
     double2 xt = ld2(pts_t + tb + t0 + t);
+    // symmetric near field (every leaf has 32 or 64 points): slices are whole warps; warp
+    // (t / 32) of the slice writes its half of the slots
+    const NearItems items{leaf_band[leaf], pe > ps ? near_end[ps] - near_begin[ps] : 0, total, 0, 2, sym,
+                          slots + (sym ? (int64_t)(t >> 5) * slot_total : 0), sym ? leaf_slot_base[leaf] : 0,
+                          sym ? ld2(v_t + tb + t0 + t) : make_double2(0.0, 0.0)};
     double ar = 0.0, ai = 0.0;
     if (pe > ps) {
       RunStager st{near_begin, near_end, ps, 0, pe, pts_t, v_t};
@@ -917,7 +996,9 @@ __global__ void combine_kernel(const int32_t* __restrict__ leaf_begin, const int
                                const double2* __restrict__ loc, const double2* __restrict__ phi,
                                const double2* __restrict__ x_t, const double* __restrict__ qk2_t,
                                const double2* __restrict__ D_t, const int32_t* __restrict__ perm,
-                               double2* __restrict__ y, int kernel_mode, int do_near, int do_far_in) {
+                               double2* __restrict__ y, int kernel_mode, int do_near, int do_far_in,
+                               const int32_t* __restrict__ in_ptr, const int64_t* __restrict__ in_off,
+                               const double2* __restrict__ slots, int64_t slot_total) {
   const int leaf = blockIdx.x;
   const int tb = leaf_begin[leaf], m = leaf_end[leaf] - tb;
   const bool do_far = do_far_in && leaf_loc_off[leaf] >= 0;
@@ -927,6 +1008,12 @@ __global__ void combine_kernel(const int32_t* __restrict__ leaf_begin, const int
       const double2 p = phi[tb + tt];
       sr = p.x;
       si = p.y;
+      if (in_ptr)  // symmetric near field: the pairs evaluated by earlier leaves (both slot halves)
+        for (int k = in_ptr[leaf]; k < in_ptr[leaf + 1]; ++k) {
+          const double2 a = slots[in_off[k] + tt], b = slots[slot_total + in_off[k] + tt];
+          sr += a.x + b.x;
+          si += a.y + b.y;
+        }
     }
     if (do_far) {  // L2P: (U u)_t, U column-major m x r
       const int rk = leaf_rank[leaf];
@@ -1236,6 +1323,13 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
        upload(d, &d.near_end, pk.near_end, err) && upload(d, &d.leaf_loc_off, pk.leaf_loc_off, err) &&
        upload(d, &d.leaf_rank, pk.leaf_rank, err) && upload(d, &d.leaf_U_off, pk.leaf_U_off, err) &&
        upload(d, &d.leaf_band, pk.leaf_band, err);
+  d.p2p_sym = pk.p2p_sym;
+  d.slot_total = pk.slot_total;
+  if (ok && d.p2p_sym) {
+    ok = upload(d, &d.leaf_slot_base, pk.leaf_slot_base, err) && upload(d, &d.in_ptr, pk.in_ptr, err) &&
+         upload(d, &d.in_off, pk.in_off, err) && alloc(d, &d.slots, (size_t)(2 * d.slot_total), err) &&
+         ck(cudaMemset(d.slots, 0, sizeof(double2) * (size_t)(2 * d.slot_total)), err, "slots memset");
+  }
   if (ok && d.m2l_targets > 0 && plan.opt.m2l_store != 0) {  // stored M2L blocks
     std::vector<int64_t> moff(d.m2l_targets);
     int64_t tot = 0;
@@ -1440,7 +1534,8 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   mark(EV_NEAR0, ns);
   if (near) {  // P2P
     p2p_kernel<<<d.nleaves, kNearThreads, 0, ns>>>(d.leaf_begin, d.leaf_end, d.near_ptr, d.near_begin, d.near_end,
-                                                   d.leaf_band, d.pts_t, d.v_t, d.phi);
+                                                   d.leaf_band, d.pts_t, d.v_t, d.phi, d.p2p_sym,
+                                                   d.leaf_slot_base, d.slots, d.slot_total);
     ++d.launches;
   }
   mark(EV_NEAR1, ns);
@@ -1453,7 +1548,9 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   mark(EV_JOIN, s);
   combine_kernel<<<d.nleaves, kCombineThreads, 0, s>>>(d.leaf_begin, d.leaf_end, d.leaf_loc_off, d.leaf_rank,
                                                         d.leaf_U_off, d.ops, d.loc, d.phi, d.x_t, d.qk2_t, d.D_t,
-                                                        d.perm, y, d.kernel_mode, near ? 1 : 0, far ? 1 : 0);
+                                                        d.perm, y, d.kernel_mode, near ? 1 : 0, far ? 1 : 0,
+                                                        d.p2p_sym ? d.in_ptr : nullptr, d.in_off, d.slots,
+                                                        d.slot_total);
   ++d.launches;
   mark(EV_END, s);
   if (d.prof) d.prof_pending = true;

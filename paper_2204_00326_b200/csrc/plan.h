@@ -125,6 +125,14 @@ struct Packed {
   std::vector<int32_t> leaf_rank;             // r_i
   std::vector<int64_t> leaf_U_off;
   std::vector<int32_t> leaf_band;             // P2P band code: near if every pair has z <= 8
+  // symmetric near field (p2p_sym): each leaf streams only its own leaf and the ranges after it
+  // in tree order; the column sums of those pairs (the contributions to the later points) go
+  // to slots (two halves: one per warp of a 64-target slice), gathered per leaf at combine
+  int p2p_sym = 0;
+  std::vector<int64_t> leaf_slot_base;        // per leaf: slot of its first streamed non-own source
+  int64_t slot_total = 0;
+  std::vector<int32_t> in_ptr;                // leaves + 1: slots holding contributions to the leaf
+  std::vector<int64_t> in_off;                // slot of the leaf's first point in each
   std::vector<int64_t> p2p_band_entries = std::vector<int64_t>(kNumBandCodes, 0);
   int max_leaf = 0;
   // statistics

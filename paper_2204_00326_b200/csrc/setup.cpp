@@ -920,6 +920,18 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
   };
   pk.near_ptr.push_back(0);
   pk.max_leaf = 0;
+  // symmetric near field when every leaf has 32 or 64 points: the pairs between
+  // two different leaves are evaluated once, by the leaf that comes first in tree order
+  pk.p2p_sym = 1;
+  for (int l = 0; l <= L; ++l)
+    for (const Box& B : P.levels[l].boxes)
+      if (B.leaf && B.end - B.begin != 64 && B.end - B.begin != 32) pk.p2p_sym = 0;
+  struct SlotRange {
+    int32_t r0, r1;
+    int64_t slot;
+  };
+  std::vector<SlotRange> slot_ranges;
+  pk.slot_total = 0;
   for (int l = 0; l <= L; ++l) {
     const Level& lv = P.levels[l];
     for (size_t b = 0; b < lv.boxes.size(); ++b) {
@@ -934,10 +946,16 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       double pb[4], qb[4], zmax = 0.0;
       bbox(B, pb);
       int64_t pairs = 0;
+      pk.leaf_slot_base.push_back(pk.slot_total);
       for (const Box* A : src) {
+        pairs += (int64_t)(B.end - B.begin) * (A->end - A->begin);
+        if (pk.p2p_sym && A != &B) {
+          if (A->end <= B.begin) continue;  // evaluated by the earlier leaves' CTAs (slots)
+          slot_ranges.push_back({A->begin, A->end, pk.slot_total});
+          pk.slot_total += A->end - A->begin;
+        }
         pk.near_begin.push_back(A->begin);
         pk.near_end.push_back(A->end);
-        pairs += (int64_t)(B.end - B.begin) * (A->end - A->begin);
         bbox(*A, qb);
         double dx = std::max(pb[2] - qb[0], qb[2] - pb[0]);
         double dy = std::max(pb[3] - qb[1], qb[3] - pb[1]);
@@ -960,6 +978,26 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
         pk.leaf_rank.push_back(0);
         pk.leaf_U_off.push_back(0);
       }
+    }
+  }
+  // slots -> leaves: every slot range covers whole leaves (near ranges are boxes)
+  pk.in_ptr.assign(1, 0);
+  pk.in_off.clear();
+  if (pk.p2p_sym) {
+    const int nl = (int)pk.leaf_begin.size();
+    std::vector<int> by_begin(nl);
+    std::iota(by_begin.begin(), by_begin.end(), 0);
+    std::sort(by_begin.begin(), by_begin.end(), [&](int a, int b) { return pk.leaf_begin[a] < pk.leaf_begin[b]; });
+    std::vector<std::vector<int64_t>> in(nl);
+    for (const SlotRange& sr : slot_ranges) {
+      auto it = std::lower_bound(by_begin.begin(), by_begin.end(), sr.r0,
+                                 [&](int li, int32_t v) { return pk.leaf_begin[li] < v; });
+      for (; it != by_begin.end() && pk.leaf_begin[*it] < sr.r1; ++it)
+        in[*it].push_back(sr.slot + (pk.leaf_begin[*it] - sr.r0));
+    }
+    for (int li = 0; li < nl; ++li) {
+      for (int64_t o : in[li]) pk.in_off.push_back(o);
+      pk.in_ptr.push_back((int32_t)pk.in_off.size());
     }
   }
   // ---- operator blocks (column-major), in parallel ----
