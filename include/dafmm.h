@@ -99,6 +99,8 @@ typedef struct {
   int64_t m2l_stream_len;       /* source pivots over all M2L target nodes (multipole gathers per matvec) */
   int64_t n_loc;                /* local-expansion coefficients (M2L outputs) */
   int64_t gmres_reorth;         /* second Gram-Schmidt passes (CGS2) in the last ls_gmres_solve */
+  int32_t p2p_symmetric;        /* 1: near-field pairs of different leaves evaluated once (every leaf
+                                   has 32 or 64 points); 0: each leaf evaluates all its pairs */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);

@@ -18,6 +18,7 @@ struct dafmm_plan {
   dafmm::DevPlan dev;
   int64_t operator_bytes = 0;
   int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0, m2l_stream_len = 0, n_loc = 0;
+  int p2p_sym = 0;
   std::vector<int64_t> m2l_band, p2p_band;
 };
 
@@ -96,6 +97,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     h->m2l_pairs = pk.m2l_pairs;
     h->m2l_stream_len = (int64_t)pk.m2l_stream_idx.size();
     h->n_loc = pk.n_loc;
+    h->p2p_sym = pk.p2p_sym;
     h->m2l_band = pk.m2l_band_entries;
     h->p2p_band = pk.p2p_band_entries;
   } catch (const std::bad_alloc&) {
@@ -222,6 +224,7 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->m2l_stream_len = h->m2l_stream_len;
   out->n_loc = h->n_loc;
   out->gmres_reorth = h->dev.gm_reorth;
+  out->p2p_symmetric = h->p2p_sym;
   for (size_t b = 0; b < h->m2l_band.size() && b < 48; ++b) out->m2l_band_entries[b] = h->m2l_band[b];
   for (size_t b = 0; b < h->p2p_band.size() && b < 48; ++b) out->p2p_band_entries[b] = h->p2p_band[b];
   return DAFMM_OK;

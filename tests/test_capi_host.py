@@ -150,3 +150,16 @@ def test_m2l_store_option_validated():
     op = binding.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1e-8, host_only=1, m2l_store=1)
     st = op.stats()
     assert st["m2l_stored"] == 0 and st["m2l_store_bytes"] == 0  # host-only plan: nothing on a device
+
+
+def test_symmetric_near_field_flag():
+    """The symmetric near field is used exactly when every leaf has 32 or 64 points (the P2P
+    CTA's slices are then whole warps); ragged leaves fall back to the one-sided near field."""
+    from paper_2204_00326_b200 import binding
+    P = make_problem("c1")
+    op = binding.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, 1e-8, host_only=1)
+    assert op.stats()["p2p_symmetric"] == 1
+    rng = np.random.default_rng(7)
+    pts = rng.uniform(-1, 1, size=(3000, 2))
+    op = binding.DAFMM(pts, np.full(3000, 4.0 / 3000), np.ones(3000), 12.0, 64, 1e-8, host_only=1)
+    assert op.stats()["p2p_symmetric"] == 0

@@ -54,6 +54,7 @@ def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     P = make_problem(name, n=n, kappa=kappa)
     op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=1)
     assert op.stats()["m2l_stored"] == 1
+    assert op.stats()["p2p_symmetric"] == 1  # 64-point leaves: the symmetric near field
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
     x = P["x"]
     y_gpu = _gpu_matvec(op, x)
@@ -115,6 +116,7 @@ def test_gpu_ragged_points_and_potential_mode(tmp_path):
     q = 1.0 + 0.5 * np.cos(3 * pts[:, 0])
     P = dict(points=pts, weights=w, q=q, kappa=12.0, nca_tol=1e-8, x=np.exp(1j * rng.uniform(0, 6.3, 3000)))
     op = _prod().DAFMM(pts, w, q, 12.0, 64, 1e-8)
+    assert op.stats()["p2p_symmetric"] == 0  # ragged leaves: every leaf evaluates all its pairs
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
     y = _gpu_matvec(op, P["x"])
     assert _rel(y - P["x"], nca.matvec(P["x"]) - P["x"]) <= 1e-11
