@@ -34,11 +34,11 @@ def _gpu_matvec(op, x, mask=3):
     return yd.cpu().numpy()
 
 
-def _oracle_on_product_plan(P, op, tmp_path):
+def _oracle_on_product_plan(P, op, tmp_path, leaf_size=64):
     op.export_plan(tmp_path / "plan")
     plan = load_plan(tmp_path / "plan")
     prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
-    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    tree = Tree(P["points"], P["weights"], P["kappa"], leaf_size)
     lists = Lists(tree)
     compare_lists(plan, tree, lists)
     piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
@@ -54,7 +54,8 @@ def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     P = make_problem(name, n=n, kappa=kappa)
     op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=1)
     assert op.stats()["m2l_stored"] == 1
-    assert op.stats()["p2p_symmetric"] == 1  # 64-point leaves: the symmetric near field
+    # 64-point leaves take the symmetric near field; the 40 x 40 grid has ragged leaves
+    assert op.stats()["p2p_symmetric"] == (0 if n == 40 else 1)
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
     x = P["x"]
     y_gpu = _gpu_matvec(op, x)
@@ -146,3 +147,25 @@ def test_gpu_invalid_inputs():
         prod.DAFMM(bad, P["weights"], P["q"], 5.0, 64, 1e-8)
     with pytest.raises(prod.DAFMMError):
         prod.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1.5)
+
+
+def test_gpu_symmetric_near_field_32_point_leaves(tmp_path):
+    """The symmetric near field with one warp per slice: a 64 x 32 lattice whose leaves (leaf size
+    32) hold 8 x 4 points each."""
+    xs = -1.0 + (np.arange(64) + 0.5) * (2.0 / 64)
+    ys = -1.0 + (np.arange(32) + 0.5) * (2.0 / 32)
+    pts = np.stack(np.meshgrid(xs, ys, indexing="ij"), axis=-1).reshape(-1, 2)
+    n = pts.shape[0]
+    w = np.full(n, 4.0 / n)
+    q = 1.5 * np.exp(-4.0 * (pts ** 2).sum(1))
+    x = np.exp(1j * np.random.default_rng(3).uniform(0, 2 * np.pi, n))
+    P = dict(points=pts, weights=w, q=q, kappa=8.0, nca_tol=1e-8, x=x)
+    op = _prod().DAFMM(pts, w, q, 8.0, 32, 1e-8)
+    assert op.stats()["p2p_symmetric"] == 1
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path, leaf_size=32)
+    y = _gpu_matvec(op, x)
+    assert _rel(y - x, nca.matvec(x) - x) <= 1e-11
+    yd = oracle.dense_matvec(prob, x)
+    assert _rel(y - x, yd - x) <= 10 * 1e-8
+    near = _gpu_matvec(op, x, 1)
+    assert _rel(near - x, nca.matvec(x, parts=("near",)) - x) <= 1e-12
