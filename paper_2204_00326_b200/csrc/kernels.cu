@@ -1085,7 +1085,10 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* sh) {
 // part[bx * stride + i] = sum over block bx's slice of conj(V_i) w for the kMD vectors
 // i = blockIdx.y * kMD + g of this block: w is read once per group of kMD basis vectors and
 // each thread keeps kMD complex partial sums (one pass, no per-vector barriers).
-constexpr int kMD = 8;
+#ifndef DAFMM_KMD
+#define DAFMM_KMD 4  // measured: C3 GMRES(200) 2.43 s at 8, 2.26 s at 4, 2.24 s at 2, 2.63 s at 16
+#endif
+constexpr int kMD = DAFMM_KMD;  // basis vectors per multi-dot block row
 #ifndef DAFMM_MD_BLOCKS
 #define DAFMM_MD_BLOCKS 148
 #endif
