@@ -1160,14 +1160,30 @@ __global__ void combine_kernel(int64_t n, int k, const double2* __restrict__ V, 
   for (int i = threadIdx.x; i < k; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    double2 acc = w[e];
-    for (int i = 0; i < k; ++i) {
-      double2 v = ld2(V + (int64_t)i * n + e);
-      double2 c = make_double2(sign * hs[i].x, sign * hs[i].y);
+    double2 acc = w[e], acc1 = make_double2(0.0, 0.0);
+    int i = 0;
+    // 4 basis vectors per step, two accumulators: 4 loads in flight, half-length FMA chains
+    for (; i + 4 <= k; i += 4) {
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = ld2(V + (int64_t)(i + q) * n + e);
+#pragma unroll
+      for (int q = 0; q < 4; q += 2) {
+        const double2 c0 = make_double2(sign * hs[i + q].x, sign * hs[i + q].y);
+        const double2 c1 = make_double2(sign * hs[i + q + 1].x, sign * hs[i + q + 1].y);
+        acc.x = fma(c0.x, v[q].x, fma(-c0.y, v[q].y, acc.x));
+        acc.y = fma(c0.x, v[q].y, fma(c0.y, v[q].x, acc.y));
+        acc1.x = fma(c1.x, v[q + 1].x, fma(-c1.y, v[q + 1].y, acc1.x));
+        acc1.y = fma(c1.x, v[q + 1].y, fma(c1.y, v[q + 1].x, acc1.y));
+      }
+    }
+    for (; i < k; ++i) {
+      const double2 v = ld2(V + (int64_t)i * n + e);
+      const double2 c = make_double2(sign * hs[i].x, sign * hs[i].y);
       acc.x = fma(c.x, v.x, fma(-c.y, v.y, acc.x));
       acc.y = fma(c.x, v.y, fma(c.y, v.x, acc.y));
     }
-    w[e] = acc;
+    w[e] = make_double2(acc.x + acc1.x, acc.y + acc1.y);
   }
 }
 
