@@ -632,7 +632,10 @@ constexpr int kMSThreads = kMSConsumers + 32;  // + one producer warp (one elect
 #ifndef DAFMM_MS_MINB
 #define DAFMM_MS_MINB 6  // register cap (<= 64): room for P2P CTAs beside the stored-M2L CTAs
 #endif
-constexpr int kMSStageE = 1024;                 // entries per TMA bulk copy (16 KB)
+#ifndef DAFMM_MS_STAGE_E
+#define DAFMM_MS_STAGE_E 1024
+#endif
+constexpr int kMSStageE = DAFMM_MS_STAGE_E;     // entries per TMA bulk copy (16 KB)
 constexpr int kMSStages = DAFMM_MS_STAGES;      // ring depth (x 16 KB in flight per CTA)
 constexpr int kMSCols = DAFMM_MS_COLS;          // source columns per work unit (multipoles double-buffered)
 constexpr int kMaxStoredRows = kMSConsumers;
