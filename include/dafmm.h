@@ -75,6 +75,14 @@ typedef struct {
                           node has more than 128 pivots; -1 (default) auto: store when the blocks
                           take at most half of the free device memory and every node has at most
                           128 pivots, else on the fly.  dafmm_stats reports the choice. */
+  int hfr_parent_search; /* NCA search sets of a directional node (B, l) whose parent is also
+                          directional (P:624-631 use IL(B, l) only): 0 (default) as the paper writes
+                          them; 1 also take the children, in the matching child cones, of the
+                          parent's IL in the two parent cones nesting in l (reading R7b).  Needed on
+                          irregular domains where IL(B, l) spans fewer directions than the parent's
+                          far field arriving through the directional L2L (L-shaped random points:
+                          1.6e-4 vs dense with 0, 7.5e-9 with 1); on the uniform configs it costs
+                          2x the ACA setup and 1.5% more M2L work for no accuracy gain. */
 } dafmm_options;
 
 /* Statistics of a plan (sizes, ranks, setup times). */
@@ -133,17 +141,24 @@ int dafmm_matvec_parts(dafmm_handle h, const void* x, void* y, unsigned mask);
  * synchronises the handle's stream before returning (the end-to-end path of bench.py). */
 int dafmm_matvec_host(dafmm_handle h, const void* x_host, void* y_host);
 
-/* Restarted GMRES(m) (reading R14: zero initial guess, m = restart (<= 0: 50),
- * classical Gram-Schmidt with re-orthogonalisation on the device) for A psi = f with the
- * DAFMM product.  f, psi: DEVICE pointers (n complex128, caller order; psi is overwritten).
- * Stops when the implicit relative residual <= tol or after maxit inner iterations, then
- * recomputes the true relative residual ||f - A psi|| / ||f|| into *relres_out.
+/* Restarted GMRES(m) (reading R14: zero initial guess, m = restart (<= 0: 50,
+ * at most 255), classical Gram-Schmidt with re-orthogonalisation on the device) for A psi = f
+ * with the DAFMM product.  f, psi: DEVICE pointers (n complex128, caller order; psi is
+ * overwritten).  A restart cycle ends when its implicit (Givens) relative residual <= tol or
+ * at maxit inner iterations; the true relative residual ||f - A psi|| / ||f|| is recomputed at
+ * every restart and decides convergence (a cycle whose implicit residual met tol while the true
+ * one did not is followed by another).  *relres_out receives the final true relative residual.
  * history (nullable, host, maxit + 1 doubles) receives the implicit residual per iteration.
- * Synchronous.  Returns DAFMM_OK, DAFMM_NOT_CONVERGED, or an error code. */
+ * The first call (and a call with a different restart) allocates the device workspace:
+ * (restart + 3) n complex128 plus small buffers; later calls allocate nothing.
+ * Synchronous.  Returns DAFMM_OK (true relres <= tol), DAFMM_NOT_CONVERGED (maxit reached),
+ * or an error code (DAFMM_EINVAL: tol <= 0, maxit < 1, restart > 255, f == psi). */
 int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int maxit, int restart, int* iters_out,
                    double* relres_out, double* history);
 
-/* Use stream s (a cudaStream_t) for all later device work of the handle. */
+/* Use stream s (a cudaStream_t) for all later device work of the handle.  Work already enqueued
+ * on the previous stream is ordered before any later work on s (the handle's scratch buffers
+ * are shared): s waits on an event recorded on the previous stream. */
 int dafmm_set_stream(dafmm_handle h, void* stream);
 
 /* Statistics of the plan (sizes, ranks, setup wall times).  Host only; never fails on a

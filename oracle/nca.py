@@ -21,11 +21,19 @@ from .core import K_block
 # --------------------------------------------------------------------------------------------
 # Partially pivoted ACA (stopping rule of [Rjasanow 2002] cited at P:816) — R10.
 # --------------------------------------------------------------------------------------------
+# R10: a residual row at or below this multiple of its original largest entry is numerically in
+# the span of the earlier terms; pivoting on it gives a singular cross matrix (measured on 2 x 2
+# point leaves: relative error 1.8e-4 instead of 8e-9, independent of eps; R10)
+ZERO_ROW_RTOL = 1e3 * np.finfo(np.float64).eps
+
+
 def aca(row_fn, col_fn, m, n, eps, max_rank=200):
     """Return (row_positions, col_positions) chosen by partially pivoted ACA on an m x n matrix.
 
     R10: first row = position 0; column pivot = argmax |residual row| over unused columns
-    (first maximum); a zero residual row is marked used and the next unused row (smallest
+    (first maximum); a zero residual row -- one whose largest residual is at rounding level,
+    at most 1e3 machine-eps times the largest entry of the row before the subtraction (the row
+    lies in the span of the earlier terms) -- is marked used and the next unused row (smallest
     position) is tried; next row = argmax |u_k| over unused rows; stop when the new term has
     ||u_k|| ||v_k|| <= eps ||S_k||_F (||S_k||_F^2 updated incrementally) and keep the k-1
     earlier pivots — the term estimates the error of the rank-(k-1) skeleton, and a pivot whose
@@ -38,14 +46,15 @@ def aca(row_fn, col_fn, m, n, eps, max_rank=200):
     norm2 = 0.0
     i = 0
     while len(rows) < rank_cap and m > 0 and n > 0:
-        r = row_fn(i).copy()
+        row = row_fn(i)
+        r = row.copy()
         for l in range(len(us)):
             r -= us[l][i] * vs[l]
         used_r[i] = True
         mag = np.abs(r)
         mag[used_c] = -1.0
         j = int(np.argmax(mag))
-        if not mag[j] > 0.0:
+        if not mag[j] > ZERO_ROW_RTOL * np.abs(row).max():
             free = np.flatnonzero(~used_r)
             if free.size == 0:
                 break
@@ -139,12 +148,13 @@ class NCA:
     (ACA ties, rounding), so parity with the product is taken on the product's pivots after
     checking them."""
 
-    def __init__(self, prob, tree, lists, eps, pivots=None):
+    def __init__(self, prob, tree, lists, eps, pivots=None, hfr_parent_search=False):
         # reading R17: nested-basis errors compound over the LFR levels of an adaptive tree, so
         # the ACA runs at eps / 2 when leaves lie on several levels
         if len({l for l, _ in tree.all_leaves()}) > 1:
             eps = 0.5 * eps
         self.prob, self.tree, self.lists, self.eps = prob, tree, lists, eps
+        self.hfr_parent_search = hfr_parent_search  # reading R7b (Lists.far_list)
         L = tree.L
         self.search = [dict() for _ in range(L + 1)]
         if pivots is None:
@@ -168,7 +178,7 @@ class NCA:
     def search_sets(self, level, node):
         """Step 1 of P:597-631: t~^{B,i}, s~^{B,i}, t~^{B,o}, s~^{B,o}."""
         tree, lists = self.tree, self.lists
-        far = lists.far_list(level, node)
+        far = lists.far_list(level, node, self.hfr_parent_search)
         if is_leaf_node(tree, level, node):  # leaf (P:599-606)
             own = node_points(tree, level, node)
             far_pts = _union([tree.boxes[level][a] for a, _ in far] + self.parent_far_points(level, node))

@@ -191,7 +191,8 @@ static double complex K_entry(int64_t i, int64_t j, const double *pts, const dou
 /* out (n_rows x n_cols, row-major, complex) = K[rows, cols]. */
 void oracle_K_block(const int64_t *rows, int64_t n_rows, const int64_t *cols, int64_t n_cols, const double *pts,
                     const double *w, const double *D, double kappa, double *out) {
-#pragma omp parallel for schedule(static)
+  /* every entry independently (a single ACA row is one long row: threads over all entries) */
+#pragma omp parallel for collapse(2) schedule(static) if (n_rows * n_cols > 512)
   for (int64_t a = 0; a < n_rows; ++a) {
     for (int64_t b = 0; b < n_cols; ++b) {
       double complex v = K_entry(rows[a], cols[b], pts, w, D, kappa);
@@ -204,7 +205,7 @@ void oracle_K_block(const int64_t *rows, int64_t n_rows, const int64_t *cols, in
 /* out (n_rows x n_cols, row-major, complex) = A[rows, cols]. */
 void oracle_A_block(const int64_t *rows, int64_t n_rows, const int64_t *cols, int64_t n_cols, const double *pts,
                     const double *w, const double *q, const double *D, double kappa, double *out) {
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for collapse(2) schedule(static) if (n_rows * n_cols > 512)
   for (int64_t a = 0; a < n_rows; ++a) {
     for (int64_t b = 0; b < n_cols; ++b) {
       double complex v = A_entry(rows[a], cols[b], pts, w, q, D, kappa);

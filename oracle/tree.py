@@ -60,6 +60,8 @@ class Tree:
                 if not split:
                     if idx.size > leaf_size:
                         raise ValueError("leaf_size not reachable within max_level")
+                    if self.is_hfr(level):  # refinement rule 3: leaves are LFR
+                        raise ValueError("high-frequency box cannot be split within max_level")
                     leaves.add(key)
                     continue
                 sh = MAXL - (level + 1)
@@ -241,21 +243,25 @@ class Lists:
                     if need:
                         self.active[l].add(b)
 
-    def far_list(self, level, node):
+    def far_list(self, level, node, parent_search=False):
         """Far-field list used for the search sets of an active node.
 
         It is IL(B) (LFR) or IL(B,l) (HFR).  R7: an active HFR node whose IL(B,l) is empty
         (active only because its parent needs it) uses the children, in the matching child
-        cones, of its parent's IL in the two parent cones that nest in l."""
+        cones, of its parent's IL in the two parent cones that nest in l.  R7b
+        (parent_search=True): every HFR node with an HFR parent takes the union of its own
+        IL(B,l) and those children."""
         tree = self.tree
         if not tree.is_hfr(level):
             return [(a, None) for a in self.IL[level][node]]
         b, k = node
         lst = self.ILdir[level][b].get(k, [])
-        if lst:
+        if lst and not (parent_search and level > 1 and tree.is_hfr(level - 1)):
+            return lst
+        if level <= 1 or not tree.is_hfr(level - 1):
             return lst
         parent = (b[0] >> 1, b[1] >> 1)
-        sub = set()
+        sub = set(lst)
         for p in (2 * k, 2 * k + 1):
             for (a, ap) in self.ILdir[level - 1][parent].get(p, []):
                 for c in range(4):

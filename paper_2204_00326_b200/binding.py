@@ -33,7 +33,8 @@ class DAFMMError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("T", ctypes.c_double), ("self_term", ctypes.c_int), ("kernel_mode", ctypes.c_int),
                 ("max_level", ctypes.c_int), ("num_threads", ctypes.c_int), ("host_only", ctypes.c_int),
-                ("symmetric_pivots", ctypes.c_int), ("m2l_store", ctypes.c_int)]
+                ("symmetric_pivots", ctypes.c_int), ("m2l_store", ctypes.c_int),
+                ("hfr_parent_search", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -107,13 +108,25 @@ def _host(a, dtype):
     return a, a.ctypes.data_as(ctypes.c_void_p)
 
 
-def _dev(t):
-    """Device pointer of a torch CUDA complex128 tensor (or an int pointer)."""
+def _dev(t, n=None):
+    """Device pointer of a torch CUDA complex128 tensor (or an int pointer, unchecked); with n,
+    the tensor must hold exactly n elements (the library reads / writes n of them)."""
     if isinstance(t, int):
         return ctypes.c_void_p(t)
     if not (t.is_cuda and t.is_contiguous() and str(t.dtype) == "torch.complex128"):
         raise ValueError("expected a contiguous CUDA complex128 tensor")
+    if n is not None and t.numel() != n:
+        raise ValueError("expected %d elements, got %d" % (n, t.numel()))
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_vec(a, n, writeable=False):
+    """Pointer of a host complex128 vector of exactly n elements, C-contiguous."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.complex128:
+        raise ValueError("host vectors must be numpy complex128 arrays")
+    if not a.flags.c_contiguous or a.size != n or (writeable and not a.flags.writeable):
+        raise ValueError("host vector must be C-contiguous%s with %d elements" % (", writeable," if writeable else "", n))
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 def default_options():
@@ -133,6 +146,7 @@ def dafmm_create_ex(points, weights, q, kappa, leaf_size, nca_tol, options=None)
     opt = options if options is not None else default_options()
     _check(load().dafmm_create_ex(pp, wp, qp, n, float(kappa), int(leaf_size), float(nca_tol), ctypes.byref(opt),
                                   ctypes.byref(h)))
+    _N_CACHE[h.value] = n
     return h
 
 
@@ -140,20 +154,34 @@ def dafmm_create(points, weights, q, kappa, leaf_size, nca_tol):
     return dafmm_create_ex(points, weights, q, kappa, leaf_size, nca_tol, None)
 
 
+_N_CACHE = {}  # handle value -> n (dafmm_create_ex fills it; a handle's n never changes)
+
+
+def _n_of(h):
+    key = h.value if isinstance(h, ctypes.c_void_p) else int(h)
+    n = _N_CACHE.get(key)
+    if n is None:
+        s = Stats()
+        _check(load().dafmm_stats(h, ctypes.byref(s)))
+        n = _N_CACHE[key] = int(s.n)
+    return n
+
+
 def dafmm_matvec(h, x, y):
-    return _check(load().dafmm_matvec(h, _dev(x), _dev(y)))
+    n = _n_of(h)
+    return _check(load().dafmm_matvec(h, _dev(x, n), _dev(y, n)))
 
 
 def dafmm_matvec_parts(h, x, y, mask):
-    return _check(load().dafmm_matvec_parts(h, _dev(x), _dev(y), int(mask)))
+    n = _n_of(h)
+    return _check(load().dafmm_matvec_parts(h, _dev(x, n), _dev(y, n), int(mask)))
 
 
 def dafmm_matvec_host(h, x_host, y_host):
-    """x_host, y_host: numpy complex128 arrays (pinned torch tensors also accepted via .numpy())."""
-    if x_host.dtype != np.complex128 or y_host.dtype != np.complex128:
-        raise ValueError("host vectors must be complex128")
-    return _check(load().dafmm_matvec_host(h, x_host.ctypes.data_as(ctypes.c_void_p),
-                                           y_host.ctypes.data_as(ctypes.c_void_p)))
+    """x_host, y_host: C-contiguous numpy complex128 arrays of n elements (pinned torch tensors
+    are accepted via .numpy())."""
+    n = _n_of(h)
+    return _check(load().dafmm_matvec_host(h, _host_vec(x_host, n), _host_vec(y_host, n, writeable=True)))
 
 
 def ls_gmres_solve(h, f, psi, tol, maxit, restart=50, history=None):
@@ -165,7 +193,8 @@ def ls_gmres_solve(h, f, psi, tol, maxit, restart=50, history=None):
         if history.dtype != np.float64 or history.size < maxit + 1:
             raise ValueError("history must be float64 with maxit + 1 entries")
         hp = history.ctypes.data_as(ctypes.c_void_p)
-    rc = _check(load().ls_gmres_solve(h, _dev(f), _dev(psi), float(tol), int(maxit), int(restart), ctypes.byref(it),
+    n = _n_of(h)
+    rc = _check(load().ls_gmres_solve(h, _dev(f, n), _dev(psi, n), float(tol), int(maxit), int(restart), ctypes.byref(it),
                                       ctypes.byref(rr), hp))
     return rc, it.value, rr.value
 
@@ -220,6 +249,7 @@ def dafmm_h0_eval(z2, out, band, stream=None):
 
 def dafmm_destroy(h):
     if h:
+        _N_CACHE.pop(h.value if isinstance(h, ctypes.c_void_p) else int(h), None)
         load().dafmm_destroy(h)
 
 

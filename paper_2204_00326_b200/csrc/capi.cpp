@@ -48,6 +48,7 @@ void dafmm_default_options(dafmm_options* opt) {
   opt->host_only = o.host_only;
   opt->symmetric_pivots = o.symmetric_pivots;
   opt->m2l_store = o.m2l_store;
+  opt->hfr_parent_search = o.hfr_parent_search;
 }
 
 int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
@@ -64,6 +65,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.host_only = opt->host_only;
     o.symmetric_pivots = opt->symmetric_pivots;
     o.m2l_store = opt->m2l_store;
+    o.hfr_parent_search = opt->hfr_parent_search;
     if (o.m2l_store < -1 || o.m2l_store > 1) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0 or 1");
   }
   std::unique_ptr<dafmm_plan> h;
@@ -159,7 +161,18 @@ int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int max
 
 int dafmm_set_stream(dafmm_handle h, void* stream) {
   if (!h) return fail(DAFMM_EINVAL, "null handle");
-  h->dev.stream = (cudaStream_t)stream;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!h->plan.opt.host_only && s != h->dev.stream) {
+    // order the new stream after everything pending on the old one: both use the handle's
+    // scratch buffers (x_t, mult, loc, phi, slots, GMRES workspace)
+    cudaEvent_t ev;
+    cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, h->dev.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ev, 0);
+    cudaEventDestroy(ev);
+    if (e != cudaSuccess) return fail(DAFMM_ECUDA, std::string("dafmm_set_stream: ") + cudaGetErrorString(e));
+  }
+  h->dev.stream = s;
   return DAFMM_OK;
 }
 

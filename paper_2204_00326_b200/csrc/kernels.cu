@@ -1,14 +1,18 @@
 // sm_100a kernels of the DAFMM matvec and the GMRES vector work.
 //
-// Passes per matvec (DESIGN.md §Kernels):
+// Passes per matvec (DESIGN.md §6):
 //   gather      x (caller order) -> x_t, v_t = w o x_t (tree order)                 HBM
-//   p2m / m2m   batched column-major GEMVs over stored operator blocks            HBM
-//   m2l         all levels in one launch: target pivots x staged source pivots,
-//               H0^(1) evaluated on the fly (never stored)                       fp64 ALU
+//   p2m / m2m   batched GEMVs over stored row-major operator blocks               HBM
+//   m2l         all levels in one persistent launch.  Default (m2l_store): the kernel-entry
+//               blocks A_{t s} were evaluated once at create and are streamed from HBM by
+//               TMA bulk copies (m2l_stored_kernel)                               HBM
+//               m2l_store = 0: entries evaluated on the fly (m2l_kernel)           fp64 ALU
 //   l2l         batched GEMVs, coarse to fine                                      HBM
-//   near        per leaf: P2P over N(leaf) with H0 on the fly + self term, fused
-//               with L2P and the combine y = x + kappa^2 q phi, scattered back       fp64 ALU
-// Every kernel works in H0 units; the (i/4) of G is applied once per target in `near`.
+//   p2p         per leaf: near field with H0 on the fly (side stream, concurrent
+//               with p2m..l2l); symmetric pairs evaluated once (column sums)       fp64 ALU
+//   combine     L2P + near-field slots + self term + y = x + kappa^2 q phi, scattered
+//               back to caller order                                               HBM
+// Every kernel works in H0 units; the (i/4) of G is applied once per target in `combine`.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1269,6 +1273,16 @@ bool upload(DevPlan& d, T** dst, const std::vector<T>& src, std::string& err) {
   return ck(cudaMemcpy(*dst, src.data(), bytes, cudaMemcpyHostToDevice), err, "cudaMemcpy H2D");
 }
 
+// free one allocation made by alloc / upload (and forget it)
+template <typename T>
+void release(DevPlan& d, T** p) {
+  if (!*p) return;
+  auto it = std::find(d.allocations.begin(), d.allocations.end(), (void*)*p);
+  if (it != d.allocations.end()) d.allocations.erase(it);
+  cudaFree(*p);
+  *p = nullptr;
+}
+
 template <typename T>
 bool alloc(DevPlan& d, T** dst, size_t count, std::string& err) {
   *dst = nullptr;
@@ -1585,11 +1599,15 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
               double* relres_out, double* history, std::string& err) {
   const int64_t n = d.n;
   const int m = restart > 0 ? restart : 50;
-  if (m > 255) { err = "restart must be <= 255"; return DAFMM_EINVAL; }
+  if (m > 255) { err = "restart must be <= 255"; return DAFMM_EINVAL; }  // combine_kernel's coefficient cache
   cudaStream_t s = d.stream;
   const int nb = grid_for(n, kVecThreads, 296);
   if (d.gm_restart != m) {
-    if (d.gm_V) { err = "GMRES workspace already sized for another restart"; return DAFMM_EINVAL; }
+    // (re)size the workspace for this restart: the previous one (another restart) is released
+    for (void** p : {(void**)&d.gm_V, (void**)&d.gm_w, (void**)&d.gm_r, (void**)&d.gm_h, (void**)&d.gm_part})
+      release(d, p);
+    if (d.gm_hostbuf) cudaFreeHost(d.gm_hostbuf);
+    d.gm_hostbuf = nullptr;
     d.gm_restart = m;
     if (!alloc(d, &d.gm_V, (size_t)(m + 1) * n, err) || !alloc(d, &d.gm_w, n, err) || !alloc(d, &d.gm_r, n, err) ||
         !alloc(d, &d.gm_h, 3 * (m + 2), err) || !alloc(d, &d.gm_part, (size_t)nb * (m + 2), err))
@@ -1625,12 +1643,15 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
   int iters = 0;
   d.gm_reorth = 0;
   bool converged = false;
-  // r = f (psi0 = 0)
+  // r = f (psi0 = 0).  Convergence is decided on the true residual r = f - A psi (recomputed at
+  // every restart): a cycle that ends because its implicit (Givens) residual reached tol starts a
+  // new cycle when the true residual has not (rounding makes the two differ slightly)
   cudaMemcpyAsync(d.gm_r, f, sizeof(double2) * n, cudaMemcpyDeviceToDevice, s);
-  while (iters < maxit && !converged) {
+  while (true) {
     double beta;
     if (!norm(d.gm_r, beta)) return DAFMM_ECUDA;
     if (beta / bnorm <= tol) { converged = true; break; }
+    if (iters >= maxit) break;
     axpby_kernel<<<nb, kVecThreads, 0, s>>>(n, 1.0 / beta, d.gm_r, 0.0, d.gm_r, d.gm_V);
     std::fill(H.begin(), H.end(), 0.0);
     std::fill(g.begin(), g.end(), 0.0);
@@ -1687,8 +1708,7 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
       k = j + 1;
       double res = std::abs(g[j + 1]) / bnorm;
       if (history) history[iters] = res;
-      if (res <= tol) { converged = true; break; }
-      if (iters >= maxit || hnext == 0.0) break;
+      if (res <= tol || iters >= maxit || hnext == 0.0) break;
     }
     // y = H^{-1} g, psi += V y
     std::vector<std::complex<double>> yv(k);
@@ -1710,7 +1730,7 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
   if (!norm(d.gm_r, rn)) return DAFMM_ECUDA;  // gm_r = f - A psi of the final iterate
   *iters_out = iters;
   *relres_out = rn / bnorm;
-  return converged ? DAFMM_OK : DAFMM_NOT_CONVERGED;
+  return (converged && rn / bnorm <= tol) ? DAFMM_OK : DAFMM_NOT_CONVERGED;
 }
 
 int h0_eval(const double* z2, double2* out, int64_t n, int code, cudaStream_t s, std::string& err) {

@@ -26,6 +26,7 @@ struct Options {
   int host_only = 0;       // skip the device upload
   int symmetric_pivots = 0;  // reading R19 (option): one ACA per node, outgoing skeleton = incoming
   int m2l_store = -1;        // M2L blocks: -1 auto, 0 evaluated on the fly every matvec, 1 stored in HBM
+  int hfr_parent_search = 0;  // reading R7b (option): HFR search sets also take the parent's far children
 };
 
 struct Box {

@@ -145,8 +145,16 @@ void aca(const Ctx& cx, const std::vector<int32_t>& rows, const std::vector<int3
   std::vector<zd> r(n), u(m);
   double norm2 = 0.0;
   int i = 0, k = 0;
+  // R10: a residual row whose largest entry is at rounding level relative to the row itself
+  // (<= 1e3 eps x its largest original entry) lies in the span of the earlier terms; pivoting on
+  // it would make the cross matrix singular, so it counts as a zero row
+  constexpr double kZeroRowRtol = 1e3 * 2.220446049250313e-16;
   while (k < cap) {
-    for (int j = 0; j < n; ++j) r[j] = cx.K(rows[i], cols[j]);
+    double row_max = 0.0;
+    for (int j = 0; j < n; ++j) {
+      r[j] = cx.K(rows[i], cols[j]);
+      row_max = std::max(row_max, std::abs(r[j]));
+    }
     entries += n;
     for (int l = 0; l < k; ++l) {
       zd ul = U[(size_t)l * m + i];
@@ -161,7 +169,7 @@ void aca(const Ctx& cx, const std::vector<int32_t>& rows, const std::vector<int3
       double a = std::abs(r[j]);
       if (a > best) { best = a; jm = j; }
     }
-    if (!(best > 0.0)) {
+    if (!(best > kZeroRowRtol * row_max)) {
       int nxt = -1;
       for (int t = 0; t < m; ++t)
         if (!used_r[t]) { nxt = t; break; }
@@ -347,6 +355,10 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
       if (!split) {
         if (cnt > leaf_size) {
           err = "leaf_size not reachable within max_level";
+          return DAFMM_EINVAL;
+        }
+        if (lv.hfr) {  // refinement rule 3: every leaf must be LFR (no directional leaf bases)
+          err = "a high-frequency box cannot be split within max_level (refinement rule 3 needs LFR leaves)";
           return DAFMM_EINVAL;
         }
         B.leaf = true;
@@ -540,7 +552,10 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
         } else {
           for (auto& e : lv.ILdir[b])
             if (e[0] == k) far.push_back({e[1], e[2]});
-          if (far.empty()) {
+          // R7: an active node with an empty IL(B,k) searches the children (matching child cones) of
+          // its parent's IL in the two parent cones nesting in k; R7b (option hfr_parent_search):
+          // every node with an HFR parent adds them to its own IL(B,k)
+          if (far.empty() || (P.opt.hfr_parent_search && l > 1 && pv.hfr)) {
             const Box& B = lv.boxes[b];
             int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
             for (auto& e : pv.ILdir[pb]) {
@@ -1108,7 +1123,8 @@ int export_plan(const Plan& P, const std::string& dir, std::string& err) {
   for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
     if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
   bool ok = true;
-  std::vector<double> meta = {(double)P.n, (double)P.L, P.W, P.x0, P.y0, P.kappa, P.opt.T, P.nca_tol};
+  std::vector<double> meta = {(double)P.n, (double)P.L, P.W, P.x0, P.y0, P.kappa, P.opt.T, P.nca_tol,
+                              (double)P.opt.hfr_parent_search};
   ok &= write_npy(dir + "/meta.npy", "<f8", meta, {(int64_t)meta.size()});
   std::vector<int64_t> perm(P.perm.begin(), P.perm.end());
   ok &= write_npy(dir + "/perm.npy", "<i8", perm, {(int64_t)perm.size()});

@@ -104,6 +104,21 @@ CONFIGS = {
 }
 
 
+def l_shaped_problem(n=4000, kappa=40.0, seed=7, nca_tol=1e-8):
+    """Seeded random points in the L-shaped domain [-1,1]^2 minus the quadrant x1, x2 > 0 (no
+    lattice structure, ragged leaves, a re-entrant corner): the geometry on which directional
+    nodes can be active only through their parent (reading R7).  Weights = area / n, q = 1 +
+    0.5 cos(3 x1), x = unit-modulus seeded phases."""
+    rng = np.random.default_rng(seed)
+    pts = rng.uniform(-1.0, 1.0, size=(3 * n, 2))
+    pts = pts[~((pts[:, 0] > 0) & (pts[:, 1] > 0))][:n]
+    w = np.full(n, 3.0 / n)
+    q = 1.0 + 0.5 * np.cos(3.0 * pts[:, 0])
+    x = unit_phase_vector(n, seed=seed + 1)
+    return dict(name="lshape", points=pts, weights=w, q=q, kappa=kappa, nca_tol=nca_tol, leaf_size=32, x=x,
+                f=plane_wave_rhs(pts, q, kappa), gmres_tol=1e-8, n_grid=None)
+
+
 def make_problem(name, n=None, kappa=None):
     """Return dict(points, weights, q, kappa, nca_tol, leaf_size, x, f, gmres_tol) for a config.
     `n` / `kappa` override the grid size (the maximum depth for the adaptive config 5) and the

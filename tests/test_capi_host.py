@@ -163,3 +163,62 @@ def test_symmetric_near_field_flag():
     pts = rng.uniform(-1, 1, size=(3000, 2))
     op = binding.DAFMM(pts, np.full(3000, 4.0 / 3000), np.ones(3000), 12.0, 64, 1e-8, host_only=1)
     assert op.stats()["p2p_symmetric"] == 0
+
+
+def test_hfr_box_at_max_level_rejected():
+    """Refinement rule 3: every leaf must be LFR.  A max_level that stops the tree while
+    its boxes are still in the high-frequency regime is an error (it would otherwise silently
+    drop the far field of such leaves); the oracle's tree refuses the same input."""
+    prod = _prod()
+    P = make_problem("c1", n=64, kappa=160.0)  # level-3 boxes: kappa b = 40 (HFR)
+    with pytest.raises(prod.DAFMMError) as e:
+        prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 4096, 1e-6, host_only=1, max_level=3)
+    assert e.value.code == -1 and "max_level" in prod.dafmm_last_error()
+    with pytest.raises(ValueError):
+        Tree(P["points"], P["weights"], P["kappa"], 4096, max_level=3)
+    # an LFR stop is fine: leaf_size 4096 holds the whole grid, kappa = 1 keeps the root LFR
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], 1.0, 4096, 1e-6, host_only=1, max_level=3)
+    assert op.stats()["levels"] == 0
+    op.close()
+
+
+def test_host_setup_l_shaped_parent_search(tmp_path):
+    """Reading R7b (hfr_parent_search=1) on the L-shaped random point set: the product's lists
+    equal the oracle's and its pivots lie in the oracle's R7b search sets; with the option off
+    the plan is the paper's (search sets of P:624-631 only)."""
+    from synth.configs import l_shaped_problem
+    P = l_shaped_problem()
+    prod = _prod()
+    for flag in (1, 0):
+        op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], P["leaf_size"], P["nca_tol"], host_only=1,
+                        hfr_parent_search=flag)
+        op.export_plan(tmp_path / ("plan%d" % flag))
+        op.close()
+        plan = load_plan(tmp_path / ("plan%d" % flag))
+        assert plan["meta"]["hfr_parent_search"] == bool(flag)
+        tree = Tree(P["points"], P["weights"], P["kappa"], P["leaf_size"])
+        lists = Lists(tree)
+        compare_lists(plan, tree, lists)
+        piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+        prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+        validate_pivots(NCA(prob, tree, lists, P["nca_tol"], pivots=piv, hfr_parent_search=bool(flag)), piv)
+
+
+def test_binding_rejects_bad_host_vectors():
+    """dafmm_matvec_host takes C-contiguous complex128 host arrays of exactly n elements; the
+    binding refuses anything else before the library could read or write past them."""
+    from paper_2204_00326_b200 import binding
+    P = make_problem("c1", n=16)
+    op = binding.DAFMM(P["points"], P["weights"], P["q"], 5.0, 64, 1e-8, host_only=1)
+    good = np.zeros(256, dtype=np.complex128)
+    for bad in (np.zeros(255, dtype=np.complex128), np.zeros(512, dtype=np.complex128)[::2],
+                np.zeros(256, dtype=np.float64)):
+        with pytest.raises(ValueError):
+            op.matvec_host(bad, good)
+        with pytest.raises(ValueError):
+            op.matvec_host(good, bad)
+    ro = np.zeros(256, dtype=np.complex128)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        op.matvec_host(good, ro)
+    op.close()

@@ -74,3 +74,31 @@ def test_gmres_zero_rhs():
     psi = torch.ones_like(f)
     rc, iters, relres = op.gmres(f, psi, 1e-8, 10, 50)
     assert rc == 0 and iters == 0 and float(psi.abs().max()) == 0.0
+
+
+def test_gmres_restart_change_and_true_residual_status():
+    """A handle re-sizes its GMRES workspace when the restart changes; DAFMM_OK always means the
+    TRUE relative residual ||f - A psi|| / ||f|| is within tol (the stopping rule uses it)."""
+    P = make_problem("c2", n=128, kappa=20.0)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    f = torch.from_numpy(P["f"]).cuda()
+    y = torch.empty_like(f)
+    for restart in (10, 30, 10):
+        psi = torch.empty_like(f)
+        rc, iters, relres = op.gmres(f, psi, 1e-9, 400, restart)
+        assert rc == 0 and relres <= 1e-9
+        op.matvec(psi, y)
+        torch.cuda.synchronize()
+        true = np.linalg.norm((y - f).cpu().numpy()) / np.linalg.norm(P["f"])
+        assert true <= 1e-9 * (1 + 1e-6)
+
+
+def test_binding_rejects_wrong_lengths():
+    P = make_problem("c1", n=32)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, 1e-8)
+    x = torch.zeros(1024, dtype=torch.complex128, device="cuda")
+    short = torch.zeros(1000, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError):
+        op.matvec(x, short)
+    with pytest.raises(ValueError):
+        op.gmres(short, x, 1e-8, 10)

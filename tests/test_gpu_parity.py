@@ -42,25 +42,55 @@ def _oracle_on_product_plan(P, op, tmp_path, leaf_size=64):
     lists = Lists(tree)
     compare_lists(plan, tree, lists)
     piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
-    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv)
+    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv, hfr_parent_search=plan["meta"]["hfr_parent_search"])
     validate_pivots(nca, piv)
     return prob, nca
 
 
+def _hfr_hfr_levels(tree, lists):
+    from oracle.nca import children_nodes
+    out = []
+    for l in range(1, tree.L):
+        if tree.is_hfr(l) and tree.is_hfr(l + 1):
+            if any(c in lists.active[l + 1] for nd in lists.active[l] for c in children_nodes(tree, l, nd)):
+                out.append(l)
+    return out
+
+
+def _leaf_rel_max(y, yo, x, prob, tree):
+    """Per-leaf diagnostic beside the l2 gate: the largest over leaves of the leaf's relative
+    l2 error of y - x (a localized error in a few leaves cannot hide under the global norm)."""
+    worst = 0.0
+    for l, b in tree.all_leaves():
+        idx = tree.boxes[l][b]
+        den = np.linalg.norm(yo[idx] - x[idx])
+        if den > 0:
+            worst = max(worst, np.linalg.norm(y[idx] - yo[idx]) / den)
+    return worst
+
+
+# ("c2", 64, 40) and ("c2", 128, 40): two directional levels (kappa b = 10 over kappa b = 5) with
+# active HFR parents over active HFR children -- directional M2M / L2L between HFR levels
+# (P:687-698, P:717-731) and the kappa b = 10 directional M2L -- over 2 x 2- and 4 x 4-point leaves
 @pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0),
-                                          ("c1", 128, 4.0), ("c1", 40, 7.0), ("c5", 5, 12.0), ("c5", 5, 8.0)])
+                                          ("c1", 128, 4.0), ("c1", 40, 7.0), ("c5", 5, 12.0), ("c5", 5, 8.0),
+                                          ("c2", 64, 40.0), ("c2", 128, 40.0)])
 def test_gpu_dafmm_matches_oracle(name, n, kappa, tmp_path):
     """Both M2L modes: the blocks stored in HBM (m2l_store=1) and evaluated on the fly (0)."""
     P = make_problem(name, n=n, kappa=kappa)
     op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=1)
     assert op.stats()["m2l_stored"] == 1
-    # 64-point leaves take the symmetric near field; the 40 x 40 grid has ragged leaves
-    assert op.stats()["p2p_symmetric"] == (0 if n == 40 else 1)
+    # 64-point leaves take the symmetric near field; the 40 x 40 grid and the kappa = 40 cases
+    # (4- and 16-point leaves) are one-sided
+    assert op.stats()["p2p_symmetric"] == (0 if (n == 40 or kappa == 40.0) else 1)
     prob, nca = _oracle_on_product_plan(P, op, tmp_path)
+    if kappa == 40.0:
+        assert _hfr_hfr_levels(nca.tree, nca.lists) == [3]
     x = P["x"]
     y_gpu = _gpu_matvec(op, x)
     y_cpu = nca.matvec(x)
     assert _rel(y_gpu - x, y_cpu - x) <= 1e-11
+    assert _leaf_rel_max(y_gpu, y_cpu, x, prob, nca.tree) <= 1e-9
     op_fly = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=0)
     assert op_fly.stats()["m2l_stored"] == 0 and op_fly.stats()["m2l_store_bytes"] == 0
     y_fly = _gpu_matvec(op_fly, x)
@@ -169,3 +199,22 @@ def test_gpu_symmetric_near_field_32_point_leaves(tmp_path):
     assert _rel(y - x, yd - x) <= 10 * 1e-8
     near = _gpu_matvec(op, x, 1)
     assert _rel(near - x, nca.matvec(x, parts=("near",)) - x) <= 1e-12
+
+
+def test_gpu_r7_substitute_lists(tmp_path):
+    """Directional nodes active only through their parent (reading R7) on an L-shaped random
+    point set (leaf size 32, ragged leaves), with the R7b search sets (hfr_parent_search=1):
+    GPU vs the oracle's serial DAFMM on the product's validated pivots, and vs dense."""
+    from synth.configs import l_shaped_problem
+    P = l_shaped_problem()
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], P["leaf_size"], P["nca_tol"],
+                       hfr_parent_search=1)
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path, leaf_size=P["leaf_size"])
+    assert nca.hfr_parent_search
+    assert any(not nca.lists.ILdir[4][b].get(k) for b, k in nca.lists.active[4])
+    x = P["x"]
+    y = _gpu_matvec(op, x)
+    y_cpu = nca.matvec(x)
+    assert _rel(y - x, y_cpu - x) <= 1e-11
+    yd = oracle.dense_matvec(prob, x)
+    assert _rel(y - x, yd - x) <= 10 * P["nca_tol"]
