@@ -74,7 +74,11 @@ typedef struct {
                           them: HBM bound), DAFMM_ENOMEM if they do not fit, DAFMM_EINVAL if a
                           node has more than 128 pivots; -1 (default) auto: store when the blocks
                           take at most half of the free device memory and every node has at most
-                          128 pivots, else on the fly.  dafmm_stats reports the choice. */
+                          128 pivots, else on the fly.  2: one block per unordered node pair
+                          {A, B} (reading R22; needs symmetric_pivots = 1: the block of A <- B is
+                          then the transpose of B <- A), applied twice per matvec (row and column
+                          sums): half the bytes of 1.  With -1 and symmetric_pivots = 1 the auto
+                          choice is 2.  dafmm_stats reports the choice. */
   int hfr_parent_search; /* NCA search sets of a directional node (B, l) whose parent is also
                           directional (P:624-631 use IL(B, l) only): 0 (default) as the paper writes
                           them; 1 also take the children, in the matching child cones, of the
@@ -102,13 +106,16 @@ typedef struct {
   int64_t m2l_band_entries[48]; /* M2L entries per H0 band code (0 generic, 1 near z<=8, 2 near z<=12,
                                     3 near z<=7, 4+b data band b; dafmm_h0_bands) */
   int64_t p2p_band_entries[48]; /* P2P point pairs per band code */
-  int32_t m2l_stored;           /* 1: M2L blocks stored in HBM (dafmm_options.m2l_store) */
+  int32_t m2l_stored;           /* 1: M2L blocks stored in HBM per target node, 2: per node pair
+                                   (dafmm_options.m2l_store); 0: evaluated on the fly */
   int64_t m2l_store_bytes;      /* their bytes (0 when evaluated on the fly) */
   int64_t m2l_stream_len;       /* source pivots over all M2L target nodes (multipole gathers per matvec) */
   int64_t n_loc;                /* local-expansion coefficients (M2L outputs) */
   int64_t gmres_reorth;         /* second Gram-Schmidt passes (CGS2) in the last ls_gmres_solve */
   int32_t p2p_symmetric;        /* 1: near-field pairs of different leaves evaluated once (every leaf
                                    has 32 or 64 points); 0: each leaf evaluates all its pairs */
+  int64_t m2l_stored_entries;   /* kernel entries in the M2L blocks as stored / streamed per matvec
+                                   (m2l_entries / 2 with m2l_store = 2, else m2l_entries) */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);

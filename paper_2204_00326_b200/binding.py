@@ -49,7 +49,8 @@ class Stats(ctypes.Structure):
                 ("aca_entries", ctypes.c_int64), ("m2l_band_entries", ctypes.c_int64 * 48),
                 ("p2p_band_entries", ctypes.c_int64 * 48), ("m2l_stored", ctypes.c_int32),
                 ("m2l_store_bytes", ctypes.c_int64), ("m2l_stream_len", ctypes.c_int64), ("n_loc", ctypes.c_int64),
-                ("gmres_reorth", ctypes.c_int64), ("p2p_symmetric", ctypes.c_int32)]
+                ("gmres_reorth", ctypes.c_int64), ("p2p_symmetric", ctypes.c_int32),
+                ("m2l_stored_entries", ctypes.c_int64)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

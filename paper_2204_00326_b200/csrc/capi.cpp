@@ -17,7 +17,8 @@ struct dafmm_plan {
   dafmm::Plan plan;
   dafmm::DevPlan dev;
   int64_t operator_bytes = 0;
-  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0, m2l_stream_len = 0, n_loc = 0;
+  int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0, m2l_stream_len = 0, n_loc = 0, m2l_stored_entries = 0;
+  int m2l_sym = 0;
   int p2p_sym = 0;
   std::vector<int64_t> m2l_band, p2p_band;
 };
@@ -66,7 +67,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.symmetric_pivots = opt->symmetric_pivots;
     o.m2l_store = opt->m2l_store;
     o.hfr_parent_search = opt->hfr_parent_search;
-    if (o.m2l_store < -1 || o.m2l_store > 1) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0 or 1");
+    if (o.m2l_store < -1 || o.m2l_store > 2) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0, 1 or 2");
   }
   std::unique_ptr<dafmm_plan> h;
   try {
@@ -81,7 +82,9 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     if (rc != DAFMM_OK) return fail(rc, err);
     double t0 = now_s();
     dafmm::Packed pk;
-    rc = dafmm::pack_plan(h->plan, pk, err);
+    size_t free_b = 0, total_b = 0;
+    if (!o.host_only && cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 0;
+    rc = dafmm::pack_plan(h->plan, pk, err, free_b);
     if (rc != DAFMM_OK) return fail(rc, err);
     double t1 = now_s();
     h->plan.t_ops = t1 - t0;
@@ -96,6 +99,8 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     h->operator_bytes = (int64_t)pk.ops.size() * 16;
     h->p2p_pairs = pk.p2p_pairs;
     h->m2l_entries = pk.m2l_entries;
+    h->m2l_stored_entries = pk.m2l_stored_entries;
+    h->m2l_sym = pk.m2l_sym;
     h->m2l_pairs = pk.m2l_pairs;
     h->m2l_stream_len = (int64_t)pk.m2l_stream_idx.size();
     h->n_loc = pk.n_loc;
@@ -232,8 +237,9 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->setup_pack_s = P.t_pack;
   out->setup_upload_s = P.t_upload;
   out->aca_entries = P.aca_entries;
-  out->m2l_stored = h->dev.m2l_mat != nullptr ? 1 : 0;
-  out->m2l_store_bytes = h->dev.m2l_mat != nullptr ? h->m2l_entries * 16 : 0;
+  out->m2l_stored = h->dev.m2l_mat != nullptr ? (h->m2l_sym ? 2 : 1) : 0;
+  out->m2l_store_bytes = h->dev.m2l_mat != nullptr ? h->m2l_stored_entries * 16 : 0;
+  out->m2l_stored_entries = h->m2l_stored_entries;
   out->m2l_stream_len = h->m2l_stream_len;
   out->n_loc = h->n_loc;
   out->gmres_reorth = h->dev.gm_reorth;

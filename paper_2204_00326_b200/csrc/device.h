@@ -74,6 +74,16 @@ struct DevPlan {
   int64_t* m2l_mat_off = nullptr;
   double2* m2l_mat = nullptr;
   int m2l_store_grid = 0;
+  // pair-stored M2L (Packed::m2l_sym, reading R22): own multipole of each target (column sums),
+  // the column-sum slots (one per stream position) and the receiving nodes' slot lists
+  int m2l_sym = 0;
+  int64_t* m2l_self_moff = nullptr;
+  double2* m2l_slots = nullptr;
+  int m2l_in_nodes = 0;
+  int64_t* m2l_in_lo = nullptr;
+  int32_t* m2l_in_rows = nullptr;
+  int32_t* m2l_in_ptr = nullptr;
+  int64_t* m2l_in_off = nullptr;
   // leaves
   int nleaves = 0, max_leaf = 0;
   int32_t* leaf_begin = nullptr;

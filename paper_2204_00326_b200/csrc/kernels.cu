@@ -937,6 +937,279 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
   cp_async_wait_all();
 }
 
+// ---- pair-stored M2L (reading R22, dafmm_options.m2l_store = 2) ---------------------------------
+// With one skeleton per node (R19: s^{B,o} = t^{B,i}) the block of (B <- A) is the transpose of
+// the block of (A <- B), G being symmetric, so each unordered interaction-list pair
+// keeps one block, in the stream of its owner B.  The owner's CTA applies it twice per matvec:
+//   row sums     u_B[t] += sum_c M[t, c] m_A[c]         (as m2l_stored_kernel)
+//   column sums  slot[c] = sum_t M[t, c] m_B[t]          (u_A's share; added by m2l_slot_gather)
+// so the HBM stream is half that of m2l_stored_kernel for the same work.  Same warp-specialised
+// TMA ring, but every stage holds whole columns (floor(kMSStageE / r) of them), so the column
+// sums of a stage are complete in shared memory: after the row pass over a stage, the consumers
+// re-read it column-wise (g threads per column, xor-shuffle reduced) -- a second shared-memory
+// read of the stage instead of a second HBM read of the block.
+struct MSPUnit {
+  int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
+  int r, pad;
+  int64_t sp, lo, self_m;  // stream offset, output offset, own multipole
+};
+__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
+    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ mat_off, const int64_t* __restrict__ self_moff, const double2* __restrict__ mat,
+    const double2* __restrict__ mult, double2* __restrict__ loc, double2* __restrict__ slots) {
+  extern __shared__ __align__(128) double2 ms_dyn[];
+  double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
+  __shared__ __align__(16) double2 mb[2][kMSCols];
+  __shared__ __align__(16) double2 mself[2][kMaxStoredRows];
+  static_assert(kMaxStoredRows == kMSConsumers, "the row reduction reuses mself[buf]");
+  __shared__ __align__(8) uint64_t full[kMSStages], empty[kMSStages], ufull[kMSUnits], uempty[kMSUnits];
+  __shared__ MSPUnit units[kMSUnits];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMSStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kMSConsumers / 32);
+    }
+    for (int i = 0; i < kMSUnits; ++i) {
+      mbar_init(&ufull[i], 1);
+      mbar_init(&uempty[i], kMSConsumers / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == kMSConsumers / 32) {  // ---- producer (one lane)
+    if (lane != 0) return;
+    int stage = 0, uslot = 0;
+    uint32_t sphase = 0, uphase = 0;
+    int tgt = -2, L = 0, c0 = 0, r = 0;
+    int64_t sp = 0, lo = 0, moff = 0, sm = 0;
+    int ntgt = blockIdx.x, nr = 0;
+    int64_t nsp = 0, nsp1 = 0, nlo = 0, nmoff = 0, nsm = 0;
+    auto prefetch_node = [&]() {
+      if (ntgt < ntargets) {
+        nr = rows[ntgt];
+        nsp = stream_ptr[ntgt];
+        nsp1 = stream_ptr[ntgt + 1];
+        nlo = loc_off[ntgt];
+        nmoff = mat_off[ntgt];
+        nsm = self_moff[ntgt];
+      }
+    };
+    prefetch_node();
+    auto next_unit = [&](MSPUnit& u) {
+      if (tgt == -1 || ((tgt == -2 || c0 >= L) && ntgt >= ntargets)) {
+        tgt = -1;
+        u = MSPUnit{-1, 0, 0, 0, 0, 0, 0, 0, 0};
+        return;
+      }
+      if (tgt == -2 || c0 >= L) {
+        tgt = ntgt;
+        r = nr;
+        sp = nsp;
+        L = (int)(nsp1 - nsp);
+        lo = nlo;
+        moff = nmoff;
+        sm = nsm;
+        c0 = 0;
+        ntgt += gridDim.x;
+        prefetch_node();
+      }
+      const int c1 = min(L, c0 + kMSCols);
+      u = MSPUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0), r, 0, sp, lo, sm};
+      c0 = c1;
+    };
+    auto publish = [&](const MSPUnit& u) {
+      mbar_wait(&uempty[uslot], uphase ^ 1);
+      units[uslot] = u;
+      mbar_arrive(&ufull[uslot]);
+      if (++uslot == kMSUnits) {
+        uslot = 0;
+        uphase ^= 1;
+      }
+    };
+    MSPUnit cur, nxt;
+    next_unit(cur);
+    int64_t cur_moff = moff;
+    publish(cur);
+    while (cur.tgt >= 0) {
+      next_unit(nxt);
+      const int64_t nxt_moff = moff;
+      publish(nxt);
+      const int cps = kMSStageE / cur.r;  // whole columns per stage
+      const double2* src = mat + cur_moff + (int64_t)cur.c0 * cur.r;
+      for (int cc = 0; cc < cur.c1 - cur.c0; cc += cps) {
+        const int cnt = min(cps, cur.c1 - cur.c0 - cc) * cur.r;
+        mbar_wait(&empty[stage], sphase ^ 1);
+        mbar_arrive_tx(&full[stage], (uint32_t)cnt * 16u);
+        bulk_load(ring[stage], src + (int64_t)cc * cur.r, (uint32_t)cnt * 16u, &full[stage]);
+        if (++stage == kMSStages) {
+          stage = 0;
+          sphase ^= 1;
+        }
+      }
+      cur = nxt;
+      cur_moff = nxt_moff;
+    }
+    return;
+  }
+  // ---- consumers
+  const int j = threadIdx.x;
+  int stage = 0, uslot = 0;
+  uint32_t sphase = 0, uphase = 0;
+  auto take = [&]() {
+    mbar_wait(&ufull[uslot], uphase);
+    const MSPUnit u = units[uslot];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&uempty[uslot]);
+    if (++uslot == kMSUnits) {
+      uslot = 0;
+      uphase ^= 1;
+    }
+    return u;
+  };
+  auto gather_idx = [&](const MSPUnit& u, int* kidx) {
+    const int64_t sp = u.sp + u.c0;
+#pragma unroll
+    for (int k = 0; k < kMSIdx; ++k) {
+      const int c = j + k * kMSConsumers;
+      kidx[k] = (u.tgt >= 0 && c < u.c1 - u.c0) ? __ldg(stream_idx + sp + c) : -1;
+    }
+  };
+  auto gather_issue = [&](const int* kidx, const MSPUnit& u, int b) {
+#pragma unroll
+    for (int k = 0; k < kMSIdx; ++k)
+      if (kidx[k] >= 0) cp_async16(&mb[b][j + k * kMSConsumers], mult + kidx[k]);
+    if (u.tgt >= 0 && j < u.r) cp_async16(&mself[b][j], mult + u.self_m + j);  // own multipole
+    cp_async_commit();
+  };
+  int nsl = 0, P = 1, buf = 0, sl = 0;
+  bool act = false;
+  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+  int kidx[kMSIdx];
+  MSPUnit u = take();
+  gather_idx(u, kidx);
+  gather_issue(kidx, u, 0);
+  while (u.tgt >= 0) {
+    const MSPUnit un = take();
+    gather_idx(un, kidx);
+    const int r = u.r;
+    if (u.flags & 1) {
+      nsl = kMSConsumers / r;
+      P = nsl * r;
+      sl = j / r;
+      act = j < P;
+      ar0 = ai0 = ar1 = ai1 = 0.0;
+    }
+    cp_async_wait_all();
+    consumers_sync();  // u's multipoles complete; everyone is done with the other buffers
+    const double2* mv = mb[buf];
+    const double2* msf = mself[buf];
+    const int nc = u.c1 - u.c0;
+    const int cps = kMSStageE / r;
+    const int nst = (nc + cps - 1) / cps;
+    // column pass geometry: g threads per column (power of 2, <= 32), kMSConsumers / g columns
+    // per round
+    for (int st = 0; st < nst; ++st) {
+      const int a = st * cps, b = min(nc, a + cps);
+      mbar_wait(&full[stage], sphase);
+      const double2* R = ring[stage];
+      if (act) {  // row pass: thread (t = j mod r, slice sl) takes columns c = sl (mod nsl)
+        const int t = j - sl * r;
+        int c = a + ((sl - a) % nsl + nsl) % nsl;
+        for (; c + 3 * nsl < b; c += 4 * nsl) {
+          const double2 m0 = R[(c - a) * r + t], v0 = mv[c];
+          const double2 m1 = R[(c + nsl - a) * r + t], v1 = mv[c + nsl];
+          const double2 m2 = R[(c + 2 * nsl - a) * r + t], v2 = mv[c + 2 * nsl];
+          const double2 m3 = R[(c + 3 * nsl - a) * r + t], v3 = mv[c + 3 * nsl];
+          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
+          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
+          ar1 = fma(m1.x, v1.x, fma(-m1.y, v1.y, ar1));
+          ai1 = fma(m1.x, v1.y, fma(m1.y, v1.x, ai1));
+          ar0 = fma(m2.x, v2.x, fma(-m2.y, v2.y, ar0));
+          ai0 = fma(m2.x, v2.y, fma(m2.y, v2.x, ai0));
+          ar1 = fma(m3.x, v3.x, fma(-m3.y, v3.y, ar1));
+          ai1 = fma(m3.x, v3.y, fma(m3.y, v3.x, ai1));
+        }
+        for (; c < b; c += nsl) {
+          const double2 m0 = R[(c - a) * r + t], v0 = mv[c];
+          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
+          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
+        }
+      }
+      {  // column pass: slot[c] = sum_t M[t, c] m_B[t] over the stage's whole columns
+        const int ncs = b - a;
+        int g = 32;
+        while (g > 1 && g * ncs > kMSConsumers) g >>= 1;
+        const int per_round = kMSConsumers / g, i = j & (g - 1);
+        for (int base = 0; base < ncs; base += per_round) {
+          const int cl = base + j / g;
+          double sr = 0.0, si = 0.0;
+          if (cl < ncs) {
+            const double2* col = R + cl * r;
+            for (int t = i; t < r; t += g) {
+              const double2 m = col[t], v = msf[t];
+              sr = fma(m.x, v.x, fma(-m.y, v.y, sr));
+              si = fma(m.x, v.y, fma(m.y, v.x, si));
+            }
+          }
+          for (int o = g >> 1; o > 0; o >>= 1) {
+            sr += __shfl_xor_sync(0xffffffffu, sr, o);
+            si += __shfl_xor_sync(0xffffffffu, si, o);
+          }
+          if (i == 0 && cl < ncs) slots[u.sp + u.c0 + a + cl] = make_double2(sr, si);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == kMSStages) {
+        stage = 0;
+        sphase ^= 1;
+      }
+      if (st == nst / 2) gather_issue(kidx, un, buf ^ 1);  // next unit's multipoles
+    }
+    if (u.flags & 2) {  // reduce the slices of each row, write u_B's own share
+      // (in mself[buf], free once every consumer has finished the unit's column passes; this keeps
+      // the CTA's shared memory small enough for two P2P CTAs beside two of these per SM)
+      double2* red = mself[buf];
+      consumers_sync();
+      red[j] = make_double2(ar0 + ar1, ai0 + ai1);
+      consumers_sync();
+      if (j < r) {
+        double sr = 0.0, si = 0.0;
+        for (int q = j; q < P; q += r) {
+          sr += red[q].x;
+          si += red[q].y;
+        }
+        loc[u.lo + j] = make_double2(sr, si);
+      }
+    }
+    u = un;
+    buf ^= 1;
+  }
+  cp_async_wait_all();
+}
+
+// loc[node] += sum of the column-sum slots the owners wrote for it (fixed order: deterministic).
+// One warp per receiving node.
+__global__ void m2l_slot_gather_kernel(int nodes, const int64_t* __restrict__ in_lo, const int32_t* __restrict__ in_rows,
+                                       const int32_t* __restrict__ in_ptr, const int64_t* __restrict__ in_off,
+                                       const double2* __restrict__ slots, double2* __restrict__ loc) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nodes) return;
+  const int r = in_rows[w], k0 = in_ptr[w], k1 = in_ptr[w + 1];
+  const int64_t lo = in_lo[w];
+  for (int c = lane; c < r; c += 32) {
+    double2 acc = loc[lo + c];
+    for (int k = k0; k < k1; ++k) {
+      const double2 v = ld2(slots + in_off[k] + c);
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    loc[lo + c] = acc;
+  }
+}
+
 // ---- near field P2P ------------------------------------------------------------
 // phi_t = sum_{j in N(leaf), j != t} H0(kappa |x_t - x_j|) v_j   (H0 units, tree order).
 // The leaf's own block is the first near entry (the only one with i == j pairs).
@@ -1388,7 +1661,7 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
             " free";
       return DAFMM_ENOMEM;
     }
-    if (tot > 0 && maxr <= kMaxStoredRows && (plan.opt.m2l_store == 1 || bytes <= free_b / 2)) {
+    if (tot > 0 && maxr <= kMaxStoredRows && (plan.opt.m2l_store == 1 || pk.m2l_sym || bytes <= free_b / 2)) {
       ok = upload(d, &d.m2l_mat_off, moff, err) && alloc(d, &d.m2l_mat, (size_t)tot, err);
       if (ok) {
         m2l_form_kernel<<<d.m2l_targets, kMSFormThreads>>>(d.m2l_loc_off, d.m2l_rows, d.m2l_stream_ptr,
@@ -1396,6 +1669,19 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
                                                          d.m2l_mat);
         ok = ck(cudaGetLastError(), err, "m2l_form_kernel") && ck(cudaDeviceSynchronize(), err, "m2l_form_kernel");
       }
+      if (!ok) return DAFMM_ECUDA;
+    }
+    if (pk.m2l_sym && !d.m2l_mat) {
+      err = "pair-stored M2L (m2l_store=2): the blocks could not be stored";
+      return DAFMM_ENOMEM;
+    }
+    if (pk.m2l_sym) {  // R22: own multipoles, column-sum slots, receiving nodes' slot lists
+      d.m2l_sym = 1;
+      d.m2l_in_nodes = (int)pk.m2l_in_lo.size();
+      ok = upload(d, &d.m2l_self_moff, pk.m2l_self_moff, err) && upload(d, &d.m2l_in_lo, pk.m2l_in_lo, err) &&
+           upload(d, &d.m2l_in_rows, pk.m2l_in_rows, err) && upload(d, &d.m2l_in_ptr, pk.m2l_in_ptr, err) &&
+           upload(d, &d.m2l_in_off, pk.m2l_in_off, err) &&
+           alloc(d, &d.m2l_slots, pk.m2l_stream_idx.size(), err);
       if (!ok) return DAFMM_ECUDA;
     }
   }
@@ -1409,6 +1695,10 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
     if (d.m2l_mat)
       ok = ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
               err, "stored M2L shared memory") &&
+           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
+              err, "pair M2L shared memory") &&
+           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
+              "carveout") &&
            ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
               "carveout") &&
            // the largest shared-memory carveout for P2P too, so an SM running three P2P CTAs has
@@ -1526,7 +1816,17 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   // M2L over targets [t0, t1) on stream st (ticket slot k for the on-the-fly kernel)
   auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
     if (t1 <= t0) return;
-    if (d.m2l_mat) {  // from the stored blocks
+    if (d.m2l_sym) {  // one block per node pair: row sums and column sums (R22)
+      m2l_pair_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, st>>>(
+          t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
+          d.m2l_self_moff + t0, d.m2l_mat, d.mult, d.loc, d.m2l_slots);
+      if (d.m2l_in_nodes > 0) {
+        m2l_slot_gather_kernel<<<(d.m2l_in_nodes + 7) / 8, 256, 0, st>>>(d.m2l_in_nodes, d.m2l_in_lo, d.m2l_in_rows,
+                                                                        d.m2l_in_ptr, d.m2l_in_off, d.m2l_slots,
+                                                                        d.loc);
+        ++d.launches;
+      }
+    } else if (d.m2l_mat) {  // from the stored blocks
       m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, st>>>(
           t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
           d.m2l_mat, d.mult, d.loc);
@@ -1543,7 +1843,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   // deepest level (the only other kernel touching those local expansions).  Measured slower
   // with stored blocks at C4 (4.18 vs 3.71 ms: two M2L launches crowd the P2P; profiles/README.md),
   // so it is off by default.
-  const int nleaf = (DAFMM_LEAF_SPLIT && far && fork && d.l2l.size() > 0) ? d.m2l_leaf_targets : 0;
+  const int nleaf = (DAFMM_LEAF_SPLIT && far && fork && d.l2l.size() > 0 && !d.m2l_sym) ? d.m2l_leaf_targets : 0;
   if (nleaf > 0) {
     cudaEventRecord(d.ev_p2m, fs);
     cudaStreamWaitEvent(d.s_leaf, d.ev_p2m, 0);

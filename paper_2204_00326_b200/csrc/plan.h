@@ -25,7 +25,7 @@ struct Options {
   int num_threads = 0;     // host setup threads (0: OpenMP default)
   int host_only = 0;       // skip the device upload
   int symmetric_pivots = 0;  // reading R19 (option): one ACA per node, outgoing skeleton = incoming
-  int m2l_store = -1;        // M2L blocks: -1 auto, 0 evaluated on the fly every matvec, 1 stored in HBM
+  int m2l_store = -1;        // M2L blocks: -1 auto, 0 on the fly every matvec, 1 stored in HBM, 2 stored per pair (R22)
   int hfr_parent_search = 0;  // reading R7b (option): HFR search sets also take the parent's far children
 };
 
@@ -138,12 +138,26 @@ struct Packed {
   int max_leaf = 0;
   // statistics
   int64_t p2p_pairs = 0, m2l_entries = 0, m2l_pairs = 0;
+  // symmetric stored M2L (reading R22, m2l_store = 2): with one skeleton per node (R19) the block
+  // of (B <- A) is the transpose of the block of (A <- B), so every unordered pair {A, B} of
+  // interaction-list nodes keeps ONE block, in the stream of its owner (the node with the lower
+  // id at the level).  The owner's CTA applies it twice: row sums into its own local
+  // expansion, column sums (with its own multipole) into per-stream-position slots, which a
+  // gather adds to the other node's local expansion.
+  int m2l_sym = 0;
+  int64_t m2l_stored_entries = 0;    // entries of the stored blocks (m2l_entries / 2 when m2l_sym)
+  std::vector<int64_t> m2l_self_moff;  // per target: its own multipole (column sums)
+  std::vector<int64_t> m2l_in_lo;      // per receiving node: local-expansion offset
+  std::vector<int32_t> m2l_in_rows;    // per receiving node: its rank
+  std::vector<int32_t> m2l_in_ptr;     // receiving nodes + 1
+  std::vector<int64_t> m2l_in_off;     // slot (stream position) of the node's first pivot in each owner stream
 };
 
 // setup.cpp
 int build_plan(Plan& plan, const double* points, const double* weights, const double* q, int64_t n,
                double kappa, int leaf_size, double nca_tol, const Options& opt, std::string& err);
-int pack_plan(const Plan& plan, Packed& pk, std::string& err);
+// device_free: free device bytes for the auto choice of the symmetric stored M2L (0: unknown)
+int pack_plan(const Plan& plan, Packed& pk, std::string& err, size_t device_free = 0);
 int export_plan(const Plan& plan, const std::string& dir, std::string& err);
 
 }  // namespace dafmm

@@ -659,7 +659,7 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
 // ============================================================================================
 // Packing: node offsets, pivot coordinates, operator blocks (P:427-562 in the G-only form of
 // DESIGN.md §Operators), and the per-pass work lists.
-int pack_plan(const Plan& P, Packed& pk, std::string& err) {
+int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   double t0 = now_s();
   const int L = P.L;
   const int64_t n = P.n;
@@ -843,6 +843,48 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       if (!t.src.empty()) tg.push_back(std::move(t));
     }
   }
+  // symmetric stored M2L (R22): keep only the pairs the target owns (source id > target id at
+  // the level; the interaction lists are symmetric, so every unordered pair is kept once)
+  {
+    int maxr = 0;
+    int64_t half = 0;
+    for (auto& t : tg) {
+      const int ri = (int)P.piv[t.level][t.node].ti.size();
+      maxr = std::max(maxr, ri);
+      for (int sn : t.src)
+        if (sn > t.node) half += (int64_t)ri * (int64_t)P.piv[t.level][sn].so.size();
+    }
+    const bool fits = device_free == 0 || (size_t)half * 16 <= device_free / 2;
+    if (P.opt.m2l_store == 2) {
+      if (!P.opt.symmetric_pivots) {
+        err = "m2l_store=2 (blocks per node pair) needs symmetric_pivots=1 (one skeleton per node)";
+        return DAFMM_EINVAL;
+      }
+      if (maxr > 128) {
+        err = "m2l_store=2: a node has " + std::to_string(maxr) + " pivots (at most 128 supported)";
+        return DAFMM_EINVAL;
+      }
+      if (device_free && (size_t)half * 16 > device_free) {
+        err = "m2l_store=2: the M2L pair blocks need " + std::to_string(half * 16) + " bytes";
+        return DAFMM_ENOMEM;
+      }
+    }
+    pk.m2l_sym = (P.opt.m2l_store == 2 || (P.opt.m2l_store == -1 && P.opt.symmetric_pivots && maxr <= 128 && fits))
+                     ? 1 : 0;
+    if (pk.m2l_sym) {
+      // incoming slots of every node: (owner target, position of the node's block in its stream)
+      for (auto& t : tg) {
+        std::vector<int> kept;
+        for (int sn : t.src)
+          if (sn > t.node) kept.push_back(sn);
+        t.src.swap(kept);
+      }
+      std::vector<M2LTarget> keep;
+      for (auto& t : tg)
+        if (!t.src.empty()) keep.push_back(std::move(t));
+      tg.swap(keep);
+    }
+  }
   std::vector<std::vector<int>> codes(tg.size());
 #pragma omp parallel for schedule(dynamic, 16)
   for (size_t i = 0; i < tg.size(); ++i) {
@@ -883,12 +925,15 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
   pk.m2l_src_ptr.push_back(0);
   pk.m2l_item_ptr.push_back(0);
   pk.m2l_stream_ptr.push_back(0);
+  // R22: per level, (receiving node, slot of its first pivot in the owner's stream)
+  std::vector<std::vector<std::pair<int, int64_t>>> in_lists((size_t)L + 1);
   for (size_t i : torder) {
     const int l = tg[i].level;
     const int ri = (int)P.piv[l][tg[i].node].ti.size();
     std::vector<int> order(tg[i].src.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return codes[i][a] < codes[i][b]; });
+    const int64_t stream0 = (int64_t)pk.m2l_stream_idx.size();
     int prev = -1;
     int32_t cum = 0;  // offset in the target's source-pivot stream
     for (int e : order) {
@@ -903,18 +948,37 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err) {
       }
       pk.m2l_src_off.push_back(moff[l][sn]);
       pk.m2l_src_cnt.push_back(ro);
+      if (pk.m2l_sym) in_lists[(size_t)l].push_back({sn, stream0 + cum});
       for (int k = 0; k < ro; ++k) pk.m2l_stream_idx.push_back((int32_t)(moff[l][sn] + k));
       cum += ro;
-      pk.m2l_entries += (int64_t)ri * ro;
-      pk.m2l_band_entries[code] += (int64_t)ri * ro;
-      ++pk.m2l_pairs;
+      const int64_t uses = pk.m2l_sym ? 2 : 1;  // a pair block serves both directions
+      pk.m2l_entries += uses * (int64_t)ri * ro;
+      pk.m2l_stored_entries += (int64_t)ri * ro;
+      pk.m2l_band_entries[code] += uses * (int64_t)ri * ro;
+      pk.m2l_pairs += uses;
     }
     pk.m2l_item_end.push_back(cum);
     pk.m2l_item_ptr.push_back((int32_t)pk.m2l_item_code.size());
     pk.m2l_loc_off.push_back(loff[l][tg[i].node]);
+    pk.m2l_self_moff.push_back(moff[l][tg[i].node]);
     pk.m2l_rows.push_back(ri);
     pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
     pk.m2l_stream_ptr.push_back((int64_t)pk.m2l_stream_idx.size());
+  }
+  if (pk.m2l_sym) {  // R22: the slot lists of every receiving node, level by level, by node id
+    pk.m2l_in_ptr.assign(1, 0);
+    for (int l = 1; l <= L; ++l) {
+      auto& v = in_lists[(size_t)l];
+      std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+      for (size_t a = 0; a < v.size();) {
+        size_t b = a;
+        while (b < v.size() && v[b].first == v[a].first) pk.m2l_in_off.push_back(v[b++].second);
+        pk.m2l_in_lo.push_back(loff[l][v[a].first]);
+        pk.m2l_in_rows.push_back((int32_t)P.piv[l][v[a].first].ti.size());
+        pk.m2l_in_ptr.push_back((int32_t)pk.m2l_in_off.size());
+        a = b;
+      }
+    }
   }
   // leaves (every level, coarse first): near field and L2P.  The near field of a leaf B at
   // level l is every source leaf C whose ancestor at level min(l, l_C) neighbours B's (P:750-755,

@@ -218,3 +218,35 @@ def test_gpu_r7_substitute_lists(tmp_path):
     assert _rel(y - x, y_cpu - x) <= 1e-11
     yd = oracle.dense_matvec(prob, x)
     assert _rel(y - x, yd - x) <= 10 * P["nca_tol"]
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 20.0), ("c3", 128, 20.0),
+                                          ("c1", 128, 4.0), ("c1", 40, 7.0), ("c5", 5, 12.0),
+                                          ("c2", 64, 40.0), ("c2", 128, 40.0)])
+def test_gpu_pair_stored_m2l(name, n, kappa, tmp_path):
+    """m2l_store=2 (reading R22): one stored block per unordered interaction-list pair, applied as
+    row sums and column sums, with one skeleton per node (symmetric_pivots=1, R19).  Against the
+    oracle's serial DAFMM on the same pivots (<= 1e-11), the on-the-fly M2L on the same plan
+    (<= 1e-13), dense rows (<= 10 nca_tol); deterministic; near + far = full."""
+    P = make_problem(name, n=n, kappa=kappa)
+    kw = dict(symmetric_pivots=1)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=2, **kw)
+    st = op.stats()
+    assert st["m2l_stored"] == 2 and 2 * st["m2l_stored_entries"] == st["m2l_entries"]
+    assert st["m2l_store_bytes"] == 16 * st["m2l_stored_entries"]
+    prob, nca = _oracle_on_product_plan(P, op, tmp_path)
+    x = P["x"]
+    y = _gpu_matvec(op, x)
+    assert np.array_equal(y, _gpu_matvec(op, x))
+    y_cpu = nca.matvec(x)
+    assert _rel(y - x, y_cpu - x) <= 1e-11
+    assert _leaf_rel_max(y, y_cpu, x, prob, nca.tree) <= 1e-9
+    op_fly = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=0, **kw)
+    assert op_fly.stats()["m2l_entries"] == st["m2l_entries"]
+    assert _rel(_gpu_matvec(op_fly, x) - x, y - x) <= 1e-13
+    rows = np.arange(0, prob.n, 3)
+    yd = oracle.dense_matvec_rows(prob, x, rows)
+    assert _rel(y[rows] - x[rows], yd - x[rows]) <= 10 * P["nca_tol"]
+    near = _gpu_matvec(op, x, 1)
+    far = _gpu_matvec(op, x, 2)
+    assert _rel(near + far, y) <= 1e-14

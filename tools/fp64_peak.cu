@@ -22,14 +22,18 @@ int main() {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   dfma_kernel<<<blocks, threads>>>(out, 100, 0.999999, 1e-7);
   cudaDeviceSynchronize();
-  for (long iters : {4000L, 80000L}) {
+  // burst (~9 ms), ~0.18 s, and a sustained run of 25 back-to-back ~0.18 s launches (~4.5 s,
+  // clocks sampled by the caller with nvidia-smi)
+  for (long iters : {4000L, 80000L, -80000L}) {
+    const int reps = iters < 0 ? 25 : 1;
+    if (iters < 0) iters = -iters;
     cudaEventRecord(e0);
-    dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+    for (int r = 0; r < reps; ++r) dfma_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
-    double dfma = (double)blocks * threads * iters * 16 * 8;
-    printf("{\"iters\": %ld, \"ms\": %.3f, \"dfma_per_s\": %.4e, \"fp64_tflops\": %.3f, \"dfma_per_clk_per_sm_at_1965\": %.2f}\n",
-           iters, ms, dfma / (ms * 1e-3), 2 * dfma / (ms * 1e-3) / 1e12, dfma / (ms * 1e-3) / sms / 1.965e9);
+    double dfma = (double)blocks * threads * iters * 16 * 8 * reps;
+    printf("{\"iters\": %ld, \"launches\": %d, \"ms\": %.3f, \"dfma_per_s\": %.4e, \"fp64_tflops\": %.3f, \"dfma_per_clk_per_sm_at_1965\": %.2f}\n",
+           iters, reps, ms, dfma / (ms * 1e-3), 2 * dfma / (ms * 1e-3) / 1e12, dfma / (ms * 1e-3) / sms / 1.965e9);
   }
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) { printf("err %s\n", cudaGetErrorString(err)); return 1; }
