@@ -77,6 +77,7 @@ struct DevPlan {
   // pair-stored M2L (Packed::m2l_sym, reading R22): own multipole of each target (column sums),
   // the column-sum slots (one per stream position) and the receiving nodes' slot lists
   int m2l_sym = 0;
+  int m2l_pair_grid = 0;
   int64_t* m2l_self_moff = nullptr;
   double2* m2l_slots = nullptr;
   int m2l_in_nodes = 0;

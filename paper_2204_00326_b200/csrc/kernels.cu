@@ -948,12 +948,27 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
 // sums of a stage are complete in shared memory: after the row pass over a stage, the consumers
 // re-read it column-wise (g threads per column, xor-shuffle reduced) -- a second shared-memory
 // read of the stage instead of a second HBM read of the block.
+#ifndef DAFMM_PC
+#define DAFMM_PC 256  // pair-M2L consumer threads (8 warps): one CTA per SM
+#endif
+#ifndef DAFMM_P_MINB
+#define DAFMM_P_MINB 3  // register cap 72: two P2P CTAs fit beside the pair-M2L CTA
+#endif
+#ifndef DAFMM_PSTAGES
+#define DAFMM_PSTAGES 6
+#endif
+constexpr int kPC = DAFMM_PC;
+constexpr int kPThreads = kPC + 32;
+constexpr int kPStages = DAFMM_PSTAGES;
+constexpr int kPIdx = kMSCols / kPC;
+constexpr size_t kPDynSmem = sizeof(double2) * kPStages * kMSStageE;
+static_assert(kMSCols % kPC == 0, "multipole gather: whole indices per thread");
 struct MSPUnit {
   int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
   int r, pad;
   int64_t sp, lo, self_m;  // stream offset, output offset, own multipole
 };
-__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
+__global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
     int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
     const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
     const int64_t* __restrict__ mat_off, const int64_t* __restrict__ self_moff, const double2* __restrict__ mat,
@@ -962,23 +977,23 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
   double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
   __shared__ __align__(16) double2 mb[2][kMSCols];
   __shared__ __align__(16) double2 mself[2][kMaxStoredRows];
-  static_assert(kMaxStoredRows == kMSConsumers, "the row reduction reuses mself[buf]");
-  __shared__ __align__(8) uint64_t full[kMSStages], empty[kMSStages], ufull[kMSUnits], uempty[kMSUnits];
+  static_assert(kPC <= kMSCols, "the row reduction reuses mb[buf]");
+  __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], ufull[kMSUnits], uempty[kMSUnits];
   __shared__ MSPUnit units[kMSUnits];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kMSStages; ++i) {
+    for (int i = 0; i < kPStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kMSConsumers / 32);
+      mbar_init(&empty[i], kPC / 32);
     }
     for (int i = 0; i < kMSUnits; ++i) {
       mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], kMSConsumers / 32);
+      mbar_init(&uempty[i], kPC / 32);
     }
     mbar_fence_init();
   }
   __syncthreads();
-  if (warp == kMSConsumers / 32) {  // ---- producer (one lane)
+  if (warp == kPC / 32) {  // ---- producer (one lane)
     if (lane != 0) return;
     int stage = 0, uslot = 0;
     uint32_t sphase = 0, uphase = 0;
@@ -1043,7 +1058,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
         mbar_wait(&empty[stage], sphase ^ 1);
         mbar_arrive_tx(&full[stage], (uint32_t)cnt * 16u);
         bulk_load(ring[stage], src + (int64_t)cc * cur.r, (uint32_t)cnt * 16u, &full[stage]);
-        if (++stage == kMSStages) {
+        if (++stage == kPStages) {
           stage = 0;
           sphase ^= 1;
         }
@@ -1071,22 +1086,22 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
   auto gather_idx = [&](const MSPUnit& u, int* kidx) {
     const int64_t sp = u.sp + u.c0;
 #pragma unroll
-    for (int k = 0; k < kMSIdx; ++k) {
-      const int c = j + k * kMSConsumers;
+    for (int k = 0; k < kPIdx; ++k) {
+      const int c = j + k * kPC;
       kidx[k] = (u.tgt >= 0 && c < u.c1 - u.c0) ? __ldg(stream_idx + sp + c) : -1;
     }
   };
   auto gather_issue = [&](const int* kidx, const MSPUnit& u, int b) {
 #pragma unroll
-    for (int k = 0; k < kMSIdx; ++k)
-      if (kidx[k] >= 0) cp_async16(&mb[b][j + k * kMSConsumers], mult + kidx[k]);
+    for (int k = 0; k < kPIdx; ++k)
+      if (kidx[k] >= 0) cp_async16(&mb[b][j + k * kPC], mult + kidx[k]);
     if (u.tgt >= 0 && j < u.r) cp_async16(&mself[b][j], mult + u.self_m + j);  // own multipole
     cp_async_commit();
   };
   int nsl = 0, P = 1, buf = 0, sl = 0;
   bool act = false;
   double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
-  int kidx[kMSIdx];
+  int kidx[kPIdx];
   MSPUnit u = take();
   gather_idx(u, kidx);
   gather_issue(kidx, u, 0);
@@ -1095,7 +1110,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
     gather_idx(un, kidx);
     const int r = u.r;
     if (u.flags & 1) {
-      nsl = kMSConsumers / r;
+      nsl = kPC / r;
       P = nsl * r;
       sl = j / r;
       act = j < P;
@@ -1108,7 +1123,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
     const int nc = u.c1 - u.c0;
     const int cps = kMSStageE / r;
     const int nst = (nc + cps - 1) / cps;
-    // column pass geometry: g threads per column (power of 2, <= 32), kMSConsumers / g columns
+    // column pass geometry: g threads per column (power of 2, <= 32), kPC / g columns
     // per round
     for (int st = 0; st < nst; ++st) {
       const int a = st * cps, b = min(nc, a + cps);
@@ -1137,22 +1152,32 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
           ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
         }
       }
-      {  // column pass: slot[c] = sum_t M[t, c] m_B[t] over the stage's whole columns
+      {  // column pass: slot[c] = sum_t M[t, c] m_B[t] over the stage's whole columns; items
+         // (column, part i < g), g threads per column (a power of 2: lane-aligned groups)
         const int ncs = b - a;
-        int g = 32;
-        while (g > 1 && g * ncs > kMSConsumers) g >>= 1;
-        const int per_round = kMSConsumers / g, i = j & (g - 1);
-        for (int base = 0; base < ncs; base += per_round) {
-          const int cl = base + j / g;
-          double sr = 0.0, si = 0.0;
+        int g = 1;
+        while (g < 32 && 2 * g * ncs <= kPC) g <<= 1;
+        const int i = j & (g - 1);
+        for (int it = j; it < ((ncs * g + kPC - 1) / kPC) * kPC; it += kPC) {
+          const int cl = it / g;
+          double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
           if (cl < ncs) {
             const double2* col = R + cl * r;
-            for (int t = i; t < r; t += g) {
-              const double2 m = col[t], v = msf[t];
-              sr = fma(m.x, v.x, fma(-m.y, v.y, sr));
-              si = fma(m.x, v.y, fma(m.y, v.x, si));
+            int t = i;
+            for (; t + g < r; t += 2 * g) {
+              const double2 m0 = col[t], v0 = msf[t], m1 = col[t + g], v1 = msf[t + g];
+              sr0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, sr0));
+              si0 = fma(m0.x, v0.y, fma(m0.y, v0.x, si0));
+              sr1 = fma(m1.x, v1.x, fma(-m1.y, v1.y, sr1));
+              si1 = fma(m1.x, v1.y, fma(m1.y, v1.x, si1));
+            }
+            if (t < r) {
+              const double2 m0 = col[t], v0 = msf[t];
+              sr0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, sr0));
+              si0 = fma(m0.x, v0.y, fma(m0.y, v0.x, si0));
             }
           }
+          double sr = sr0 + sr1, si = si0 + si1;
           for (int o = g >> 1; o > 0; o >>= 1) {
             sr += __shfl_xor_sync(0xffffffffu, sr, o);
             si += __shfl_xor_sync(0xffffffffu, si, o);
@@ -1162,16 +1187,15 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_pair_kernel(
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == kMSStages) {
+      if (++stage == kPStages) {
         stage = 0;
         sphase ^= 1;
       }
       if (st == nst / 2) gather_issue(kidx, un, buf ^ 1);  // next unit's multipoles
     }
     if (u.flags & 2) {  // reduce the slices of each row, write u_B's own share
-      // (in mself[buf], free once every consumer has finished the unit's column passes; this keeps
-      // the CTA's shared memory small enough for two P2P CTAs beside two of these per SM)
-      double2* red = mself[buf];
+      // (in mb[buf], free once every consumer has finished the unit's passes)
+      double2* red = mb[buf];
       consumers_sync();
       red[j] = make_double2(ar0 + ar1, ai0 + ai1);
       consumers_sync();
@@ -1692,10 +1716,11 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
          ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
     d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
     d.m2l_store_grid = std::max(1, std::min(d.m2l_targets, DAFMM_MS_PER_SM * sms));
+    d.m2l_pair_grid = std::max(1, std::min(d.m2l_targets, sms));
     if (d.m2l_mat)
       ok = ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
               err, "stored M2L shared memory") &&
-           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
+           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPDynSmem),
               err, "pair M2L shared memory") &&
            ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
               "carveout") &&
@@ -1817,7 +1842,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
     if (t1 <= t0) return;
     if (d.m2l_sym) {  // one block per node pair: row sums and column sums (R22)
-      m2l_pair_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, st>>>(
+      m2l_pair_kernel<<<d.m2l_pair_grid, kPThreads, kPDynSmem, st>>>(
           t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
           d.m2l_self_moff + t0, d.m2l_mat, d.mult, d.loc, d.m2l_slots);
       if (d.m2l_in_nodes > 0) {

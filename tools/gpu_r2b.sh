@@ -1,0 +1,7 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "pair" > gpurun_out/pytest_pair.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_pair.log
+timeout 1500 python tools/mode_probe.py c4 '{}' '{"symmetric_pivots": 1, "m2l_store": 1}' '{"symmetric_pivots": 1, "m2l_store": 2}' > gpurun_out/probe_r2b.log 2>&1
+timeout 600 python tools/mode_probe.py c3 '{}' '{"symmetric_pivots": 1, "m2l_store": 2}' >> gpurun_out/probe_r2b.log 2>&1
+echo done
