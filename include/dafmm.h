@@ -87,6 +87,11 @@ typedef struct {
                           far field arriving through the directional L2L (L-shaped random points:
                           1.6e-4 vs dense with 0, 7.5e-9 with 1); on the uniform configs it costs
                           2x the ACA setup and 1.5% more M2L work for no accuracy gain. */
+  int setup_device;    /* 1 (default): the ACAs of the NCA setup run on the device, one
+                          CTA per (node, direction), level by level; the search sets are still built
+                          on the host.  0: on the host (OpenMP).  Host-only plans always use the
+                          host.  Both give valid pivots; they may differ where rounding breaks a
+                          tie of the ACA's argmax. */
 } dafmm_options;
 
 /* Statistics of a plan (sizes, ranks, setup times). */
@@ -210,6 +215,43 @@ int dafmm_pass_times(dafmm_handle h, double* ms_out, int64_t* matvecs_out, int64
  * (n < 0, null pointer with n > 0, band code out of range), DAFMM_ECUDA (launch). */
 int dafmm_h0_bands(double* zlo, double* zhi, int cap);
 int dafmm_h0_eval(const void* z2, void* h0, int64_t n, int band, void* stream);
+
+/* ---- HODLR preconditioner and hybrid solver (Eq. hybrid; readings HR1-HR4) ----
+ * Ã is a Hierarchically Off-Diagonal Low-Rank approximation of the handle's matrix A (kernel_mode
+ * 0) in the handle's tree order: a binary tree of midpoint splits of the tree positions with
+ * leaves of at most leaf_size points (HR1); the leaf diagonal blocks of A are kept dense, and
+ * every off-diagonal sibling block A[alpha, beta] is replaced by its cross approximation
+ * A[alpha, J] A[I, J]^{-1} A[I, beta] with pivots from partially pivoted ACA capped at rank
+ * `rank` ("apriori fixing the rank"; HR2).  Ã is factorised on the device by the recursive
+ * Sherman-Morrison-Woodbury form (HR3): O(N r log N) memory, O(N r log N) per solve.
+ *
+ * dafmm_hodlr_create: rank in [1, 32], leaf_size in [1, 64].  Synchronous.  The preconditioner
+ *   refers to the handle's device plan: destroy it before the handle.  Errors: DAFMM_EINVAL
+ *   (arguments, host-only plan, kernel_mode 1), DAFMM_ENOMEM / DAFMM_ECUDA, DAFMM_ESETUP
+ *   (singular leaf block, cross matrix or Woodbury factor).
+ * dafmm_hodlr_solve: x = Ã^{-1} b (the HODLR direct solver), b and x DEVICE pointers, n
+ *   complex128, caller order (b may equal x).  Enqueued on the handle's stream.
+ * dafmm_hodlr_export: writes hodlr_blocks.npy (nblocks x 5: depth, a, b, c, d for the block of
+ *   rows [a, b) and columns [c, d) of tree positions), hodlr_piv_ptr.npy, hodlr_I.npy,
+ *   hodlr_J.npy (pivots, tree positions), hodlr_perm.npy (tree position -> caller index) and
+ *   hodlr_meta.npy (rank, leaf_size, n) into directory `path`, for the oracle.
+ * ls_gmres_solve_prec: as ls_gmres_solve on the right-preconditioned system A Ã^{-1} u = f,
+ *   psi = Ã^{-1} u (HR4: the paper writes the left form; the right form keeps the GMRES residual
+ *   equal to the true residual ||A psi - f|| / ||f||).  p = NULL gives ls_gmres_solve. */
+typedef struct dafmm_hodlr_s* dafmm_hodlr;
+typedef struct {
+  int32_t rank, leaf_size, depths, leaves, max_rank;
+  double mean_rank;
+  int64_t device_bytes, aca_entries;
+  double setup_aca_s, setup_basis_s, setup_factor_s;
+} dafmm_hodlr_stats_t;
+int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, dafmm_hodlr* out);
+int dafmm_hodlr_solve(dafmm_hodlr p, const void* b, void* x);
+int dafmm_hodlr_stats(dafmm_hodlr p, dafmm_hodlr_stats_t* out);
+int dafmm_hodlr_export(dafmm_hodlr p, const char* path);
+void dafmm_hodlr_destroy(dafmm_hodlr p);
+int ls_gmres_solve_prec(dafmm_handle h, dafmm_hodlr p, const void* f, void* psi, double tol, int maxit, int restart,
+                        int* iters_out, double* relres_out, double* history);
 
 /* Write the tree, lists, cones and pivot index sets as .npy files into directory `path`
  * (created if missing) for the independent CPU oracle.  Synchronous, host only. */

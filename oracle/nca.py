@@ -85,15 +85,19 @@ def aca(row_fn, col_fn, m, n, eps, max_rank=200):
     return rows, cols
 
 
-def aca_pivots(prob, t_set, s_set, eps):
-    """Pivots (t_piv, s_piv) of A[t_set, s_set] by ACA; empty sets give rank 0 (R11)."""
+def aca_pivots(prob, t_set, s_set, eps, compress="K"):
+    """Pivots (t_piv, s_piv) of K[t_set, s_set] by ACA; empty sets give rank 0 (R11).
+    compress="A" is the ablation of reading R9: the ACA sees the rows of A = I + kappa^2 diag(q) K
+    (off-diagonal: kappa^2 q_i K_ij), as P:353-360 literally say; tests/test_oracle_nca.py shows
+    why the product compresses K."""
     t_set = np.asarray(t_set, dtype=np.int64)
     s_set = np.asarray(s_set, dtype=np.int64)
     if t_set.size == 0 or s_set.size == 0:
         e = np.zeros(0, dtype=np.int64)
         return e, e
-    rows, cols = aca(lambda i: K_block(prob, t_set[i:i + 1], s_set)[0],
-                     lambda j: K_block(prob, t_set, s_set[j:j + 1])[:, 0],
+    rs = prob.kappa ** 2 * prob.q[t_set] if compress == "A" else np.ones(t_set.size)
+    rows, cols = aca(lambda i: rs[i] * K_block(prob, t_set[i:i + 1], s_set)[0],
+                     lambda j: rs * K_block(prob, t_set, s_set[j:j + 1])[:, 0],
                      t_set.size, s_set.size, eps)
     return t_set[np.asarray(rows, dtype=np.int64)], s_set[np.asarray(cols, dtype=np.int64)]
 
@@ -148,7 +152,7 @@ class NCA:
     (ACA ties, rounding), so parity with the product is taken on the product's pivots after
     checking them."""
 
-    def __init__(self, prob, tree, lists, eps, pivots=None, hfr_parent_search=False):
+    def __init__(self, prob, tree, lists, eps, pivots=None, hfr_parent_search=False, compress="K"):
         # reading R17: nested-basis errors compound over the LFR levels of an adaptive tree, so
         # the ACA runs at eps / 2 when leaves lie on several levels
         if len({l for l, _ in tree.all_leaves()}) > 1:
@@ -165,8 +169,8 @@ class NCA:
                 for node in sorted(lists.active[level], key=lambda nd: (not is_leaf_node(tree, level, nd), nd)):
                     ts = self.search_sets(level, node)
                     self.search[level][node] = ts
-                    ti, si = aca_pivots(prob, ts["ti"], ts["si"], eps)
-                    to, so = aca_pivots(prob, ts["to"], ts["so"], eps)
+                    ti, si = aca_pivots(prob, ts["ti"], ts["si"], eps, compress)
+                    to, so = aca_pivots(prob, ts["to"], ts["so"], eps, compress)
                     self.pivots[level][node] = dict(ti=ti, si=si, to=to, so=so)
         else:
             self.pivots = pivots

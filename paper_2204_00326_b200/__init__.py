@@ -8,4 +8,6 @@ is missing (run ``python -m paper_2204_00326_b200.build`` or ``__graft_entry__.b
 from .binding import (DAFMMError, Options, Stats, dafmm_create, dafmm_create_ex, dafmm_matvec,  # noqa: F401
                       dafmm_matvec_parts, dafmm_matvec_host, ls_gmres_solve, dafmm_set_stream, dafmm_stats,
                       dafmm_export_plan, dafmm_destroy, dafmm_last_error, dafmm_set_profiling,
-                      dafmm_pass_times, dafmm_h0_bands, dafmm_h0_eval, library_path, load, DAFMM, EXPORTED, PASS_NAMES)
+                      dafmm_pass_times, dafmm_h0_bands, dafmm_h0_eval, library_path, load, DAFMM, EXPORTED, PASS_NAMES, HODLR, HodlrStats,
+                      dafmm_hodlr_create, dafmm_hodlr_solve, dafmm_hodlr_stats, dafmm_hodlr_export,
+                      dafmm_hodlr_destroy, ls_gmres_solve_prec)

@@ -15,7 +15,8 @@ _lib = None
 EXPORTED = ["dafmm_default_options", "dafmm_create", "dafmm_create_ex", "dafmm_matvec", "dafmm_matvec_parts",
             "dafmm_matvec_host", "ls_gmres_solve", "dafmm_set_stream", "dafmm_stats", "dafmm_export_plan",
             "dafmm_destroy", "dafmm_last_error", "dafmm_set_profiling", "dafmm_pass_times", "dafmm_h0_bands",
-            "dafmm_h0_eval"]
+            "dafmm_h0_eval", "dafmm_hodlr_create", "dafmm_hodlr_solve", "dafmm_hodlr_stats", "dafmm_hodlr_export",
+            "dafmm_hodlr_destroy", "ls_gmres_solve_prec"]
 
 NUM_PASSES = 9
 PASS_NAMES = ["gather", "p2m", "m2m", "m2l", "l2l", "near", "combine", "overlap_span", "m2l_leaf"]
@@ -34,7 +35,7 @@ class Options(ctypes.Structure):
     _fields_ = [("T", ctypes.c_double), ("self_term", ctypes.c_int), ("kernel_mode", ctypes.c_int),
                 ("max_level", ctypes.c_int), ("num_threads", ctypes.c_int), ("host_only", ctypes.c_int),
                 ("symmetric_pivots", ctypes.c_int), ("m2l_store", ctypes.c_int),
-                ("hfr_parent_search", ctypes.c_int)]
+                ("hfr_parent_search", ctypes.c_int), ("setup_device", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):
@@ -57,6 +58,16 @@ class Stats(ctypes.Structure):
         for k in ("m2l_band_entries", "p2p_band_entries"):
             d[k] = list(d[k])
         return d
+
+
+class HodlrStats(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int32), ("leaf_size", ctypes.c_int32), ("depths", ctypes.c_int32),
+                ("leaves", ctypes.c_int32), ("max_rank", ctypes.c_int32), ("mean_rank", ctypes.c_double),
+                ("device_bytes", ctypes.c_int64), ("aca_entries", ctypes.c_int64), ("setup_aca_s", ctypes.c_double),
+                ("setup_basis_s", ctypes.c_double), ("setup_factor_s", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 def library_path():
@@ -86,6 +97,13 @@ def load():
     lib.dafmm_pass_times.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.dafmm_h0_bands.argtypes = [vp, vp, i32]
     lib.dafmm_h0_eval.argtypes = [vp, vp, i64, i32, vp]
+    lib.dafmm_hodlr_create.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    lib.dafmm_hodlr_solve.argtypes = [vp, vp, vp]
+    lib.dafmm_hodlr_stats.argtypes = [vp, ctypes.POINTER(HodlrStats)]
+    lib.dafmm_hodlr_export.argtypes = [vp, ctypes.c_char_p]
+    lib.dafmm_hodlr_destroy.argtypes = [vp]
+    lib.dafmm_hodlr_destroy.restype = None
+    lib.ls_gmres_solve_prec.argtypes = [vp, vp, vp, vp, dbl, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(dbl), vp]
     lib.dafmm_destroy.argtypes = [vp]
     lib.dafmm_destroy.restype = None
     lib.dafmm_last_error.restype = ctypes.c_char_p
@@ -200,6 +218,51 @@ def ls_gmres_solve(h, f, psi, tol, maxit, restart=50, history=None):
     return rc, it.value, rr.value
 
 
+def _history_ptr(history, maxit):
+    if history is None:
+        return None
+    if history.dtype != np.float64 or history.size < maxit + 1:
+        raise ValueError("history must be float64 with maxit + 1 entries")
+    return history.ctypes.data_as(ctypes.c_void_p)
+
+
+def dafmm_hodlr_create(h, rank, leaf_size=64):
+    p = ctypes.c_void_p()
+    _check(load().dafmm_hodlr_create(h, int(rank), int(leaf_size), ctypes.byref(p)))
+    return p
+
+
+def dafmm_hodlr_solve(p, h, b, x):
+    """x = Ã^{-1} b on the device (h: the owning DAFMM handle, for the length check)."""
+    n = _n_of(h)
+    return _check(load().dafmm_hodlr_solve(p, _dev(b, n), _dev(x, n)))
+
+
+def dafmm_hodlr_stats(p):
+    s = HodlrStats()
+    _check(load().dafmm_hodlr_stats(p, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def dafmm_hodlr_export(p, path):
+    return _check(load().dafmm_hodlr_export(p, str(path).encode()))
+
+
+def dafmm_hodlr_destroy(p):
+    if p:
+        load().dafmm_hodlr_destroy(p)
+
+
+def ls_gmres_solve_prec(h, p, f, psi, tol, maxit, restart=50, history=None):
+    """Right-preconditioned GMRES (HR4); returns (status, iterations, true relative residual)."""
+    it = ctypes.c_int()
+    rr = ctypes.c_double()
+    n = _n_of(h)
+    rc = _check(load().ls_gmres_solve_prec(h, p, _dev(f, n), _dev(psi, n), float(tol), int(maxit), int(restart),
+                                           ctypes.byref(it), ctypes.byref(rr), _history_ptr(history, maxit)))
+    return rc, it.value, rr.value
+
+
 def dafmm_set_stream(h, stream):
     """stream: a torch.cuda.Stream or a raw cudaStream_t integer."""
     ptr = stream if isinstance(stream, int) else stream.cuda_stream
@@ -278,7 +341,10 @@ class DAFMM:
         dafmm_matvec_host(self.h, x_host, y_host)
         return y_host
 
-    def gmres(self, f, psi, tol, maxit, restart=50, history=None):
+    def gmres(self, f, psi, tol, maxit, restart=50, history=None, prec=None):
+        """prec: a HODLR of this operator (right preconditioning, HR4) or None."""
+        if prec is not None:
+            return ls_gmres_solve_prec(self.h, prec.p, f, psi, tol, maxit, restart, history)
         return ls_gmres_solve(self.h, f, psi, tol, maxit, restart, history)
 
     def stats(self):
@@ -297,6 +363,36 @@ class DAFMM:
         if self.h:
             dafmm_destroy(self.h)
             self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HODLR:
+    """Owning wrapper of the HODLR preconditioner of a DAFMM operator:
+    ``pc = HODLR(op, rank=16, leaf_size=64); pc.solve(b, x); op.gmres(f, psi, tol, maxit, prec=pc)``."""
+
+    def __init__(self, op, rank=16, leaf_size=64):
+        self.op = op  # keeps the owning handle alive
+        self.p = dafmm_hodlr_create(op.h, rank, leaf_size)
+
+    def solve(self, b, x):
+        dafmm_hodlr_solve(self.p, self.op.h, b, x)
+        return x
+
+    def stats(self):
+        return dafmm_hodlr_stats(self.p)
+
+    def export(self, path):
+        dafmm_hodlr_export(self.p, path)
+
+    def close(self):
+        if self.p:
+            dafmm_hodlr_destroy(self.p)
+            self.p = None
 
     def __del__(self):
         try:

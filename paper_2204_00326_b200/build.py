@@ -20,7 +20,7 @@ if os.environ.get("DAFMM_LIB_NAME"):
     LIB = os.path.join(OUT_DIR, os.environ["DAFMM_LIB_NAME"])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["kernels.cu"]
+CU_SOURCES = ["kernels.cu", "setup_device.cu", "hodlr.cu"]
 CPP_SOURCES = ["setup.cpp", "capi.cpp"]
 
 

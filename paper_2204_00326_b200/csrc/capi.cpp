@@ -11,6 +11,7 @@
 #include "dafmm.h"
 #include "device.h"
 #include "hankel.cuh"
+#include "hodlr.h"
 #include "plan.h"
 
 struct dafmm_plan {
@@ -21,6 +22,11 @@ struct dafmm_plan {
   int m2l_sym = 0;
   int p2p_sym = 0;
   std::vector<int64_t> m2l_band, p2p_band;
+};
+
+struct dafmm_hodlr_s {
+  dafmm_plan* owner = nullptr;
+  dafmm::HodlrPlan hp;
 };
 
 namespace {
@@ -50,6 +56,7 @@ void dafmm_default_options(dafmm_options* opt) {
   opt->symmetric_pivots = o.symmetric_pivots;
   opt->m2l_store = o.m2l_store;
   opt->hfr_parent_search = o.hfr_parent_search;
+  opt->setup_device = o.setup_device;
 }
 
 int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
@@ -67,6 +74,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.symmetric_pivots = opt->symmetric_pivots;
     o.m2l_store = opt->m2l_store;
     o.hfr_parent_search = opt->hfr_parent_search;
+    o.setup_device = opt->setup_device;
     if (o.m2l_store < -1 || o.m2l_store > 2) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0, 1 or 2");
   }
   std::unique_ptr<dafmm_plan> h;
@@ -96,7 +104,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
       }
       h->plan.t_upload = now_s() - t1;
     }
-    h->operator_bytes = (int64_t)pk.ops.size() * 16;
+    h->operator_bytes = (int64_t)pk.ops_len * 16;
     h->p2p_pairs = pk.p2p_pairs;
     h->m2l_entries = pk.m2l_entries;
     h->m2l_stored_entries = pk.m2l_stored_entries;
@@ -160,6 +168,89 @@ int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int max
   std::string err;
   int rc = dafmm::run_gmres(h->dev, (const double2*)f, (double2*)psi, tol, maxit, restart, iters_out, relres_out,
                             history, err);
+  if (rc < 0) return fail(rc, err);
+  return rc;
+}
+
+int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, dafmm_hodlr* out) {
+  if (!out) return fail(DAFMM_EINVAL, "out is null");
+  *out = nullptr;
+  if (!h) return fail(DAFMM_EINVAL, "null handle");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  std::unique_ptr<dafmm_hodlr_s> p;
+  try {
+    p.reset(new dafmm_hodlr_s());
+    p->owner = h;
+    std::string err;
+    int rc = dafmm::hodlr_create(h->plan, h->dev, rank, leaf_size, p->hp, err);
+    if (rc != DAFMM_OK) {
+      dafmm::hodlr_free(p->hp);
+      return fail(rc, err);
+    }
+  } catch (const std::bad_alloc&) {
+    if (p) dafmm::hodlr_free(p->hp);
+    return fail(DAFMM_ENOMEM, "host allocation failed (HODLR)");
+  }
+  *out = p.release();
+  g_last_error.clear();
+  return DAFMM_OK;
+}
+
+int dafmm_hodlr_solve(dafmm_hodlr p, const void* b, void* x) {
+  if (!p || !b || !x) return fail(DAFMM_EINVAL, "null argument");
+  std::string err;
+  int rc = dafmm::hodlr_apply(p->hp, (const double2*)b, (double2*)x, p->owner->dev.stream, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
+
+int dafmm_hodlr_stats(dafmm_hodlr p, dafmm_hodlr_stats_t* out) {
+  if (!p || !out) return fail(DAFMM_EINVAL, "null argument");
+  const dafmm::HodlrPlan& hp = p->hp;
+  std::memset(out, 0, sizeof(*out));
+  out->rank = hp.r;
+  out->leaf_size = hp.n0;
+  out->depths = hp.depths;
+  out->leaves = (int32_t)hp.leaf_a.size();
+  out->max_rank = hp.max_rank;
+  out->mean_rank = hp.mean_rank;
+  out->device_bytes = (int64_t)hp.device_bytes;
+  out->aca_entries = hp.aca_entries;
+  out->setup_aca_s = hp.t_aca;
+  out->setup_basis_s = hp.t_basis;
+  out->setup_factor_s = hp.t_factor;
+  return DAFMM_OK;
+}
+
+int dafmm_hodlr_export(dafmm_hodlr p, const char* path) {
+  if (!p || !path) return fail(DAFMM_EINVAL, "null argument");
+  std::string err;
+  int rc = dafmm::hodlr_export(p->hp, p->owner->plan, path, err);
+  return rc == DAFMM_OK ? DAFMM_OK : fail(rc, err);
+}
+
+void dafmm_hodlr_destroy(dafmm_hodlr p) {
+  if (!p) return;
+  if (p->owner && p->owner->dev.stream) cudaStreamSynchronize(p->owner->dev.stream);
+  else cudaDeviceSynchronize();
+  dafmm::hodlr_free(p->hp);
+  delete p;
+}
+
+int ls_gmres_solve_prec(dafmm_handle h, dafmm_hodlr p, const void* f, void* psi, double tol, int maxit, int restart,
+                        int* iters_out, double* relres_out, double* history) {
+  if (!h || !f || !psi || !iters_out || !relres_out) return fail(DAFMM_EINVAL, "null argument");
+  if (f == psi) return fail(DAFMM_EINVAL, "f and psi must not alias");
+  if (!(tol > 0.0) || maxit < 1) return fail(DAFMM_EINVAL, "tol must be > 0 and maxit >= 1");
+  if (h->plan.opt.host_only) return fail(DAFMM_EINVAL, "host-only plan");
+  if (p && p->owner != h) return fail(DAFMM_EINVAL, "the preconditioner was built for another handle");
+  std::string err;
+  dafmm::Precond prec;
+  if (p)
+    prec = [h, p](const double2* v, double2* z, std::string& e) {
+      return dafmm::hodlr_apply(p->hp, v, z, h->dev.stream, e);
+    };
+  int rc = dafmm::run_gmres(h->dev, (const double2*)f, (double2*)psi, tol, maxit, restart, iters_out, relres_out,
+                            history, err, prec);
   if (rc < 0) return fail(rc, err);
   return rc;
 }

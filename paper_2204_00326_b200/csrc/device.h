@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -21,7 +22,13 @@ enum ProfEvent {
 
 struct DevBatch {
   int items = 0;
-  bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
+  // layout / kernel: 0 column-major blocks streamed by translate_stream_kernel (default), 1
+  // column-major with an item of more than 128 rows (translate_cols_kernel), 2 / 3 legacy
+  // row-major blocks (translate_kernel warp per row / translate_rows_kernel lane per row)
+  int kind = 0;
+  int grid = 1;  // translate_stream_kernel CTAs
+  int64_t* stream_ptr = nullptr;
+  int32_t* stream_idx = nullptr;
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;
@@ -117,6 +124,7 @@ struct DevPlan {
   double2* gm_r = nullptr;
   double2* gm_h = nullptr;     // restart + 1 coefficients
   double2* gm_part = nullptr;  // partial sums
+  double2* gm_z = nullptr;     // preconditioned vector (right preconditioning)
   double* gm_hostbuf = nullptr;  // pinned
   int gm_part_blocks = 0;
   int64_t gm_reorth = 0;       // reorthogonalisation passes in the last ls_gmres_solve
@@ -140,8 +148,10 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
 void free_plan(DevPlan& d);
 // y = A x (mask bit 0 near, bit 1 far); x, y device pointers in caller order
 int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::string& err);
+// Right preconditioner z = M^{-1} v (device vectors, caller order, on the handle's stream; v may equal z).
+using Precond = std::function<int(const double2* v, double2* z, std::string& err)>;
 int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit, int restart, int* iters,
-              double* relres, double* history, std::string& err);
+              double* relres, double* history, std::string& err, const Precond& prec = nullptr);
 // out[i] = H0^(1)(sqrt(z2[i])) by band `code` (device pointers, enqueued on s)
 int h0_eval(const double* z2, double2* out, int64_t n, int code, cudaStream_t s, std::string& err);
 

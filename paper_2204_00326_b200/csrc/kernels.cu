@@ -18,10 +18,12 @@
 #include <algorithm>
 #include <string>
 #include <cstdio>
+#include <cstring>
 #include <vector>
 
 #include "dafmm.h"
 #include "device.h"
+#include "setup_device.h"
 
 namespace dafmm {
 
@@ -603,6 +605,44 @@ __global__ void __launch_bounds__(kM2LThreads, DAFMM_M2L_MINB) m2l_kernel(
   }
 }
 
+// Column-major items with more rows than the streamed kernel's consumers (rank > 128): one warp
+// per item, lanes own rows; column c of the item is one coalesced run over the lanes.
+__global__ void translate_cols_kernel(int items, const int64_t* __restrict__ dst_off,
+                                      const int32_t* __restrict__ dst_rows, const int64_t* __restrict__ item_mat_off,
+                                      const int32_t* __restrict__ item_cols, const int32_t* __restrict__ term_ptr,
+                                      const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
+                                      const double2* __restrict__ ops, const double2* src, double2* dst,
+                                      int accumulate) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= items) return;
+  const int R = dst_rows[warp];
+  const int tb = term_ptr[warp], te = term_ptr[warp + 1];
+  const int64_t doff = dst_off[warp];
+  const double2* M = ops + item_mat_off[warp];
+  for (int r = lane; r < R; r += 32) {
+    double ar = 0.0, ai = 0.0;
+    int cs = 0;
+    for (int t = tb; t < te; ++t) {
+      const int n = src_cols[t];
+      const double2* sv = src + src_off[t];
+      for (int c = 0; c < n; ++c) {
+        const double2 a = ld2(M + (int64_t)(cs + c) * R + r), b = sv[c];
+        ar = fma(a.x, b.x, fma(-a.y, b.y, ar));
+        ai = fma(a.x, b.y, fma(a.y, b.x, ai));
+      }
+      cs += n;
+    }
+    double2 o = make_double2(ar, ai);
+    if (accumulate) {
+      const double2 p = dst[doff + r];
+      o.x += p.x;
+      o.y += p.y;
+    }
+    dst[doff + r] = o;
+  }
+}
+
 // ---- stored M2L blocks (dafmm_options.m2l_store) ------------------------------------------
 // The M2L operator of a target node is the block A_{t s} of kernel entries between its
 // incoming pivots t and the outgoing pivots s of every node in its interaction lists (
@@ -725,11 +765,14 @@ struct MSUnit {
 };
 constexpr int kMSUnits = 4;
 constexpr int kMSIdx = kMSCols / kMSConsumers;  // multipole indices per consumer thread per unit
-__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
-    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
-    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
-    const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
-    double2* __restrict__ loc) {
+// The body serves the M2L (m2l_stored_kernel: loc = the blocks times the gathered multipoles)
+// and, with the same column-major block layout, the translations P2M / M2M / L2L
+// (translate_stream_kernel: dst (+)= item operator times the gathered sources).
+__device__ __forceinline__ void stored_gemv(int ntargets, const int64_t* __restrict__ loc_off,
+                                            const int32_t* __restrict__ rows, const int64_t* __restrict__ stream_ptr,
+                                            const int32_t* __restrict__ stream_idx,
+                                            const int64_t* __restrict__ mat_off, const double2* __restrict__ mat,
+                                            const double2* mult, double2* loc, int accumulate) {
   extern __shared__ __align__(128) double2 ms_dyn[];  // the TMA ring: kMSStages x kMSStageE entries
   double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
   __shared__ __align__(16) double2 mb[2][kMSCols];
@@ -928,6 +971,11 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
           sr += red[q].x;
           si += red[q].y;
         }
+        if (accumulate) {
+          const double2 p = loc[u.lo + j];
+          sr += p.x;
+          si += p.y;
+        }
         loc[u.lo + j] = make_double2(sr, si);
       }
     }
@@ -935,6 +983,26 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     buf ^= 1;
   }
   cp_async_wait_all();
+}
+
+__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
+    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
+    double2* __restrict__ loc) {
+  stored_gemv(ntargets, loc_off, rows, stream_ptr, stream_idx, mat_off, mat, mult, loc, 0);
+}
+
+// Translations (P2M, M2M, L2L) through the same TMA-streamed GEMV: item i
+// = one output node (dst_rows rows at dst_off), its operator column-major at item_mat_off, its
+// source stream = the slots of its terms' sources (leaf points, child multipoles, parent
+// locals) in column order.  src and dst may be the same array (disjoint slots).
+__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) translate_stream_kernel(
+    int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ item_mat_off, const double2* __restrict__ ops, const double2* src, double2* dst,
+    int accumulate) {
+  stored_gemv(items, dst_off, dst_rows, stream_ptr, stream_idx, item_mat_off, ops, src, dst, accumulate);
 }
 
 // ---- pair-stored M2L (reading R22, dafmm_options.m2l_store = 2) ---------------------------------
@@ -1590,30 +1658,57 @@ bool alloc(DevPlan& d, T** dst, size_t count, std::string& err) {
   return true;
 }
 
-bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& err) {
+bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, bool rowmajor, std::string& err) {
   b.items = (int)h.dst_off.size();
-  // kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32 lanes
-  // and reduce across the warp; narrow ones give each lane a row
-  int64_t cols = 0;
-  for (int32_t c : h.item_cols) cols += c;
-  b.wide = b.items > 0 && cols >= 48 * (int64_t)b.items;
+  if (rowmajor) {
+    // legacy kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32
+    // lanes and reduce across the warp; narrow ones give each lane a row
+    int64_t cols = 0;
+    for (int32_t c : h.item_cols) cols += c;
+    b.kind = b.items > 0 && cols >= 48 * (int64_t)b.items ? 2 : 3;
+  } else {
+    b.kind = h.max_rows <= kMSConsumers ? 0 : 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  b.grid = std::max(1, std::min(b.items, DAFMM_MS_PER_SM * sms));
+  if (b.kind == 0 && !ck(cudaFuncSetAttribute(translate_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)kMSDynSmem),
+                         err, "translate_stream_kernel shared memory"))
+    return false;
   return upload(d, &b.dst_off, h.dst_off, err) && upload(d, &b.dst_rows, h.dst_rows, err) &&
          upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.item_mat_off, h.item_mat_off, err) &&
-         upload(d, &b.item_cols, h.item_cols, err) &&
-         upload(d, &b.src_off, h.src_off, err) && upload(d, &b.src_cols, h.src_cols, err);
+         upload(d, &b.item_cols, h.item_cols, err) && upload(d, &b.src_off, h.src_off, err) &&
+         upload(d, &b.src_cols, h.src_cols, err) && upload(d, &b.stream_ptr, h.stream_ptr, err) &&
+         upload(d, &b.stream_idx, h.stream_idx, err);
 }
 
 int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate,
                      cudaStream_t st) {
   if (b.items == 0) return 0;
-  int threads = 256;
-  int blocks = (b.items * 32 + threads - 1) / threads;
-  if (b.wide)
-    translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                 b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
-  else
-    translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                      b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
+  const int threads = 256;
+  const int blocks = (b.items * 32 + threads - 1) / threads;
+  switch (b.kind) {
+    case 0:
+      translate_stream_kernel<<<b.grid, kMSThreads, kMSDynSmem, st>>>(b.items, b.dst_off, b.dst_rows, b.stream_ptr,
+                                                                     b.stream_idx, b.item_mat_off, d.ops, src, dst,
+                                                                     accumulate);
+      break;
+    case 1:
+      translate_cols_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                        b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst,
+                                                        accumulate);
+      break;
+    case 2:
+      translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                   b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
+      break;
+    default:
+      translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                        b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst,
+                                                        accumulate);
+  }
   return 1;
 }
 
@@ -1631,17 +1726,32 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   for (int64_t k = 0; k < pk.n_mult; ++k) so[k] = make_double2(pk.so_xy[2 * k], pk.so_xy[2 * k + 1]);
   for (int64_t k = 0; k < pk.n_loc; ++k) ti[k] = make_double2(pk.ti_xy[2 * k], pk.ti_xy[2 * k + 1]);
   std::vector<double2> ops(pk.ops.size());
-  for (size_t k = 0; k < pk.ops.size(); ++k) ops[k] = make_double2(pk.ops[k].re, pk.ops[k].im);
+  std::memcpy(ops.data(), pk.ops.data(), sizeof(double2) * ops.size());
   d.n_mult = pk.n_mult;
   d.n_loc = pk.n_loc;
-  d.ops_len = (int64_t)ops.size();
+  d.ops_len = pk.ops_on_device ? pk.ops_len : (int64_t)ops.size();
   bool ok = upload(d, &d.pts_t, pts, err) && upload(d, &d.w_t, pk.w_t, err) && upload(d, &d.qk2_t, pk.qk2_t, err) &&
             upload(d, &d.D_t, D, err) && upload(d, &d.perm, pk.perm, err) && upload(d, &d.so_xy, so, err) &&
-            upload(d, &d.ti_xy, ti, err) && upload(d, &d.ops, ops, err) && upload_batch(d, d.p2m, pk.p2m, err);
+            upload(d, &d.ti_xy, ti, err) &&
+            (pk.ops_on_device ? alloc(d, &d.ops, (size_t)pk.ops_len, err) : upload(d, &d.ops, ops, err)) && upload_batch(d, d.p2m, pk.p2m, pk.translate_rowmajor, err);
   d.m2m.assign(pk.m2m.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], err);
+  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], pk.translate_rowmajor, err);
   d.l2l.assign(pk.l2l.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err);
+  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], pk.translate_rowmajor, err);
+  if (ok && pk.ops_on_device) {  // F2: translation operators formed on the device
+    std::vector<OpGroup> groups(pk.opd_groups.size());
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const auto& a = pk.opd_groups[g];
+      groups[g] = OpGroup{a[0], a[1], a[2], a[3], a[4], a[5]};
+    }
+    std::vector<OpJob> jobs(pk.opd_jobs.size());
+    for (size_t j = 0; j < jobs.size(); ++j) {
+      const auto& a = pk.opd_jobs[j];
+      jobs[j] = OpJob{a.off, a.rows, a.col_start, a.src_off, a.src_len, 0};
+    }
+    const int rc = form_ops_device(plan.pts.data(), plan.n, plan.kappa, pk.opd_piv, groups, jobs, d.ops, err);
+    if (rc != DAFMM_OK) return rc;
+  }
   d.m2l_targets = (int)pk.m2l_loc_off.size();
   d.m2l_leaf_targets = pk.m2l_leaf_targets;
   ok = ok && upload(d, &d.m2l_loc_off, pk.m2l_loc_off, err) && upload(d, &d.m2l_rows, pk.m2l_rows, err) &&
@@ -1921,7 +2031,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
 // ============================================================================================
 // Restarted GMRES (reading R14) with CGS2 orthogonalisation (R20) on the device.
 int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit, int restart, int* iters_out,
-              double* relres_out, double* history, std::string& err) {
+              double* relres_out, double* history, std::string& err, const Precond& prec) {
   const int64_t n = d.n;
   const int m = restart > 0 ? restart : 50;
   if (m > 255) { err = "restart must be <= 255"; return DAFMM_EINVAL; }  // combine_kernel's coefficient cache
@@ -1929,13 +2039,15 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
   const int nb = grid_for(n, kVecThreads, 296);
   if (d.gm_restart != m) {
     // (re)size the workspace for this restart: the previous one (another restart) is released
-    for (void** p : {(void**)&d.gm_V, (void**)&d.gm_w, (void**)&d.gm_r, (void**)&d.gm_h, (void**)&d.gm_part})
+    for (void** p : {(void**)&d.gm_V, (void**)&d.gm_w, (void**)&d.gm_r, (void**)&d.gm_h, (void**)&d.gm_part,
+                     (void**)&d.gm_z})
       release(d, p);
     if (d.gm_hostbuf) cudaFreeHost(d.gm_hostbuf);
     d.gm_hostbuf = nullptr;
     d.gm_restart = m;
     if (!alloc(d, &d.gm_V, (size_t)(m + 1) * n, err) || !alloc(d, &d.gm_w, n, err) || !alloc(d, &d.gm_r, n, err) ||
-        !alloc(d, &d.gm_h, 3 * (m + 2), err) || !alloc(d, &d.gm_part, (size_t)nb * (m + 2), err))
+        !alloc(d, &d.gm_h, 3 * (m + 2), err) || !alloc(d, &d.gm_part, (size_t)nb * (m + 2), err) ||
+        !alloc(d, &d.gm_z, n, err))
       return DAFMM_ECUDA;
     if (!ck(cudaMallocHost((void**)&d.gm_hostbuf, sizeof(double2) * 3 * (m + 2)), err, "cudaMallocHost"))
       return DAFMM_ECUDA;
@@ -1985,7 +2097,13 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
     for (int j = 0; j < m; ++j) {
       double2* vj = d.gm_V + (int64_t)j * n;
       double2* vj1 = d.gm_V + (int64_t)(j + 1) * n;
-      if (run_matvec(d, vj, d.gm_w, 3u, err) != DAFMM_OK) return DAFMM_ECUDA;
+      // right preconditioning (reading HR4): w = A M^{-1} v_j
+      if (prec) {
+        if (prec(vj, d.gm_z, err) != DAFMM_OK) return DAFMM_ECUDA;
+        if (run_matvec(d, d.gm_z, d.gm_w, 3u, err) != DAFMM_OK) return DAFMM_ECUDA;
+      } else if (run_matvec(d, vj, d.gm_w, 3u, err) != DAFMM_OK) {
+        return DAFMM_ECUDA;
+      }
       ++iters;
       // CGS2 (reading R20): two passes of h = V^H w, w -= V h, one host synchronisation.  (A DGKS
       // test that skips the second pass was measured: the projection cancels ||w|| below 1/sqrt(2)
@@ -2045,7 +2163,14 @@ int run_gmres(DevPlan& d, const double2* f, double2* psi, double tol, int maxit,
     std::vector<double2> yh(k);
     for (int i = 0; i < k; ++i) yh[i] = make_double2(yv[i].real(), yv[i].imag());
     cudaMemcpyAsync(d.gm_h, yh.data(), sizeof(double2) * k, cudaMemcpyHostToDevice, s);
-    combine_kernel<<<nb, kVecThreads, 0, s>>>(n, k, d.gm_V, d.gm_h, 1.0, psi);
+    if (prec) {  // psi += M^{-1} (V y)
+      cudaMemsetAsync(d.gm_z, 0, sizeof(double2) * n, s);
+      combine_kernel<<<nb, kVecThreads, 0, s>>>(n, k, d.gm_V, d.gm_h, 1.0, d.gm_z);
+      if (prec(d.gm_z, d.gm_z, err) != DAFMM_OK) return DAFMM_ECUDA;
+      axpby_kernel<<<nb, kVecThreads, 0, s>>>(n, 1.0, psi, 1.0, d.gm_z, psi);
+    } else {
+      combine_kernel<<<nb, kVecThreads, 0, s>>>(n, k, d.gm_V, d.gm_h, 1.0, psi);
+    }
     // r = f - A psi
     if (run_matvec(d, psi, d.gm_w, 3u, err) != DAFMM_OK) return DAFMM_ECUDA;
     axpby_kernel<<<nb, kVecThreads, 0, s>>>(n, 1.0, f, -1.0, d.gm_w, d.gm_r);

@@ -7,6 +7,8 @@
 // from the matvec (dafmm_stats).
 #include <omp.h>
 
+#include <memory>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -14,10 +16,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <tuple>
 #include <sys/stat.h>
 
 #include "dafmm.h"
 #include "plan.h"
+#include "setup_device.h"
 
 namespace dafmm {
 
@@ -515,6 +519,13 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
   // ---- NCA pivots, bottom-up ----
   Ctx cx(P);
   P.piv.assign(L + 1, {});
+  // F2: the ACAs run on the device unless the plan is host-only or opt.setup_device = 0
+  std::unique_ptr<DeviceAca> dev_aca;
+  if (opt.setup_device && !opt.host_only) {
+    dev_aca.reset(new DeviceAca());
+    int rc = dev_aca->init(P.pts.data(), P.w.data(), n, kappa, err);
+    if (rc != DAFMM_OK) return rc;
+  }
   int64_t total_entries = 0;
   for (int l = L; l >= 1; --l) {
     Level& lv = P.levels[l];
@@ -539,113 +550,178 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     // leaf nodes first: a non-leaf node's search sets use the pivots of the leaves in its
     // interaction list (adaptive trees); two parallel sweeps
     int64_t level_entries = 0;
-    for (int sweep = 0; sweep < 2; ++sweep) {
-#pragma omp parallel for schedule(dynamic, 1) reduction(+ : level_entries)
-      for (int nd = 0; nd < (int)lv.nodes.size(); ++nd) {
-        const bool leafnode = is_leaf_node(nd);
-        if (leafnode != (sweep == 0)) continue;
-        int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
-        // far list: IL(B) / IL(B,k); R7 substitute for an active HFR node with empty IL(B,k)
-        std::vector<std::pair<int, int>> far;
-        if (!lv.hfr) {
-          for (int a : lv.IL[b]) far.push_back({a, -1});
-        } else {
-          for (auto& e : lv.ILdir[b])
-            if (e[0] == k) far.push_back({e[1], e[2]});
-          // R7: an active node with an empty IL(B,k) searches the children (matching child cones) of
-          // its parent's IL in the two parent cones nesting in k; R7b (option hfr_parent_search):
-          // every node with an HFR parent adds them to its own IL(B,k)
-          if (far.empty() || (P.opt.hfr_parent_search && l > 1 && pv.hfr)) {
-            const Box& B = lv.boxes[b];
-            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
-            for (auto& e : pv.ILdir[pb]) {
-              if (e[0] != 2 * k && e[0] != 2 * k + 1) continue;
-              const Box& A = pv.boxes[e[1]];
-              for (int c = 0; c < 4; ++c) {
-                auto it = lv.index.find(pack_key(2 * A.ix + (c & 1), 2 * A.iy + (c >> 1)));
-                if (it != lv.index.end()) far.push_back({it->second, e[2] / 2});
-              }
-            }
-            std::sort(far.begin(), far.end());
-            far.erase(std::unique(far.begin(), far.end()), far.end());
-          }
-        }
-        std::vector<int32_t> ti, si, to, so;
-        if (leafnode) {
+    // search sets t~^{B,i}, s~^{B,i}, t~^{B,o}, s~^{B,o} of node nd
+    auto build_sets = [&](int nd, bool leafnode, std::vector<int32_t>& ti, std::vector<int32_t>& si,
+                          std::vector<int32_t>& to, std::vector<int32_t>& so) {
+      int b = lv.nodes[nd].first, k = lv.nodes[nd].second;
+      // far list: IL(B) / IL(B,k); R7 substitute for an active HFR node with empty IL(B,k)
+      std::vector<std::pair<int, int>> far;
+      if (!lv.hfr) {
+        for (int a : lv.IL[b]) far.push_back({a, -1});
+      } else {
+        for (auto& e : lv.ILdir[b])
+          if (e[0] == k) far.push_back({e[1], e[2]});
+        // R7: an active node with an empty IL(B,k) searches the children (matching child cones) of
+        // its parent's IL in the two parent cones nesting in k; R7b (option hfr_parent_search):
+        // every node with an HFR parent adds them to its own IL(B,k)
+        if (far.empty() || (P.opt.hfr_parent_search && l > 1 && pv.hfr)) {
           const Box& B = lv.boxes[b];
-          for (int32_t t = B.begin; t < B.end; ++t) ti.push_back(P.perm[t]);
-          so = ti;
-          auto add_box = [&](const Box& A) {
-            for (int32_t t = A.begin; t < A.end; ++t) si.push_back(P.perm[t]);
-          };
-          for (auto& f : far) add_box(lv.boxes[f.first]);
-          // reading R16: a leaf whose LFR parent has a leaf neighbour also searches IL(parent)
-          if (l >= 2 && !pv.hfr) {
-            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
-            bool leaf_nb = false;
-            for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
-            if (leaf_nb)
-              for (int a : pv.IL[pb]) add_box(pv.boxes[a]);
+          int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+          for (auto& e : pv.ILdir[pb]) {
+            if (e[0] != 2 * k && e[0] != 2 * k + 1) continue;
+            const Box& A = pv.boxes[e[1]];
+            for (int c = 0; c < 4; ++c) {
+              auto it = lv.index.find(pack_key(2 * A.ix + (c & 1), 2 * A.iy + (c >> 1)));
+              if (it != lv.index.end()) far.push_back({it->second, e[2] / 2});
+            }
           }
-          sorted_union(ti);
-          sorted_union(so);
-          sorted_union(si);
-          to = si;
-        } else {
-          std::vector<int> kids;
-          children(lv, l, b, k, kids);
+          std::sort(far.begin(), far.end());
+          far.erase(std::unique(far.begin(), far.end()), far.end());
+        }
+      }
+      if (leafnode) {
+        const Box& B = lv.boxes[b];
+        for (int32_t t = B.begin; t < B.end; ++t) ti.push_back(P.perm[t]);
+        so = ti;
+        auto add_box = [&](const Box& A) {
+          for (int32_t t = A.begin; t < A.end; ++t) si.push_back(P.perm[t]);
+        };
+        for (auto& f : far) add_box(lv.boxes[f.first]);
+        // reading R16: a leaf whose LFR parent has a leaf neighbour also searches IL(parent)
+        if (l >= 2 && !pv.hfr) {
+          int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+          bool leaf_nb = false;
+          for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
+          if (leaf_nb)
+            for (int a : pv.IL[pb]) add_box(pv.boxes[a]);
+        }
+        sorted_union(ti);
+        sorted_union(so);
+        sorted_union(si);
+        to = si;
+      } else {
+        std::vector<int> kids;
+        children(lv, l, b, k, kids);
+        for (int c : kids) {
+          const NodePivots& pc = P.piv[l + 1][c];
+          ti.insert(ti.end(), pc.ti.begin(), pc.ti.end());
+          so.insert(so.end(), pc.so.begin(), pc.so.end());
+        }
+        for (auto& f : far) {
+          if (!lv.hfr && lv.boxes[f.first].leaf) {
+            // a leaf in the interaction list has no children: its own pivots at this level
+            const NodePivots& pa = P.piv[l][lv.node_id(f.first, 0)];
+            si.insert(si.end(), pa.so.begin(), pa.so.end());
+            to.insert(to.end(), pa.ti.begin(), pa.ti.end());
+            continue;
+          }
+          children(lv, l, f.first, f.second, kids);
           for (int c : kids) {
             const NodePivots& pc = P.piv[l + 1][c];
-            ti.insert(ti.end(), pc.ti.begin(), pc.ti.end());
-            so.insert(so.end(), pc.so.begin(), pc.so.end());
+            si.insert(si.end(), pc.so.begin(), pc.so.end());
+            to.insert(to.end(), pc.ti.begin(), pc.ti.end());
           }
-          for (auto& f : far) {
-            if (!lv.hfr && lv.boxes[f.first].leaf) {
-              // a leaf in the interaction list has no children: its own pivots at this level
-              const NodePivots& pa = P.piv[l][lv.node_id(f.first, 0)];
-              si.insert(si.end(), pa.so.begin(), pa.so.end());
-              to.insert(to.end(), pa.ti.begin(), pa.ti.end());
-              continue;
-            }
-            children(lv, l, f.first, f.second, kids);
-            for (int c : kids) {
-              const NodePivots& pc = P.piv[l + 1][c];
-              si.insert(si.end(), pc.so.begin(), pc.so.end());
-              to.insert(to.end(), pc.ti.begin(), pc.ti.end());
-            }
-          }
-          // reading R16 for non-leaf nodes: the points of IL(parent) when the LFR parent has a
-          // leaf neighbour (the directions its own interaction list does not reach)
-          if (!lv.hfr && l >= 2 && !pv.hfr) {
-            const Box& B = lv.boxes[b];
-            int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
-            bool leaf_nb = false;
-            for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
-            if (leaf_nb)
-              for (int a : pv.IL[pb])
-                for (int32_t t = pv.boxes[a].begin; t < pv.boxes[a].end; ++t) {
-                  si.push_back(P.perm[t]);
-                  to.push_back(P.perm[t]);
-                }
-          }
-          sorted_union(ti);
-          sorted_union(so);
-          sorted_union(si);
-          sorted_union(to);
         }
-        NodePivots& np = P.piv[l][nd];
-        int64_t ent = 0;
-        aca(cx, ti, si, eps, np.ti, np.si, ent);
-        if (P.opt.symmetric_pivots) {
-          // reading R19: G is symmetric, and the outgoing search sets equal the incoming ones
-          // with rows and columns swapped, so the incoming skeleton (t^{B,i}, s^{B,i}) also serves
-          // as the outgoing one (s^{B,o} = t^{B,i}, t^{B,o} = s^{B,i}): one ACA per node
+        // reading R16 for non-leaf nodes: the points of IL(parent) when the LFR parent has a
+        // leaf neighbour (the directions its own interaction list does not reach)
+        if (!lv.hfr && l >= 2 && !pv.hfr) {
+          const Box& B = lv.boxes[b];
+          int pb = pv.index.at(pack_key(B.ix >> 1, B.iy >> 1));
+          bool leaf_nb = false;
+          for (int a : pv.N[pb]) leaf_nb = leaf_nb || pv.boxes[a].leaf;
+          if (leaf_nb)
+            for (int a : pv.IL[pb])
+              for (int32_t t = pv.boxes[a].begin; t < pv.boxes[a].end; ++t) {
+                si.push_back(P.perm[t]);
+                to.push_back(P.perm[t]);
+              }
+        }
+        sorted_union(ti);
+        sorted_union(so);
+        sorted_union(si);
+        sorted_union(to);
+      }
+    };
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      std::vector<int> sweep_nodes;
+      for (int nd = 0; nd < (int)lv.nodes.size(); ++nd)
+        if (is_leaf_node(nd) == (sweep == 0)) sweep_nodes.push_back(nd);
+      if (sweep_nodes.empty()) continue;
+      if (!dev_aca) {
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : level_entries)
+        for (int t = 0; t < (int)sweep_nodes.size(); ++t) {
+          const int nd = sweep_nodes[t];
+          std::vector<int32_t> ti, si, to, so;
+          build_sets(nd, sweep == 0, ti, si, to, so);
+          NodePivots& np = P.piv[l][nd];
+          int64_t ent = 0;
+          aca(cx, ti, si, eps, np.ti, np.si, ent);
+          if (P.opt.symmetric_pivots) {
+            // reading R19: G is symmetric, and the outgoing search sets equal the incoming ones
+            // with rows and columns swapped, so the incoming skeleton (t^{B,i}, s^{B,i}) also serves
+            // as the outgoing one (s^{B,o} = t^{B,i}, t^{B,o} = s^{B,i}): one ACA per node
+            np.so = np.ti;
+            np.to = np.si;
+          } else {
+            aca(cx, to, so, eps, np.to, np.so, ent);
+          }
+          level_entries += ent;
+        }
+        continue;
+      }
+      // device ACA (F2): the search sets of every node of the sweep, packed into one index
+      // array; one ACA problem per (node, direction), all run by one launch
+      const int ns = (int)sweep_nodes.size();
+      std::vector<std::array<std::vector<int32_t>, 4>> sets(ns);
+#pragma omp parallel for schedule(dynamic, 4)
+      for (int t = 0; t < ns; ++t) {
+        auto& S = sets[t];
+        build_sets(sweep_nodes[t], sweep == 0, S[0], S[1], S[2], S[3]);
+      }
+      // leaf nodes: to = si, so = ti (stored once)
+      const bool leafsweep = sweep == 0;
+      std::vector<int64_t> off(4 * (size_t)ns + 1, 0);
+      for (int t = 0; t < ns; ++t)
+        for (int c = 0; c < 4; ++c) {
+          const bool dup = leafsweep && c >= 2;
+          off[4 * t + c + 1] = off[4 * t + c] + (dup ? 0 : (int64_t)sets[t][c].size());
+        }
+      std::vector<int32_t> idx(off.back());
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int t = 0; t < ns; ++t)
+        for (int c = 0; c < 4; ++c)
+          if (!(leafsweep && c >= 2)) std::copy(sets[t][c].begin(), sets[t][c].end(), idx.begin() + off[4 * t + c]);
+      auto set_off = [&](int t, int c) { return leafsweep && c >= 2 ? off[4 * t + (c == 2 ? 1 : 0)] : off[4 * t + c]; };
+      auto set_len = [&](int t, int c) {
+        return (int32_t)(leafsweep && c >= 2 ? sets[t][c == 2 ? 1 : 0].size() : sets[t][c].size());
+      };
+      const int dirs = P.opt.symmetric_pivots ? 1 : 2;
+      std::vector<AcaProblem> probs((size_t)dirs * ns);
+      for (int t = 0; t < ns; ++t) {
+        probs[(size_t)dirs * t] = {set_off(t, 0), set_off(t, 1), set_len(t, 0), set_len(t, 1), 0, 0, 0, 0, 0};
+        if (dirs == 2) probs[(size_t)dirs * t + 1] = {set_off(t, 2), set_off(t, 3), set_len(t, 2), set_len(t, 3), 0, 0, 0, 0, 0};
+      }
+      std::vector<int32_t> prow, pcol, rank;
+      int rc = dev_aca->run(idx, probs, eps, prow, pcol, rank, level_entries, err);
+      if (rc != DAFMM_OK) return rc;
+#pragma omp parallel for schedule(dynamic, 16)
+      for (int t = 0; t < ns; ++t) {
+        NodePivots& np = P.piv[l][sweep_nodes[t]];
+        auto take = [&](const AcaProblem& pr, int r, std::vector<int32_t>& out_r, std::vector<int32_t>& out_c) {
+          out_r.resize(r);
+          out_c.resize(r);
+          for (int q = 0; q < r; ++q) {
+            out_r[q] = idx[pr.row_off + prow[pr.out_off + q]];
+            out_c[q] = idx[pr.col_off + pcol[pr.out_off + q]];
+          }
+        };
+        take(probs[(size_t)dirs * t], rank[(size_t)dirs * t], np.ti, np.si);
+        if (dirs == 2) {
+          take(probs[(size_t)dirs * t + 1], rank[(size_t)dirs * t + 1], np.to, np.so);
+        } else {  // reading R19 (see the host path)
           np.so = np.ti;
           np.to = np.si;
-        } else {
-          aca(cx, to, so, eps, np.to, np.so, ent);
         }
-        level_entries += ent;
       }
     }
     total_entries += level_entries;
@@ -665,6 +741,10 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   const int64_t n = P.n;
   Ctx cx(P);
   pk.perm = P.perm;
+  {
+    const char* e = std::getenv("DAFMM_TRANSLATE_ROWMAJOR");
+    pk.translate_rowmajor = e && e[0] == '1' ? 1 : 0;
+  }
   pk.pts_t.resize(2 * n);
   pk.w_t.resize(n);
   pk.qk2_t.resize(n);
@@ -717,11 +797,12 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     int64_t off;             // block start
     int64_t stride;          // row stride (row-major item block); 0: column-major
     int col_start;           // first column of this term inside the item block
+    int rows;                // the item's rows (column-major: column stride)
   };
   std::vector<Job> jobs;
   int64_t ops_len = 0;
   auto add_job = [&](int kind, int l, int nd, int ch, int64_t len) {
-    jobs.push_back({kind, l, nd, ch, ops_len, 0, 0});
+    jobs.push_back({kind, l, nd, ch, ops_len, 0, 0, 0});
     ops_len += len;
     return jobs.back().off;
   };
@@ -741,13 +822,17 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     bt.item_mat_off.push_back(off);
     bt.item_cols.push_back(C);
     bt.term_ptr.push_back((int32_t)bt.src_off.size());
+    if (bt.stream_ptr.empty()) bt.stream_ptr.push_back(0);
+    bt.max_rows = std::max(bt.max_rows, rows);
     int cs = 0;
     for (const Term& t : terms) {
-      jobs.push_back({kind, l, t.node, t.child, off, C, cs});
+      jobs.push_back({kind, l, t.node, t.child, off, C, cs, rows});
       bt.src_off.push_back(t.src_off);
       bt.src_cols.push_back(t.cols);
+      for (int k = 0; k < t.cols; ++k) bt.stream_idx.push_back((int32_t)(t.src_off + k));
       cs += t.cols;
     }
+    bt.stream_ptr.push_back((int64_t)bt.stream_idx.size());
   };
   auto child_nodes = [&](int l, int nd, std::vector<int>& out) {
     out.clear();
@@ -1079,6 +1164,57 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       pk.in_ptr.push_back((int32_t)pk.in_off.size());
     }
   }
+  pk.ops_len = ops_len;
+  // ---- operator blocks on the device (F2): one group per (node, V~ or U~) sharing its cross
+  // matrix; every job lists the caller indices of its columns (V~) or rows (U~) ----
+  bool dev_ops = P.opt.setup_device && !P.opt.host_only && !pk.translate_rowmajor;
+  for (size_t jb = 0; dev_ops && jb < jobs.size(); ++jb) {
+    const NodePivots& np = P.piv[jobs[jb].level][jobs[jb].node];
+    if ((int)std::max(np.so.size(), np.ti.size()) > 64) dev_ops = false;  // kDeviceOpsMaxRank
+  }
+  if (dev_ops) {
+    std::vector<size_t> order(jobs.size());
+    std::iota(order.begin(), order.end(), 0);
+    auto gkey = [&](const Job& J) { return std::make_tuple(J.level, J.node, J.kind >= 2 ? 1 : 0); };
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) { return gkey(jobs[a]) < gkey(jobs[b]); });
+    auto push = [&](const std::vector<int32_t>& v) {
+      const int64_t o = (int64_t)pk.opd_piv.size();
+      pk.opd_piv.insert(pk.opd_piv.end(), v.begin(), v.end());
+      return o;
+    };
+    for (size_t q = 0; q < order.size();) {
+      const Job& J0 = jobs[order[q]];
+      const int type = J0.kind >= 2 ? 1 : 0;
+      const NodePivots& np = P.piv[J0.level][J0.node];
+      const std::vector<int32_t>& A = type == 0 ? np.to : np.ti;
+      const std::vector<int32_t>& B = type == 0 ? np.so : np.si;
+      std::array<int32_t, 6> g = {(int32_t)push(A), (int32_t)push(B), (int32_t)A.size(), type,
+                                  (int32_t)pk.opd_jobs.size(), 0};
+      size_t e = q;
+      for (; e < order.size() && gkey(jobs[order[e]]) == gkey(J0); ++e) {
+        const Job& J = jobs[order[e]];
+        std::vector<int32_t> src;
+        int rows = J.rows;
+        if (J.kind == 0 || J.kind == 3) {  // the leaf's points
+          const Level& jl = P.levels[J.level];
+          const Box& Bx = J.kind == 0 ? jl.boxes[jl.nodes[J.node].first] : jl.boxes[J.child];
+          for (int32_t t = Bx.begin; t < Bx.end; ++t) src.push_back(P.perm[t]);
+          if (J.kind == 3) rows = Bx.end - Bx.begin;
+        } else if (J.kind == 1) {
+          src = P.piv[J.level + 1][J.child].so;
+        } else {
+          src = P.piv[J.level + 1][J.child].ti;
+        }
+        const int64_t so = push(src);
+        pk.opd_jobs.push_back({J.off, rows, J.col_start, so, (int32_t)src.size(), 0});
+      }
+      g[5] = (int32_t)pk.opd_jobs.size();
+      if (g[2] > 0) pk.opd_groups.push_back(g);
+      q = e;
+    }
+    pk.ops_on_device = 1;
+    return DAFMM_OK;
+  }
   // ---- operator blocks (column-major), in parallel ----
   try {
     pk.ops.assign((size_t)ops_len, cplx{0.0, 0.0});
@@ -1116,7 +1252,11 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       for (size_t c = 0; c < cols.size(); ++c) {
         for (int a = 0; a < r; ++a) rhs[a] = cx.H(np.to[a], cols[c]);
         lu.solve(rhs.data());
-        for (int a = 0; a < r; ++a) out[(size_t)a * J.stride + J.col_start + c] = {rhs[a].real(), rhs[a].imag()};
+        for (int a = 0; a < r; ++a) {
+          const size_t at = pk.translate_rowmajor ? (size_t)a * J.stride + J.col_start + c
+                                                  : (size_t)(J.col_start + c) * J.rows + a;
+          out[at] = {rhs[a].real(), rhs[a].imag()};
+        }
       }
     } else {
       // U~ = H(t, si) H(ti, si)^{-1}: rows = t (leaf points or child's ti), cols = ti.
@@ -1144,7 +1284,8 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
         for (int c = 0; c < r; ++c) rhs[c] = cx.H(rows[a], np.si[c]);
         lu.solve(rhs.data());
         for (int c = 0; c < r; ++c) {
-          const size_t at = J.kind == 3 ? (size_t)c * nr + a : (size_t)a * J.stride + J.col_start + c;
+          const size_t at = J.kind == 3 || !pk.translate_rowmajor ? (size_t)(J.col_start + c) * nr + a
+                                                                  : (size_t)a * J.stride + J.col_start + c;
           out[at] = {rhs[c].real(), rhs[c].imag()};
         }
       }

@@ -43,3 +43,45 @@ def test_full_size_sampled_rows(name, rows):
     if zero.any():
         assert np.array_equal(yg[zero], P["x"][zero])
     op.close()
+
+
+def test_full_c2_matches_oracle_dafmm(tmp_path):
+    """Config 2 at its full size (N = 65536, kappa = 40; directional levels kappa b = 5 and 10)
+    against the oracle's serial DAFMM on the product's validated pivots: <= 1e-11 relative l2
+    on y - x (the north-star gate, D10), plus the per-leaf worst case beside the global norm, in
+    bench.py's launch configuration (non-default stream)."""
+    import paper_2204_00326_b200 as prod
+    from oracle.nca import NCA
+    from oracle.plan_io import compare_lists, load_plan, validate_pivots
+    from oracle.tree import Lists, Tree
+    P = make_problem("c2")
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    s = torch.cuda.Stream()
+    op.set_stream(s)
+    x = torch.from_numpy(P["x"]).cuda()
+    y = torch.empty_like(x)
+    with torch.cuda.stream(s):
+        op.matvec(x, y)
+    s.synchronize()
+    yg = y.cpu().numpy()
+    op.export_plan(str(tmp_path / "plan"))
+    plan = load_plan(tmp_path / "plan")
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    compare_lists(plan, tree, lists)
+    piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv)
+    validate_pivots(nca, piv)
+    xs = P["x"]
+    yo = nca.matvec(xs)
+    err = np.linalg.norm((yg - xs) - (yo - xs)) / np.linalg.norm(yo - xs)
+    assert err <= 1e-11, err
+    worst = 0.0
+    for l, b in tree.all_leaves():
+        idx = tree.boxes[l][b]
+        den = np.linalg.norm(yo[idx] - xs[idx])
+        if den > 0:
+            worst = max(worst, np.linalg.norm(yg[idx] - yo[idx]) / den)
+    assert worst <= 1e-9, worst
+    op.close()

@@ -250,3 +250,30 @@ def test_gpu_pair_stored_m2l(name, n, kappa, tmp_path):
     near = _gpu_matvec(op, x, 1)
     far = _gpu_matvec(op, x, 2)
     assert _rel(near + far, y) <= 1e-14
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c2", 128, 20.0), ("c5", 5, 12.0), ("c2", 128, 40.0)])
+def test_gpu_device_aca_matches_host_aca(name, n, kappa, tmp_path):
+    """F2: the NCA ACAs run on the device (setup_device=1, default) or on the host (0).  Same
+    algorithm (R10) on the same search sets, so the pivots agree node by node except where
+    rounding of the two H0 evaluators breaks an argmax tie; both plans pass the oracle's
+    validation and give the same operator to within the compression tolerance."""
+    P = make_problem(name, n=n, kappa=kappa)
+    op_d = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], setup_device=1)
+    op_h = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], setup_device=0)
+    (tmp_path / "d").mkdir()
+    (tmp_path / "h").mkdir()
+    prob, nca_d = _oracle_on_product_plan(P, op_d, tmp_path / "d")
+    _, nca_h = _oracle_on_product_plan(P, op_h, tmp_path / "h")
+    same = total = 0
+    for l in range(1, nca_d.tree.L + 1):
+        for node, pd in nca_d.pivots[l].items():
+            ph = nca_h.pivots[l][node]
+            total += 1
+            same += all(np.array_equal(pd[k], ph[k]) for k in ("ti", "si", "to", "so"))
+    assert total > 0 and same >= 0.9 * total, (same, total)
+    assert op_d.stats()["aca_entries"] > 0
+    x = P["x"]
+    yd, yh = _gpu_matvec(op_d, x), _gpu_matvec(op_h, x)
+    assert _rel(yd - x, nca_d.matvec(x) - x) <= 1e-11
+    assert _rel(yd - x, yh - x) <= 10 * P["nca_tol"]

@@ -211,3 +211,22 @@ def test_dafmm_r7_substitute_lists_match_dense():
     y = nca.matvec(P["x"])
     yd = oracle.dense_matvec(prob, P["x"])
     assert _rel_z(y, yd, P["x"]) <= 10 * P["nca_tol"]
+
+
+def test_r9_compressing_A_is_blind_where_q_vanishes():
+    """Reading R9 evidence: the NCA compresses K = G w, not A = I + kappa^2 diag(q) K.
+    With the ACA run on A's rows (P:353-360 read literally) the interaction-list restricted
+    pivot search cannot see targets with q = 0, so on the disk contrast of config 3
+    (scaled: n = 128, kappa = 20) the outgoing bases miss the far field that reaches q != 0
+    targets through the parents: 0.2 relative error, against <= 10 nca_tol with K
+    (test_dafmm_matches_dense_scaled_configs covers the same case with K)."""
+    P = make_problem("c3", n=128, kappa=20.0)
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    lists = Lists(tree)
+    nca_a = NCA(prob, tree, lists, P["nca_tol"], compress="A")
+    rows = np.arange(0, prob.n, 7)
+    yd = oracle.dense_matvec_rows(prob, P["x"], rows)
+    x = P["x"][rows]
+    err = np.linalg.norm((nca_a.matvec(P["x"])[rows] - x) - (yd - x)) / np.linalg.norm(yd - x)
+    assert err > 1e-2, err
