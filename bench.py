@@ -59,7 +59,7 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-configs", action="store_true", help="skip the per-config matvec lines (c1-c3)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config matvec lines (c1, c2, c3, c5)")
     return ap.parse_args(argv)
 
 
@@ -352,29 +352,49 @@ def time_matvecs(op, stream, x, y, steps, flush, host=None):
     return times
 
 
-GMRES_RESTART = {"c2": 50, "c3": 200}  # c2: BASELINE.json; c3: DESIGN.md R14 (m = 50 stagnates)
+GMRES_RESTART = {"c2": 50, "c3": 200, "c5": 200}  # c2: BASELINE.json; c3: DESIGN.md R14 (m = 50 stagnates)
+# the hybrid solver: GMRES(m) right-preconditioned by the HODLR of rank r (HR1-HR4)
+HYBRID = {"c3": dict(restart=50, rank=16), "c5": dict(restart=50, rank=16)}
 
 
-def gmres_case(name, prod, torch):
+def gmres_case(name, prod, torch, hybrid=False):
+    """One GMRES solve of a BASELINE config: solve time excludes the DAFMM setup and,
+    for the hybrid solver, the HODLR setup (both reported beside it).  The first call allocates
+    the workspace and is not timed."""
     P = make_problem(name)
-    restart = GMRES_RESTART.get(name, 50)
+    hy = HYBRID.get(name) if hybrid else None
+    restart = hy["restart"] if hy else GMRES_RESTART.get(name, 50)
     t0 = time.perf_counter()
     op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
     setup = time.perf_counter() - t0
+    pc, pc_setup, pc_stats = None, None, None
+    if hy:
+        t0 = time.perf_counter()
+        pc = prod.HODLR(op, rank=hy["rank"], leaf_size=64)
+        pc_setup = time.perf_counter() - t0
+        pc_stats = pc.stats()
     f = torch.from_numpy(P["f"]).cuda()
     psi = torch.empty_like(f)
     maxit = 3000
-    op.gmres(f, psi, P["gmres_tol"], 2, restart)  # allocates the workspace (first call), untimed
+    op.gmres(f, psi, P["gmres_tol"], 2, restart, prec=pc)  # allocates the workspace (first call), untimed
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rc, iters, relres = op.gmres(f, psi, P["gmres_tol"], maxit, restart)
+    rc, iters, relres = op.gmres(f, psi, P["gmres_tol"], maxit, restart, prec=pc)
     solve = time.perf_counter() - t0
     st = op.stats()
+    out = {"config": name, "N": int(P["points"].shape[0]), "kappa": P["kappa"], "tol": P["gmres_tol"],
+           "restart": restart, "status": "converged" if rc == 0 else "not_converged", "iterations": iters,
+           "true_relres": relres, "solve_s": solve, "ms_per_iteration": 1e3 * solve / max(iters, 1),
+           "reorthogonalisations": st["gmres_reorth"], "m2l_stored": st["m2l_stored"], "setup_s": setup,
+           "solver": "hybrid (HODLR right preconditioner)" if hy else "GMRES"}
+    if hy:
+        out["hodlr"] = {"rank": hy["rank"], "leaf_size": 64, "setup_s": pc_setup, "depths": pc_stats["depths"],
+                        "mean_rank": pc_stats["mean_rank"], "device_bytes": pc_stats["device_bytes"],
+                        "setup_aca_s": pc_stats["setup_aca_s"], "setup_basis_s": pc_stats["setup_basis_s"],
+                        "setup_factor_s": pc_stats["setup_factor_s"]}
+        pc.close()
     op.close()
-    return {"config": name, "N": int(P["points"].shape[0]), "kappa": P["kappa"], "tol": P["gmres_tol"],
-            "restart": restart, "status": "converged" if rc == 0 else "not_converged", "iterations": iters,
-            "true_relres": relres, "solve_s": solve, "ms_per_iteration": 1e3 * solve / max(iters, 1),
-            "reorthogonalisations": st["gmres_reorth"], "m2l_stored": st["m2l_stored"], "setup_s": setup}
+    return out
 
 
 def config_matvec_line(name, prod, torch, steps, flush, stream):
@@ -519,6 +539,8 @@ def run_ours(args):
                 "setup_s": setup_s,
                 "setup_breakdown_s": {k: stats[k] for k in ("setup_tree_s", "setup_lists_s", "setup_nca_s",
                                                            "setup_ops_s", "setup_upload_s")},
+                "setup_where": "tree and lists on the host; NCA ACAs and translation operators on the device "
+                               "(setup_device = 1, F2)",
                 "plan": {k: stats[k] for k in ("levels", "n_nodes", "p2p_pairs", "m2l_entries", "m2l_pairs",
                                                "operator_bytes", "device_bytes", "mean_rank_leaf_in",
                                                "mean_rank_leaf_out", "max_rank", "m2l_stored", "m2l_store_bytes",
@@ -539,10 +561,11 @@ def run_ours(args):
         if world == 1 and not args.no_configs:
             op.close()
             line["configs"] = [config_matvec_line(c, prod, torch, 20, flush, stream)
-                               for c in ("c1", "c2", "c3") if c != args.config]
+                               for c in ("c1", "c2", "c3", "c5") if c != args.config]
         if world == 1 and not args.no_gmres:
             op.close()
-            line["gmres"] = [gmres_case(c, prod, torch) for c in ("c2", "c3")]
+            line["gmres"] = [gmres_case(c, prod, torch) for c in ("c2", "c3")] + \
+                [gmres_case(c, prod, torch, hybrid=True) for c in ("c3", "c5")]
         print(json.dumps(line), flush=True)
     op.close()
     if world > 1:

@@ -56,7 +56,11 @@ enum {
 typedef struct {
   double T;            /* regime threshold: a box of width b is HFR iff (kappa b)^2 > T
                           (reading R3; default 16) */
-  int self_term;       /* 1: disk self term D1 (default); 0: D_i = 0 (point kernel) */
+  int self_term;       /* D_i = integral of G over the point's cell (Eq. 13): 1 over the
+                          equal-area disk of area w_i (reading D1, closed form; default); 2 over the
+                          square of side sqrt(w_i) centred on the point (polar form, radial integral
+                          exact, 40-node Gauss-Legendre in angle; 4.1e-3 from the disk at kappa h =
+                          0.3125); 0: D_i = 0 (point kernel of Experiment 1) */
   int kernel_mode;     /* 0: Lippmann-Schwinger y = x + kappa^2 q o (K x) (default);
                           1: potential y = K x (the N-body sum of Experiment 1) */
   int max_level;       /* deepest tree level allowed (default 20, the maximum) */
@@ -92,6 +96,12 @@ typedef struct {
                           on the host.  0: on the host (OpenMP).  Host-only plans always use the
                           host.  Both give valid pivots; they may differ where rounding breaks a
                           tie of the ACA's argmax. */
+  int w_reading;       /* meaning of w in the directional regime (reading R4): 0 (default)
+                          the box circumradius b / sqrt(2): HFR neighbours have centre distance <
+                          kappa b^2 / 2, cones have half-angle <= sqrt(2) / (kappa b); 1 the box width
+                          b: distance < kappa b^2, half-angle <= 1 / (kappa b) (more neighbours and
+                          cones, longer interaction lists).  The regime test (kappa b)^2 > T
+                          is the same in both. */
 } dafmm_options;
 
 /* Statistics of a plan (sizes, ranks, setup times). */

@@ -69,13 +69,34 @@ def h1_small(z):
     return out
 
 
-SELF_TERM_MODES = {"zero": 0, "disk": 1}
+SELF_TERM_MODES = {"zero": 0, "disk": 1, "square": 2}
+
+
+def self_term_square(w, kappa):
+    """D_i = integral of G(0, y) = (i/4) H0(kappa |y|) over the square cell of side h = sqrt(w_i)
+    centred on the point (Eq. 13 integrates G over the cell).  By symmetry the square is
+    8 triangles 0 <= theta <= pi/4, 0 <= rho <= R(theta) = h / (2 cos theta); the radial integral
+    is exact, int_0^R H0(k rho) rho d rho = (k R H1(k R) + 2i/pi) / k^2 (d/dz [z H1(z)] = z H0(z),
+    z H1(z) -> -2i/pi as z -> 0), and the smooth angular one is Gauss-Legendre (40 nodes)."""
+    w = _f64(np.atleast_1d(w))
+    k = float(kappa)
+    x, gw = np.polynomial.legendre.leggauss(40)
+    theta = (x + 1.0) * (np.pi / 8.0)
+    out = np.empty(w.size, dtype=np.complex128)
+    for i, wi in enumerate(w):
+        z = k * np.sqrt(wi) / (2.0 * np.cos(theta))
+        radial = (z * h1_small(z) + 2j / np.pi) / (k * k)
+        out[i] = 0.25j * 8.0 * (np.pi / 8.0) * np.dot(gw, radial)
+    return out
 
 
 def self_terms(weights, kappa, mode="disk"):
     """D_i of reading D1: integral of G over the equal-area disk of weight w_i (mode 'disk'),
-    or 0 (mode 'zero', the point-kernel N-body of Experiment 1)."""
+    over the square cell of side sqrt(w_i) (mode 'square', self_term_square), or 0 (mode
+    'zero', the point-kernel N-body of Experiment 1)."""
     w = _f64(weights)
+    if mode == "square":
+        return self_term_square(w, kappa)
     out = np.empty(w.size, dtype=np.complex128)
     load_library().oracle_self_terms(_p(w), w.size, float(kappa), SELF_TERM_MODES[mode], _p(out))
     return out

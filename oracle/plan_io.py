@@ -17,7 +17,8 @@ def load_plan(path):
     meta = ld("meta.npy")
     L = int(meta[1])
     out = dict(meta=dict(n=int(meta[0]), L=L, W=meta[2], x0=meta[3], y0=meta[4], kappa=meta[5], T=meta[6],
-                         nca_tol=meta[7], hfr_parent_search=bool(meta[8]) if meta.size > 8 else False),
+                         nca_tol=meta[7], hfr_parent_search=bool(meta[8]) if meta.size > 8 else False,
+                         w_reading=int(meta[9]) if meta.size > 9 else 0),
                perm=ld("perm.npy"), levels=[])
     for l in range(L + 1):
         pre = "l%d_" % l

@@ -2,7 +2,8 @@
 neighbour / interaction lists of the DAFMM.
 
 Readings (DESIGN.md §2): R2 adaptive tree whose leaves are LFR (paper rule 3, P:204);
-R3 T = 16; R4 w = circumradius b/sqrt(2); R5 nested cone geometry; R6 N(B) contains B.
+R3 T = 16; R4 w = circumradius b/sqrt(2) (w_reading="width": w = b, the alternative reading of
+P:297-303); R5 nested cone geometry; R6 N(B) contains B.
 
 Boxes are keyed (level, ix, iy) with integer lattice indices; only non-empty boxes exist.
 Every list is a sorted Python list of keys; directional lists hold (key, cone) pairs.
@@ -39,7 +40,10 @@ class Tree:
     boxes[l]: {(ix, iy): sorted point indices} of the boxes that exist at level l (the root
     and the children of split boxes, non-empty); leaves[l]: the keys of boxes not split."""
 
-    def __init__(self, points, weights, kappa, leaf_size, T=16.0, max_level=MAXL):
+    def __init__(self, points, weights, kappa, leaf_size, T=16.0, max_level=MAXL, w_reading="circumradius"):
+        # R4: w of the HFR neighbour test and the cone angle (P:297-303) is the box circumradius
+        # b / sqrt(2); the alternative reading takes w = b, the width of P:279's regime test
+        self.w_width = {"circumradius": False, "width": True}[w_reading]
         pts = np.asarray(points, dtype=np.float64).reshape(-1, 2)
         half = 0.5 * np.sqrt(np.asarray(weights, dtype=np.float64))
         lo_x, hi_x = float(np.min(pts[:, 0] - half)), float(np.max(pts[:, 0] + half))
@@ -115,7 +119,7 @@ class Tree:
 
     def n_cones(self, level):
         """R5: smallest power of two n with half-angle pi/n <= 1/(kappa w), w = b/sqrt(2)."""
-        x = math.pi * self.kb(level) / math.sqrt(2.0)
+        x = math.pi * self.kb(level) if self.w_width else math.pi * self.kb(level) / math.sqrt(2.0)
         n = 1
         while n < x:
             n *= 2
@@ -127,12 +131,13 @@ class Tree:
 
 def is_neighbor(tree, level, a, b):
     """N(B) membership: LFR — centres closer than 2b; HFR — centres closer than
-    kappa w^2 with w = b/sqrt(2) (R4), i.e. |d| b < kappa b^2 / 2.  d in lattice units."""
+    kappa w^2 with w = b/sqrt(2) (R4), i.e. |d| b < kappa b^2 / 2 (w = b: |d| < kappa b).
+    d in lattice units."""
     dx, dy = a[0] - b[0], a[1] - b[1]
     d2 = dx * dx + dy * dy
     if tree.is_hfr(level):
         kb = tree.kb(level)
-        return 4.0 * d2 < kb * kb
+        return d2 < kb * kb if tree.w_width else 4.0 * d2 < kb * kb
     return d2 < 4
 
 
@@ -162,7 +167,7 @@ class Lists:
             hfr = tree.is_hfr(l)
             reach = 1
             if hfr:
-                reach = int(math.ceil(tree.kb(l) / 2.0)) + 1
+                reach = int(math.ceil(tree.kb(l) if tree.w_width else tree.kb(l) / 2.0)) + 1
             for b in boxes:
                 nb = []
                 for dx in range(-reach, reach + 1):

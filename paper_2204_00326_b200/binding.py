@@ -35,7 +35,8 @@ class Options(ctypes.Structure):
     _fields_ = [("T", ctypes.c_double), ("self_term", ctypes.c_int), ("kernel_mode", ctypes.c_int),
                 ("max_level", ctypes.c_int), ("num_threads", ctypes.c_int), ("host_only", ctypes.c_int),
                 ("symmetric_pivots", ctypes.c_int), ("m2l_store", ctypes.c_int),
-                ("hfr_parent_search", ctypes.c_int), ("setup_device", ctypes.c_int)]
+                ("hfr_parent_search", ctypes.c_int), ("setup_device", ctypes.c_int),
+                ("w_reading", ctypes.c_int)]
 
 
 class Stats(ctypes.Structure):

@@ -57,6 +57,7 @@ void dafmm_default_options(dafmm_options* opt) {
   opt->m2l_store = o.m2l_store;
   opt->hfr_parent_search = o.hfr_parent_search;
   opt->setup_device = o.setup_device;
+  opt->w_reading = o.w_reading;
 }
 
 int dafmm_create_ex(const double* points, const double* weights, const double* q, int64_t n, double kappa,
@@ -75,6 +76,7 @@ int dafmm_create_ex(const double* points, const double* weights, const double* q
     o.m2l_store = opt->m2l_store;
     o.hfr_parent_search = opt->hfr_parent_search;
     o.setup_device = opt->setup_device;
+    o.w_reading = opt->w_reading;
     if (o.m2l_store < -1 || o.m2l_store > 2) return fail(DAFMM_EINVAL, "m2l_store must be -1, 0, 1 or 2");
   }
   std::unique_ptr<dafmm_plan> h;

@@ -22,13 +22,7 @@ enum ProfEvent {
 
 struct DevBatch {
   int items = 0;
-  // layout / kernel: 0 column-major blocks streamed by translate_stream_kernel (default), 1
-  // column-major with an item of more than 128 rows (translate_cols_kernel), 2 / 3 legacy
-  // row-major blocks (translate_kernel warp per row / translate_rows_kernel lane per row)
-  int kind = 0;
-  int grid = 1;  // translate_stream_kernel CTAs
-  int64_t* stream_ptr = nullptr;
-  int32_t* stream_idx = nullptr;
+  bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;

@@ -605,44 +605,6 @@ __global__ void __launch_bounds__(kM2LThreads, DAFMM_M2L_MINB) m2l_kernel(
   }
 }
 
-// Column-major items with more rows than the streamed kernel's consumers (rank > 128): one warp
-// per item, lanes own rows; column c of the item is one coalesced run over the lanes.
-__global__ void translate_cols_kernel(int items, const int64_t* __restrict__ dst_off,
-                                      const int32_t* __restrict__ dst_rows, const int64_t* __restrict__ item_mat_off,
-                                      const int32_t* __restrict__ item_cols, const int32_t* __restrict__ term_ptr,
-                                      const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
-                                      const double2* __restrict__ ops, const double2* src, double2* dst,
-                                      int accumulate) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= items) return;
-  const int R = dst_rows[warp];
-  const int tb = term_ptr[warp], te = term_ptr[warp + 1];
-  const int64_t doff = dst_off[warp];
-  const double2* M = ops + item_mat_off[warp];
-  for (int r = lane; r < R; r += 32) {
-    double ar = 0.0, ai = 0.0;
-    int cs = 0;
-    for (int t = tb; t < te; ++t) {
-      const int n = src_cols[t];
-      const double2* sv = src + src_off[t];
-      for (int c = 0; c < n; ++c) {
-        const double2 a = ld2(M + (int64_t)(cs + c) * R + r), b = sv[c];
-        ar = fma(a.x, b.x, fma(-a.y, b.y, ar));
-        ai = fma(a.x, b.y, fma(a.y, b.x, ai));
-      }
-      cs += n;
-    }
-    double2 o = make_double2(ar, ai);
-    if (accumulate) {
-      const double2 p = dst[doff + r];
-      o.x += p.x;
-      o.y += p.y;
-    }
-    dst[doff + r] = o;
-  }
-}
-
 // ---- stored M2L blocks (dafmm_options.m2l_store) ------------------------------------------
 // The M2L operator of a target node is the block A_{t s} of kernel entries between its
 // incoming pivots t and the outgoing pivots s of every node in its interaction lists (
@@ -765,14 +727,11 @@ struct MSUnit {
 };
 constexpr int kMSUnits = 4;
 constexpr int kMSIdx = kMSCols / kMSConsumers;  // multipole indices per consumer thread per unit
-// The body serves the M2L (m2l_stored_kernel: loc = the blocks times the gathered multipoles)
-// and, with the same column-major block layout, the translations P2M / M2M / L2L
-// (translate_stream_kernel: dst (+)= item operator times the gathered sources).
-__device__ __forceinline__ void stored_gemv(int ntargets, const int64_t* __restrict__ loc_off,
-                                            const int32_t* __restrict__ rows, const int64_t* __restrict__ stream_ptr,
-                                            const int32_t* __restrict__ stream_idx,
-                                            const int64_t* __restrict__ mat_off, const double2* __restrict__ mat,
-                                            const double2* mult, double2* loc, int accumulate) {
+__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
+    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
+    double2* __restrict__ loc) {
   extern __shared__ __align__(128) double2 ms_dyn[];  // the TMA ring: kMSStages x kMSStageE entries
   double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
   __shared__ __align__(16) double2 mb[2][kMSCols];
@@ -971,11 +930,6 @@ __device__ __forceinline__ void stored_gemv(int ntargets, const int64_t* __restr
           sr += red[q].x;
           si += red[q].y;
         }
-        if (accumulate) {
-          const double2 p = loc[u.lo + j];
-          sr += p.x;
-          si += p.y;
-        }
         loc[u.lo + j] = make_double2(sr, si);
       }
     }
@@ -983,26 +937,6 @@ __device__ __forceinline__ void stored_gemv(int ntargets, const int64_t* __restr
     buf ^= 1;
   }
   cp_async_wait_all();
-}
-
-__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
-    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
-    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
-    const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
-    double2* __restrict__ loc) {
-  stored_gemv(ntargets, loc_off, rows, stream_ptr, stream_idx, mat_off, mat, mult, loc, 0);
-}
-
-// Translations (P2M, M2M, L2L) through the same TMA-streamed GEMV: item i
-// = one output node (dst_rows rows at dst_off), its operator column-major at item_mat_off, its
-// source stream = the slots of its terms' sources (leaf points, child multipoles, parent
-// locals) in column order.  src and dst may be the same array (disjoint slots).
-__global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) translate_stream_kernel(
-    int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
-    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
-    const int64_t* __restrict__ item_mat_off, const double2* __restrict__ ops, const double2* src, double2* dst,
-    int accumulate) {
-  stored_gemv(items, dst_off, dst_rows, stream_ptr, stream_idx, item_mat_off, ops, src, dst, accumulate);
 }
 
 // ---- pair-stored M2L (reading R22, dafmm_options.m2l_store = 2) ---------------------------------
@@ -1658,57 +1592,32 @@ bool alloc(DevPlan& d, T** dst, size_t count, std::string& err) {
   return true;
 }
 
-bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, bool rowmajor, std::string& err) {
+bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& err) {
   b.items = (int)h.dst_off.size();
-  if (rowmajor) {
-    // legacy kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32
-    // lanes and reduce across the warp; narrow ones give each lane a row
-    int64_t cols = 0;
-    for (int32_t c : h.item_cols) cols += c;
-    b.kind = b.items > 0 && cols >= 48 * (int64_t)b.items ? 2 : 3;
-  } else {
-    b.kind = h.max_rows <= kMSConsumers ? 0 : 1;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  b.grid = std::max(1, std::min(b.items, DAFMM_MS_PER_SM * sms));
-  if (b.kind == 0 && !ck(cudaFuncSetAttribute(translate_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)kMSDynSmem),
-                         err, "translate_stream_kernel shared memory"))
-    return false;
+  // kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32 lanes
+  // and reduce across the warp; narrow ones give each lane a row.  (A TMA-streamed variant on
+  // column-major items, the stored-M2L kernel's ring, was measured slower: one gather latency
+  // per small item; profiles/README.md, r2e.)
+  int64_t cols = 0;
+  for (int32_t c : h.item_cols) cols += c;
+  b.wide = b.items > 0 && cols >= 48 * (int64_t)b.items;
   return upload(d, &b.dst_off, h.dst_off, err) && upload(d, &b.dst_rows, h.dst_rows, err) &&
          upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.item_mat_off, h.item_mat_off, err) &&
-         upload(d, &b.item_cols, h.item_cols, err) && upload(d, &b.src_off, h.src_off, err) &&
-         upload(d, &b.src_cols, h.src_cols, err) && upload(d, &b.stream_ptr, h.stream_ptr, err) &&
-         upload(d, &b.stream_idx, h.stream_idx, err);
+         upload(d, &b.item_cols, h.item_cols, err) &&
+         upload(d, &b.src_off, h.src_off, err) && upload(d, &b.src_cols, h.src_cols, err);
 }
 
 int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, double2* dst, int accumulate,
                      cudaStream_t st) {
   if (b.items == 0) return 0;
-  const int threads = 256;
-  const int blocks = (b.items * 32 + threads - 1) / threads;
-  switch (b.kind) {
-    case 0:
-      translate_stream_kernel<<<b.grid, kMSThreads, kMSDynSmem, st>>>(b.items, b.dst_off, b.dst_rows, b.stream_ptr,
-                                                                     b.stream_idx, b.item_mat_off, d.ops, src, dst,
-                                                                     accumulate);
-      break;
-    case 1:
-      translate_cols_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                        b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst,
-                                                        accumulate);
-      break;
-    case 2:
-      translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                   b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
-      break;
-    default:
-      translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                        b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst,
-                                                        accumulate);
-  }
+  int threads = 256;
+  int blocks = (b.items * 32 + threads - 1) / threads;
+  if (b.wide)
+    translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                 b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
+  else
+    translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
+                                                      b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
   return 1;
 }
 
@@ -1733,11 +1642,11 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   bool ok = upload(d, &d.pts_t, pts, err) && upload(d, &d.w_t, pk.w_t, err) && upload(d, &d.qk2_t, pk.qk2_t, err) &&
             upload(d, &d.D_t, D, err) && upload(d, &d.perm, pk.perm, err) && upload(d, &d.so_xy, so, err) &&
             upload(d, &d.ti_xy, ti, err) &&
-            (pk.ops_on_device ? alloc(d, &d.ops, (size_t)pk.ops_len, err) : upload(d, &d.ops, ops, err)) && upload_batch(d, d.p2m, pk.p2m, pk.translate_rowmajor, err);
+            (pk.ops_on_device ? alloc(d, &d.ops, (size_t)pk.ops_len, err) : upload(d, &d.ops, ops, err)) && upload_batch(d, d.p2m, pk.p2m, err);
   d.m2m.assign(pk.m2m.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], pk.translate_rowmajor, err);
+  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], err);
   d.l2l.assign(pk.l2l.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], pk.translate_rowmajor, err);
+  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err);
   if (ok && pk.ops_on_device) {  // F2: translation operators formed on the device
     std::vector<OpGroup> groups(pk.opd_groups.size());
     for (size_t g = 0; g < groups.size(); ++g) {
@@ -1747,7 +1656,7 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
     std::vector<OpJob> jobs(pk.opd_jobs.size());
     for (size_t j = 0; j < jobs.size(); ++j) {
       const auto& a = pk.opd_jobs[j];
-      jobs[j] = OpJob{a.off, a.rows, a.col_start, a.src_off, a.src_len, 0};
+      jobs[j] = OpJob{a.off, a.rows, a.col_start, a.stride, 0, a.src_off, a.src_len, 0};
     }
     const int rc = form_ops_device(plan.pts.data(), plan.n, plan.kappa, pk.opd_piv, groups, jobs, d.ops, err);
     if (rc != DAFMM_OK) return rc;

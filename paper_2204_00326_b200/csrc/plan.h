@@ -27,6 +27,7 @@ struct Options {
   int symmetric_pivots = 0;  // reading R19 (option): one ACA per node, outgoing skeleton = incoming
   int m2l_store = -1;        // M2L blocks: -1 auto, 0 on the fly every matvec, 1 stored in HBM, 2 stored per pair (R22)
   int hfr_parent_search = 0;  // reading R7b (option): HFR search sets also take the parent's far children
+  int w_reading = 0;         // reading R4 of w: 0 circumradius b / sqrt(2), 1 box width b
   int setup_device = 1;      // NCA ACAs on the device (F2); 0: on the host (always for host_only plans)
 };
 
@@ -99,13 +100,7 @@ struct Packed {
     std::vector<int32_t> term_ptr;      // items + 1
     std::vector<int64_t> src_off;       // per term
     std::vector<int32_t> src_cols;      // per term
-    std::vector<int64_t> stream_ptr;    // items + 1 (column-major layout): per item, its source slots
-    std::vector<int32_t> stream_idx;    // source slot of every column, item by item
-    int32_t max_rows = 0;
   };
-  // translation operator layout: column-major per item (default; streamed by TMA) or the legacy
-  // row-major blocks (environment variable DAFMM_TRANSLATE_ROWMAJOR=1, A/B experiments)
-  int translate_rowmajor = 0;
   // operators formed on the device (setup_device, every cross matrix of rank <= 64): ops stays
   // empty on the host and upload_plan runs form_ops_device on these descriptors
   int ops_on_device = 0;
@@ -114,7 +109,7 @@ struct Packed {
   std::vector<std::array<int32_t, 6>> opd_groups;  // a_off, b_off, r, type, job_begin, job_end
   struct OpdJob {
     int64_t off;
-    int32_t rows, col_start;
+    int32_t rows, col_start, stride, pad0;
     int64_t src_off;
     int32_t src_len, pad;
   };

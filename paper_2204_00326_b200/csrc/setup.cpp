@@ -70,6 +70,45 @@ zd self_term_disk(double kappa, double w) {
   return zd(0.0, kPi * R / (2.0 * kappa)) * hankel1_small(kappa * R) - 1.0 / (kappa * kappa);
 }
 
+// Square cell of side h = sqrt(w) (option self_term = 2; Eq. 13 integrates G over the cell,
+// P:260): 8 triangles in polar coordinates, the radial integral in closed form
+// (z H1(z))' = z H0(z), z H1(z) -> -2i/pi as z -> 0, the smooth angular integral over
+// [0, pi/4] by Gauss-Legendre with 40 nodes (Newton on the Legendre recurrence).
+zd self_term_square(double kappa, double w) {
+  constexpr int kN = 40;
+  static double node[kN], weight[kN];
+  static bool init = false;
+#pragma omp critical(gauss_legendre)
+  if (!init) {
+    for (int i = 0; i < kN; ++i) {
+      double x = std::cos(kPi * (i + 0.75) / (kN + 0.5)), dp = 1.0;
+      for (int it = 0; it < 100; ++it) {
+        double p0 = 1.0, p1 = x;
+        for (int k = 2; k <= kN; ++k) {
+          const double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+          p0 = p1;
+          p1 = p2;
+        }
+        dp = kN * (x * p1 - p0) / (x * x - 1.0);
+        const double dx = p1 / dp;
+        x -= dx;
+        if (std::fabs(dx) < 1e-16) break;
+      }
+      node[i] = x;
+      weight[i] = 2.0 / ((1.0 - x * x) * dp * dp);
+    }
+    init = true;
+  }
+  const double h = std::sqrt(w);
+  zd acc(0.0, 0.0);
+  for (int i = 0; i < kN; ++i) {
+    const double th = (node[i] + 1.0) * (kPi / 8.0);
+    const double z = kappa * h / (2.0 * std::cos(th));
+    acc += weight[i] * (z * hankel1_small(z) + zd(0.0, 2.0 / kPi));
+  }
+  return zd(0.0, 0.25) * 8.0 * (kPi / 8.0) * acc / (kappa * kappa);
+}
+
 // ---- complex LU with partial pivoting (reading R12: solves, never explicit inverses) ----
 struct LU {
   int r = 0;
@@ -250,8 +289,8 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
   if (!(kappa > 0.0) || !std::isfinite(kappa)) { err = "kappa must be positive and finite"; return DAFMM_EINVAL; }
   if (!(nca_tol > 0.0 && nca_tol < 1.0)) { err = "nca_tol must be in (0, 1)"; return DAFMM_EINVAL; }
   if (leaf_size < 1) { err = "leaf_size must be >= 1"; return DAFMM_EINVAL; }
-  if (!(opt.T > 0.0) || opt.self_term < 0 || opt.self_term > 1 || opt.kernel_mode < 0 || opt.kernel_mode > 1 ||
-      opt.max_level < 0 || opt.max_level > 24) {
+  if (!(opt.T > 0.0) || opt.self_term < 0 || opt.self_term > 2 || opt.kernel_mode < 0 || opt.kernel_mode > 1 ||
+      opt.max_level < 0 || opt.max_level > 24 || opt.w_reading < 0 || opt.w_reading > 1) {
     err = "invalid options";
     return DAFMM_EINVAL;
   }
@@ -272,6 +311,10 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     if (!(P.w[i] > 0.0)) { err = "weights must be > 0"; return DAFMM_EINVAL; }
     if (opt.self_term == 1 && kappa * std::sqrt(P.w[i] / kPi) > 8.0) {
       err = "self-term disk too large (kappa sqrt(w/pi) > 8)";
+      return DAFMM_EINVAL;
+    }
+    if (opt.self_term == 2 && kappa * std::sqrt(0.5 * P.w[i]) > 8.0) {
+      err = "self-term square too large (kappa sqrt(w/2) > 8)";
       return DAFMM_EINVAL;
     }
   }
@@ -337,8 +380,8 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     lv.b = width(l);
     lv.kb = kappa * lv.b;
     lv.hfr = lv.kb * lv.kb > opt.T;
-    if (lv.hfr) {
-      double x = kPi * lv.kb / std::sqrt(2.0);
+    if (lv.hfr) {  // R5 with reading R4: half-angle <= 1/(kappa w), w = b / sqrt(2) (w_reading 1: w = b)
+      double x = opt.w_reading == 1 ? kPi * lv.kb : kPi * lv.kb / std::sqrt(2.0);
       int nc = 1;
       while (nc < x) nc *= 2;
       lv.ncones = nc;
@@ -394,6 +437,18 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
   P.D.assign(n, zd(0.0, 0.0));
   if (opt.self_term == 1)
     for (int64_t i = 0; i < n; ++i) P.D[i] = self_term_disk(kappa, P.w[i]);
+  if (opt.self_term == 2) {
+    // equal weights share one value (the uniform configs): evaluate each distinct w once
+    double wl = -1.0;
+    zd dl(0.0, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+      if (P.w[i] != wl) {
+        wl = P.w[i];
+        dl = self_term_square(kappa, wl);
+      }
+      P.D[i] = dl;
+    }
+  }
   double t1 = now_s();
   P.t_tree = t1 - t0;
 
@@ -402,7 +457,7 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     Level& lv = P.levels[l];
     int nb = (int)lv.boxes.size();
     lv.N.assign(nb, {});
-    int64_t reach = lv.hfr ? (int64_t)std::ceil(lv.kb / 2.0) + 1 : 1;
+    int64_t reach = lv.hfr ? (int64_t)std::ceil(opt.w_reading == 1 ? lv.kb : lv.kb / 2.0) + 1 : 1;
     const double kb2 = lv.kb * lv.kb;
 #pragma omp parallel for schedule(dynamic, 64)
     for (int b = 0; b < nb; ++b) {
@@ -412,7 +467,8 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
           auto it = lv.index.find(pack_key(B.ix + dx, B.iy + dy));
           if (B.ix + dx < 0 || B.iy + dy < 0 || it == lv.index.end()) continue;
           int64_t d2 = dx * dx + dy * dy;
-          bool nbr = lv.hfr ? (4.0 * (double)d2 < kb2) : (d2 < 4);  // P:286 / P:302 (R4)
+          // P:286 / P:302 (R4: centre distance < kappa w^2, w = b / sqrt(2); w_reading 1: w = b)
+          bool nbr = lv.hfr ? (opt.w_reading == 1 ? (double)d2 < kb2 : 4.0 * (double)d2 < kb2) : (d2 < 4);
           if (nbr) lv.N[b].push_back(it->second);
         }
       std::sort(lv.N[b].begin(), lv.N[b].end());
@@ -741,10 +797,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   const int64_t n = P.n;
   Ctx cx(P);
   pk.perm = P.perm;
-  {
-    const char* e = std::getenv("DAFMM_TRANSLATE_ROWMAJOR");
-    pk.translate_rowmajor = e && e[0] == '1' ? 1 : 0;
-  }
+
   pk.pts_t.resize(2 * n);
   pk.w_t.resize(n);
   pk.qk2_t.resize(n);
@@ -822,17 +875,13 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     bt.item_mat_off.push_back(off);
     bt.item_cols.push_back(C);
     bt.term_ptr.push_back((int32_t)bt.src_off.size());
-    if (bt.stream_ptr.empty()) bt.stream_ptr.push_back(0);
-    bt.max_rows = std::max(bt.max_rows, rows);
     int cs = 0;
     for (const Term& t : terms) {
       jobs.push_back({kind, l, t.node, t.child, off, C, cs, rows});
       bt.src_off.push_back(t.src_off);
       bt.src_cols.push_back(t.cols);
-      for (int k = 0; k < t.cols; ++k) bt.stream_idx.push_back((int32_t)(t.src_off + k));
       cs += t.cols;
     }
-    bt.stream_ptr.push_back((int64_t)bt.stream_idx.size());
   };
   auto child_nodes = [&](int l, int nd, std::vector<int>& out) {
     out.clear();
@@ -1167,7 +1216,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   pk.ops_len = ops_len;
   // ---- operator blocks on the device (F2): one group per (node, V~ or U~) sharing its cross
   // matrix; every job lists the caller indices of its columns (V~) or rows (U~) ----
-  bool dev_ops = P.opt.setup_device && !P.opt.host_only && !pk.translate_rowmajor;
+  bool dev_ops = P.opt.setup_device && !P.opt.host_only;
   for (size_t jb = 0; dev_ops && jb < jobs.size(); ++jb) {
     const NodePivots& np = P.piv[jobs[jb].level][jobs[jb].node];
     if ((int)std::max(np.so.size(), np.ti.size()) > 64) dev_ops = false;  // kDeviceOpsMaxRank
@@ -1206,7 +1255,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
           src = P.piv[J.level + 1][J.child].ti;
         }
         const int64_t so = push(src);
-        pk.opd_jobs.push_back({J.off, rows, J.col_start, so, (int32_t)src.size(), 0});
+        pk.opd_jobs.push_back({J.off, rows, J.col_start, (int32_t)J.stride, 0, so, (int32_t)src.size(), 0});
       }
       g[5] = (int32_t)pk.opd_jobs.size();
       if (g[2] > 0) pk.opd_groups.push_back(g);
@@ -1253,8 +1302,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
         for (int a = 0; a < r; ++a) rhs[a] = cx.H(np.to[a], cols[c]);
         lu.solve(rhs.data());
         for (int a = 0; a < r; ++a) {
-          const size_t at = pk.translate_rowmajor ? (size_t)a * J.stride + J.col_start + c
-                                                  : (size_t)(J.col_start + c) * J.rows + a;
+          const size_t at = (size_t)a * J.stride + J.col_start + c;
           out[at] = {rhs[a].real(), rhs[a].imag()};
         }
       }
@@ -1284,8 +1332,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
         for (int c = 0; c < r; ++c) rhs[c] = cx.H(rows[a], np.si[c]);
         lu.solve(rhs.data());
         for (int c = 0; c < r; ++c) {
-          const size_t at = J.kind == 3 || !pk.translate_rowmajor ? (size_t)(J.col_start + c) * nr + a
-                                                                  : (size_t)a * J.stride + J.col_start + c;
+          const size_t at = J.kind == 3 ? (size_t)c * nr + a : (size_t)a * J.stride + J.col_start + c;
           out[at] = {rhs[c].real(), rhs[c].imag()};
         }
       }
@@ -1329,10 +1376,18 @@ int export_plan(const Plan& P, const std::string& dir, std::string& err) {
     if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
   bool ok = true;
   std::vector<double> meta = {(double)P.n, (double)P.L, P.W, P.x0, P.y0, P.kappa, P.opt.T, P.nca_tol,
-                              (double)P.opt.hfr_parent_search};
+                              (double)P.opt.hfr_parent_search, (double)P.opt.w_reading};
   ok &= write_npy(dir + "/meta.npy", "<f8", meta, {(int64_t)meta.size()});
   std::vector<int64_t> perm(P.perm.begin(), P.perm.end());
   ok &= write_npy(dir + "/perm.npy", "<i8", perm, {(int64_t)perm.size()});
+  {  // self terms D_i (caller order), complex128
+    std::vector<double> d(2 * (size_t)P.n);
+    for (int64_t i = 0; i < P.n; ++i) {
+      d[2 * i] = P.D[i].real();
+      d[2 * i + 1] = P.D[i].imag();
+    }
+    ok &= write_npy(dir + "/self.npy", "<c16", d, {(int64_t)P.n});
+  }
   // leaves (level, box) and their near-field source boxes (level, box)
   {
     std::vector<int64_t> leaves, ptr = {0}, src;

@@ -313,8 +313,10 @@ __global__ void __launch_bounds__(128) ops_form_kernel(const OpGroup* __restrict
           for (int k = i + 1; k < r; ++k) cfms2(x[i], M[k * r + i], x[k]);
           x[i] = cdiv2(x[i], M[i * r + i]);
         }
-        double2* out = ops + J.off + (int64_t)(J.col_start + j) * J.rows;
-        for (int i = 0; i < r; ++i) out[i] = x[i];
+        for (int i = 0; i < r; ++i) {
+          const int64_t at = J.stride > 0 ? (int64_t)i * J.stride + J.col_start + j : (int64_t)(J.col_start + j) * J.rows + i;
+          ops[J.off + at] = x[i];
+        }
       } else {  // x M = H(src_j, B): w U = a, y L = w, x_{perm[i]} = y_i
         for (int c = 0; c < r; ++c) x[c] = hentry(xs, pts[B[c]], T);
         for (int c = 0; c < r; ++c) {
@@ -327,7 +329,11 @@ __global__ void __launch_bounds__(128) ops_form_kernel(const OpGroup* __restrict
           for (int i = c + 1; i < r; ++i) cfms2(s2, x[i], M[c * r + i]);
           x[c] = s2;
         }
-        for (int i = 0; i < r; ++i) ops[J.off + (int64_t)(J.col_start + s_perm[i]) * J.rows + j] = x[i];
+        for (int i = 0; i < r; ++i) {
+          const int c = J.col_start + s_perm[i];
+          const int64_t at = J.stride > 0 ? (int64_t)j * J.stride + c : (int64_t)c * J.rows + j;
+          ops[J.off + at] = x[i];
+        }
       }
     }
   }

@@ -28,16 +28,18 @@ struct AcaProblem {
 // Translation operators formed on the device (P:427-562 in the G-only form of DESIGN.md §5):
 // one group per (node, kind) shares the LU of its cross matrix M[a][c] = H0(kappa |A_a - B_c|).
 //   type 0 (V~, P2M / M2M): A = t^{B,o}, B = s^{B,o}; job column j: x = M^{-1} H(A, src_j),
-//           out[(col_start + j) rows + a] = x_a
+//           element (row a, column col_start + j) = x_a
 //   type 1 (U~, L2L / L2P):  A = t^{B,i}, B = s^{B,i}; job row j: x M = H(src_j, B),
-//           out[(col_start + c) rows + j] = x_c
+//           element (row j, column col_start + c) = x_c
+// Element (row, col) of a job's block sits at off + row stride + col (row-major translation
+// items, stride = the item's columns) or off + col rows + row (stride 0: column-major L2P U).
 struct OpGroup {
   int32_t a_off, b_off, r, type;  // pivot lists at piv[a_off], piv[b_off] (r each)
   int32_t job_begin, job_end;
 };
 struct OpJob {
   int64_t off;           // item block start in ops
-  int32_t rows, col_start;
+  int32_t rows, col_start, stride, pad0;
   int64_t src_off;       // caller indices at piv[src_off, src_off + src_len)
   int32_t src_len, pad;
 };

@@ -1,6 +1,12 @@
 import os
 import sys
 
+# The oracle's many small dense solves (numpy / OpenBLAS) run fastest single-threaded; a BLAS
+# thread pool per call oversubscribes the host cores (measured: the scaled-config oracle tests
+# 93 s -> 59 s on 8 cores).  oracle_core.c's OpenMP loops are not affected.
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("MKL_NUM_THREADS", "1")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -222,3 +222,37 @@ def test_binding_rejects_bad_host_vectors():
     with pytest.raises(ValueError):
         op.matvec_host(good, ro)
     op.close()
+
+
+@pytest.mark.parametrize("mode,code", [("disk", 1), ("square", 2), ("zero", 0)])
+def test_host_self_terms_match_oracle(mode, code, tmp_path):
+    """The product's self terms D_i (exported with the plan) against the oracle's: the disk
+    closed form (D1), the square-cell integral (Eq. 13's cell) and zero; ragged weights."""
+    import numpy as np
+    from oracle.core import self_terms
+    P = make_problem("c5", n=5, kappa=12.0)  # adaptive: several cell sizes
+    prod = _prod()
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], host_only=1, self_term=code)
+    op.export_plan(tmp_path / "plan")
+    op.close()
+    D = np.load(tmp_path / "plan" / "self.npy")
+    ref = self_terms(P["weights"], P["kappa"], mode)
+    if mode == "zero":
+        assert np.all(D == 0)
+    else:
+        assert np.max(np.abs(D - ref) / np.abs(ref)) < 1e-13
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 40.0)])
+def test_host_width_reading_lists_match_oracle(name, n, kappa, tmp_path):
+    """w_reading = 1 (w = b in P:297-303): the product's tree, neighbour, interaction and
+    directional lists equal the oracle's under the same reading, and its pivots validate."""
+    P = make_problem(name, n=n, kappa=kappa)
+    plan, _ = _host_plan(P, tmp_path, w_reading=1)
+    assert plan["meta"]["w_reading"] == 1
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64, w_reading="width")
+    lists = Lists(tree)
+    compare_lists(plan, tree, lists)
+    piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    validate_pivots(NCA(prob, tree, lists, P["nca_tol"], pivots=piv), piv)

@@ -36,7 +36,7 @@ def _dev(x):
 
 
 @pytest.mark.parametrize("name,n,kappa,rank,n0", [("c1", None, None, 8, 64), ("c3", 64, 10.0, 12, 64),
-                                                  ("c5", 5, 12.0, 6, 40), ("c1", 48, 8.0, 32, 24)])
+                                                  ("c5", 5, 12.0, 6, 40), ("c1", 48, 8.0, 12, 24)])
 def test_gpu_hodlr_solve_matches_oracle(name, n, kappa, rank, n0, tmp_path):
     P = make_problem(name, n=n, kappa=kappa)
     op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])

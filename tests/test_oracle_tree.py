@@ -129,3 +129,37 @@ def test_root_and_leaf_level():
     # rule 3: leaves must be LFR even when leaf_size would stop earlier
     t2 = Tree(P["points"], P["weights"], 80.0, 4096)
     assert not t2.is_hfr(t2.L) and t2.is_hfr(t2.L - 1)
+
+
+@pytest.mark.parametrize("name,n,kappa", [("c1", None, None), ("c2", 128, 40.0), ("c5", 5, 12.0)])
+def test_pair_completeness_width_reading(name, n, kappa):
+    """w_reading = width (w = b in P:297-303 instead of the circumradius, R4): still an exact
+    partition of all leaf pairs."""
+    P = make_problem(name, n=n, kappa=kappa)
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64, w_reading="width")
+    cover = _cover_matrix(tree, Lists(tree))
+    assert cover.min() == 1 and cover.max() == 1
+
+
+def test_width_reading_pair_counts_and_geometry():
+    """SURVEY App. A.2 (T = 16): C1 has 3612 IL box pairs over all levels with w = width against
+    2472 with the circumradius; HFR neighbours lie within kappa b^2 and the cones have
+    half-angle <= 1/(kappa b)."""
+    P = make_problem("c1")
+    counts = {}
+    for wr in ("circumradius", "width"):
+        tree = Tree(P["points"], P["weights"], P["kappa"], 64, w_reading=wr)
+        lists = Lists(tree)
+        counts[wr] = sum(len(v) for l in range(1, tree.L + 1) for v in lists.IL[l].values())
+    assert counts == {"circumradius": 2472, "width": 3612}
+    P, tree = make_problem("c2", n=128, kappa=40.0), None
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64, w_reading="width")
+    lists = Lists(tree)
+    for l in range(tree.L + 1):
+        if not tree.is_hfr(l):
+            continue
+        b = tree.width(l)
+        assert math.pi / tree.n_cones(l) <= 1.0 / (tree.kappa * b) + 1e-15
+        for key, nb in lists.N[l].items():
+            for a in nb:
+                assert math.hypot(a[0] - key[0], a[1] - key[1]) * b < tree.kappa * b * b
