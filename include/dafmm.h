@@ -131,6 +131,10 @@ typedef struct {
                                    has 32 or 64 points); 0: each leaf evaluates all its pairs */
   int64_t m2l_stored_entries;   /* kernel entries in the M2L blocks as stored / streamed per matvec
                                    (m2l_entries / 2 with m2l_store = 2, else m2l_entries) */
+  double setup_nca_device_s;    /* part of setup_nca_s spent in the device ACA launches (F2) */
+  double setup_ops_device_s;    /* part of setup_upload_s spent forming the operators on the device */
+  int32_t level_restricted;     /* 1: every two leaves that share a boundary (edge or corner) are at
+                                   most one level apart (the paper's level-restricted tree) */
 } dafmm_stats_t;
 
 void dafmm_default_options(dafmm_options* opt);
@@ -235,7 +239,9 @@ int dafmm_h0_eval(const void* z2, void* h0, int64_t n, int band, void* stream);
  * `rank` ("apriori fixing the rank"; HR2).  Ã is factorised on the device by the recursive
  * Sherman-Morrison-Woodbury form (HR3): O(N r log N) memory, O(N r log N) per solve.
  *
- * dafmm_hodlr_create: rank in [1, 32], leaf_size in [1, 64].  Synchronous.  The preconditioner
+ * dafmm_hodlr_create: rank in [1, 32], leaf_size in [1, 64]; max_block >= 0: sibling blocks with
+ *   more than max_block rows are dropped (rank 0; reading HR5, an option: 0 keeps every block, as
+ *   the paper's HODLR does).  Synchronous.  The preconditioner
  *   refers to the handle's device plan: destroy it before the handle.  Errors: DAFMM_EINVAL
  *   (arguments, host-only plan, kernel_mode 1), DAFMM_ENOMEM / DAFMM_ECUDA, DAFMM_ESETUP
  *   (singular leaf block, cross matrix or Woodbury factor).
@@ -244,7 +250,7 @@ int dafmm_h0_eval(const void* z2, void* h0, int64_t n, int band, void* stream);
  * dafmm_hodlr_export: writes hodlr_blocks.npy (nblocks x 5: depth, a, b, c, d for the block of
  *   rows [a, b) and columns [c, d) of tree positions), hodlr_piv_ptr.npy, hodlr_I.npy,
  *   hodlr_J.npy (pivots, tree positions), hodlr_perm.npy (tree position -> caller index) and
- *   hodlr_meta.npy (rank, leaf_size, n) into directory `path`, for the oracle.
+ *   hodlr_meta.npy (rank, leaf_size, n, max_block) into directory `path`, for the oracle.
  * ls_gmres_solve_prec: as ls_gmres_solve on the right-preconditioned system A Ã^{-1} u = f,
  *   psi = Ã^{-1} u (HR4: the paper writes the left form; the right form keeps the GMRES residual
  *   equal to the true residual ||A psi - f|| / ||f||).  p = NULL gives ls_gmres_solve. */
@@ -252,10 +258,11 @@ typedef struct dafmm_hodlr_s* dafmm_hodlr;
 typedef struct {
   int32_t rank, leaf_size, depths, leaves, max_rank;
   double mean_rank;
+  int64_t max_block;
   int64_t device_bytes, aca_entries;
   double setup_aca_s, setup_basis_s, setup_factor_s;
 } dafmm_hodlr_stats_t;
-int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, dafmm_hodlr* out);
+int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, int64_t max_block, dafmm_hodlr* out);
 int dafmm_hodlr_solve(dafmm_hodlr p, const void* b, void* x);
 int dafmm_hodlr_stats(dafmm_hodlr p, dafmm_hodlr_stats_t* out);
 int dafmm_hodlr_export(dafmm_hodlr p, const char* path);

@@ -21,6 +21,8 @@ Readings (HR1-HR4):
   HR4  right preconditioning A Ã^{-1} u = f, psi = Ã^{-1} u (the paper writes left preconditioning,
        Eq. hybrid; the right form leaves the GMRES residual equal to the true residual
        ||A psi - f|| / ||f|| that the paper reports).
+  HR5  (option) max_block > 0: sibling blocks with more than max_block rows are dropped (rank 0),
+       so the top of the tree is block diagonal; 0 keeps every block (the paper's HODLR).
 """
 import numpy as np
 
@@ -97,7 +99,7 @@ class HODLR:
     pivots: {(rows_a, rows_b, cols_a, cols_b): (I, J)} with I, J tree positions; built by HR2
     when not given (imported from the product and then only validated, as for the NCA)."""
 
-    def __init__(self, prob, perm, n0, r, pivots=None):
+    def __init__(self, prob, perm, n0, r, pivots=None, max_block=0):
         self.prob, self.perm, self.n0, self.r = prob, np.asarray(perm, dtype=np.int64), n0, r
         self.n = self.perm.size
         self.blocks = sibling_blocks(self.n, n0)
@@ -107,7 +109,7 @@ class HODLR:
                 rows_pts, cols_pts = self.perm[a:b], self.perm[c:d]
                 q = np.abs(prob.q[rows_pts])
                 first = int(np.argmax(q))
-                if not q[first] > 0:
+                if not q[first] > 0 or (max_block > 0 and b - a > max_block):  # HR5
                     pivots[(a, b, c, d)] = (np.zeros(0, np.int64), np.zeros(0, np.int64))
                     continue
                 I, J = aca_fixed_rank(lambda i: A_block(prob, rows_pts[i:i + 1], cols_pts)[0],

@@ -129,6 +129,26 @@ class Tree:
         return sorted(self.boxes[level].keys(), key=lambda k: morton(*k))
 
 
+def level_restricted(tree):
+    """every two leaves that share a boundary (an edge or a corner) are at most one
+    level apart.  Brute force over all leaf pairs by their closed squares (small trees)."""
+    leaves = tree.all_leaves()
+    sq = []
+    for l, (i, j) in leaves:
+        b = tree.width(l)
+        sq.append((l, tree.x0 + i * b, tree.y0 + j * b, b))
+    for p in range(len(sq)):
+        lp, xp, yp, bp = sq[p]
+        for q in range(len(sq)):
+            lq, xq, yq, bq = sq[q]
+            if lq <= lp + 1:
+                continue
+            touch = xp <= xq + bq + 1e-12 and xq <= xp + bp + 1e-12 and yp <= yq + bq + 1e-12 and yq <= yp + bp + 1e-12
+            if touch:
+                return False
+    return True
+
+
 def is_neighbor(tree, level, a, b):
     """N(B) membership: LFR — centres closer than 2b; HFR — centres closer than
     kappa w^2 with w = b/sqrt(2) (R4), i.e. |d| b < kappa b^2 / 2 (w = b: |d| < kappa b).

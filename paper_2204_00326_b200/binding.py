@@ -52,7 +52,8 @@ class Stats(ctypes.Structure):
                 ("p2p_band_entries", ctypes.c_int64 * 48), ("m2l_stored", ctypes.c_int32),
                 ("m2l_store_bytes", ctypes.c_int64), ("m2l_stream_len", ctypes.c_int64), ("n_loc", ctypes.c_int64),
                 ("gmres_reorth", ctypes.c_int64), ("p2p_symmetric", ctypes.c_int32),
-                ("m2l_stored_entries", ctypes.c_int64)]
+                ("m2l_stored_entries", ctypes.c_int64), ("setup_nca_device_s", ctypes.c_double),
+                ("setup_ops_device_s", ctypes.c_double), ("level_restricted", ctypes.c_int32)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}
@@ -64,6 +65,7 @@ class Stats(ctypes.Structure):
 class HodlrStats(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("leaf_size", ctypes.c_int32), ("depths", ctypes.c_int32),
                 ("leaves", ctypes.c_int32), ("max_rank", ctypes.c_int32), ("mean_rank", ctypes.c_double),
+                ("max_block", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("aca_entries", ctypes.c_int64), ("setup_aca_s", ctypes.c_double),
                 ("setup_basis_s", ctypes.c_double), ("setup_factor_s", ctypes.c_double)]
 
@@ -98,7 +100,7 @@ def load():
     lib.dafmm_pass_times.argtypes = [vp, ctypes.POINTER(dbl), ctypes.POINTER(i64), ctypes.POINTER(i64)]
     lib.dafmm_h0_bands.argtypes = [vp, vp, i32]
     lib.dafmm_h0_eval.argtypes = [vp, vp, i64, i32, vp]
-    lib.dafmm_hodlr_create.argtypes = [vp, i32, i32, ctypes.POINTER(vp)]
+    lib.dafmm_hodlr_create.argtypes = [vp, i32, i32, i64, ctypes.POINTER(vp)]
     lib.dafmm_hodlr_solve.argtypes = [vp, vp, vp]
     lib.dafmm_hodlr_stats.argtypes = [vp, ctypes.POINTER(HodlrStats)]
     lib.dafmm_hodlr_export.argtypes = [vp, ctypes.c_char_p]
@@ -227,9 +229,9 @@ def _history_ptr(history, maxit):
     return history.ctypes.data_as(ctypes.c_void_p)
 
 
-def dafmm_hodlr_create(h, rank, leaf_size=64):
+def dafmm_hodlr_create(h, rank, leaf_size=64, max_block=0):
     p = ctypes.c_void_p()
-    _check(load().dafmm_hodlr_create(h, int(rank), int(leaf_size), ctypes.byref(p)))
+    _check(load().dafmm_hodlr_create(h, int(rank), int(leaf_size), int(max_block), ctypes.byref(p)))
     return p
 
 
@@ -376,9 +378,9 @@ class HODLR:
     """Owning wrapper of the HODLR preconditioner of a DAFMM operator:
     ``pc = HODLR(op, rank=16, leaf_size=64); pc.solve(b, x); op.gmres(f, psi, tol, maxit, prec=pc)``."""
 
-    def __init__(self, op, rank=16, leaf_size=64):
+    def __init__(self, op, rank=16, leaf_size=64, max_block=0):
         self.op = op  # keeps the owning handle alive
-        self.p = dafmm_hodlr_create(op.h, rank, leaf_size)
+        self.p = dafmm_hodlr_create(op.h, rank, leaf_size, max_block)
 
     def solve(self, b, x):
         dafmm_hodlr_solve(self.p, self.op.h, b, x)

@@ -174,7 +174,7 @@ int ls_gmres_solve(dafmm_handle h, const void* f, void* psi, double tol, int max
   return rc;
 }
 
-int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, dafmm_hodlr* out) {
+int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, int64_t max_block, dafmm_hodlr* out) {
   if (!out) return fail(DAFMM_EINVAL, "out is null");
   *out = nullptr;
   if (!h) return fail(DAFMM_EINVAL, "null handle");
@@ -184,7 +184,7 @@ int dafmm_hodlr_create(dafmm_handle h, int rank, int leaf_size, dafmm_hodlr* out
     p.reset(new dafmm_hodlr_s());
     p->owner = h;
     std::string err;
-    int rc = dafmm::hodlr_create(h->plan, h->dev, rank, leaf_size, p->hp, err);
+    int rc = dafmm::hodlr_create(h->plan, h->dev, rank, leaf_size, max_block, p->hp, err);
     if (rc != DAFMM_OK) {
       dafmm::hodlr_free(p->hp);
       return fail(rc, err);
@@ -211,6 +211,7 @@ int dafmm_hodlr_stats(dafmm_hodlr p, dafmm_hodlr_stats_t* out) {
   std::memset(out, 0, sizeof(*out));
   out->rank = hp.r;
   out->leaf_size = hp.n0;
+  out->max_block = hp.max_block;
   out->depths = hp.depths;
   out->leaves = (int32_t)hp.leaf_a.size();
   out->max_rank = hp.max_rank;
@@ -328,6 +329,9 @@ int dafmm_stats(dafmm_handle h, dafmm_stats_t* out) {
   out->setup_nca_s = P.t_nca;
   out->setup_ops_s = P.t_ops;
   out->setup_pack_s = P.t_pack;
+  out->setup_nca_device_s = P.t_nca_device;
+  out->level_restricted = P.level_restricted ? 1 : 0;
+  out->setup_ops_device_s = h->dev.t_ops_device;
   out->setup_upload_s = P.t_upload;
   out->aca_entries = P.aca_entries;
   out->m2l_stored = h->dev.m2l_mat != nullptr ? (h->m2l_sym ? 2 : 1) : 0;

@@ -23,6 +23,7 @@ enum ProfEvent {
 struct DevBatch {
   int items = 0;
   bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
+  int ipw = 1;        // translate_rows_kernel: items per warp (lane groups of 32 / ipw)
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;
@@ -123,6 +124,7 @@ struct DevPlan {
   int gm_part_blocks = 0;
   int64_t gm_reorth = 0;       // reorthogonalisation passes in the last ls_gmres_solve
   size_t device_bytes = 0;
+  double t_ops_device = 0;       // upload_plan: operator formation on the device (F2)
   std::vector<void*> allocations;
   // per-pass CUDA-event profiling (dafmm_set_profiling / dafmm_pass_times)
   int64_t launches = 0;          // kernels launched by run_matvec / run_gmres since the last reset

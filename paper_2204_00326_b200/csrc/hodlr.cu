@@ -16,9 +16,11 @@
 // solves and then each depth's (I + W Z^H)^{-1} are applied to the U columns of all coarser
 // depths (one N x (depths r) row-major matrix, Ucat).
 //
-// Layout: per point t (tree position) and depth, r complex columns of Ucat (W rows) and of Vcat
-// (A[I_sib, t], the point's column of the sibling block's V^H), zero-padded beyond the block's
-// rank.  Padding is exact: a zero column of Vcat / Ucat adds identity rows and columns to S.
+// Layout: one plane per depth, N x r row-major: per point t (tree position), r complex values of
+// Ucat (its row of W) and of Vcat (A[I_sib, t], its column of the sibling block's V^H),
+// zero-padded beyond the block's rank.  Padding is exact: a zero column of Vcat / Ucat adds
+// identity rows and columns to S.  Column c of the factorisation's right-hand sides (the U of
+// all depths) is value c % r of plane c / r.
 // Kernels per depth: segdot (Y_gamma = sum_t Vcat[t]^T X[t] over parts of each child),
 // node (S factor / solve per split node), update (X[t] -= W[t] C_nu(t)).  The same kernels run the
 // factorisation (X = Ucat, column chunks) and the apply (X = one vector).
@@ -77,6 +79,17 @@ struct AEntries {
   }
 };
 
+// Element (t, c) of a set of column planes: p + (c / pc) plane + t rs + c % pc.  The U planes
+// (pc = rs = r, plane = N r) or one vector (pc = rs = 1).
+struct XA {
+  double2* p;
+  int64_t plane;
+  int pc, rs;
+  __device__ __forceinline__ double2& at(int64_t t, int c) const {
+    return p[(int64_t)(c / pc) * plane + t * rs + c % pc];
+  }
+};
+
 // ---- leaves: dense A[leaf, leaf] and its LU ----
 __global__ void hodlr_leaf_lu_kernel(const int64_t* __restrict__ la, const int32_t* __restrict__ ln,
                                      const int64_t* __restrict__ lu_off, AEntries A, double2* __restrict__ lu,
@@ -99,8 +112,7 @@ __global__ void hodlr_leaf_lu_kernel(const int64_t* __restrict__ la, const int32
 // X[leaf rows, xc0 .. xc0 + nc) <- A_leaf^{-1} X (factorisation: many columns, one per thread)
 __global__ void hodlr_leaf_solve_multi_kernel(const int64_t* __restrict__ la, const int32_t* __restrict__ ln,
                                               const int64_t* __restrict__ lu_off, const double2* __restrict__ lu,
-                                              const int32_t* __restrict__ prow, double2* __restrict__ X, int ldx,
-                                              int nc) {
+                                              const int32_t* __restrict__ prow, XA X, int nc) {
   extern __shared__ double2 M[];
   const int leaf = blockIdx.x;
   const int64_t a = la[leaf];
@@ -110,14 +122,14 @@ __global__ void hodlr_leaf_solve_multi_kernel(const int64_t* __restrict__ la, co
   const int32_t* pr = prow + (int64_t)leaf * kMaxLeaf;
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
     double2 v[kMaxLeaf];
-    for (int i = 0; i < n; ++i) v[i] = X[(a + pr[i]) * ldx + c];
+    for (int i = 0; i < n; ++i) v[i] = X.at(a + pr[i], c);
     for (int i = 1; i < n; ++i)
       for (int j = 0; j < i; ++j) cfms2(v[i], M[j * n + i], v[j]);
     for (int i = n - 1; i >= 0; --i) {
       for (int j = i + 1; j < n; ++j) cfms2(v[i], M[j * n + i], v[j]);
       v[i] = cdiv2(v[i], M[i * n + i]);
     }
-    for (int i = 0; i < n; ++i) X[(a + i) * ldx + c] = v[i];
+    for (int i = 0; i < n; ++i) X.at(a + i, c) = v[i];
   }
 }
 
@@ -170,8 +182,8 @@ __global__ void hodlr_leaf_solve_vec_kernel(int nleaves, const int64_t* __restri
 __global__ void hodlr_basis_u_kernel(const int32_t* __restrict__ tiles, const int64_t* __restrict__ ca,
                                      const int64_t* __restrict__ cb, const int32_t* __restrict__ ck,
                                      const int32_t* __restrict__ po, const int32_t* __restrict__ bI,
-                                     const int32_t* __restrict__ bJ, AEntries A, double2* __restrict__ Ucat, int ld,
-                                     int col0, int r, int* status) {
+                                     const int32_t* __restrict__ bJ, AEntries A, double2* __restrict__ Up, int r,
+                                     int* status) {
   __shared__ PolyTable T;
   __shared__ double2 C[kMaxRank * kMaxRank];
   __shared__ int s_perm[kMaxRank];
@@ -186,7 +198,7 @@ __global__ void hodlr_basis_u_kernel(const int32_t* __restrict__ tiles, const in
   const int64_t t = ca[g] + t0 + threadIdx.x;
   if (k == 0) {
     if (t < rb)
-      for (int c = 0; c < r; ++c) Ucat[t * ld + col0 + c] = make_double2(0.0, 0.0);
+      for (int c = 0; c < r; ++c) Up[t * r + c] = make_double2(0.0, 0.0);
     return;
   }
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) C[e] = A(I[e % k], J[e / k], T);
@@ -206,16 +218,16 @@ __global__ void hodlr_basis_u_kernel(const int32_t* __restrict__ tiles, const in
     for (int i = j + 1; i < k; ++i) cfms2(s, a[i], C[j * k + i]);
     a[j] = s;
   }
-  double2* out = Ucat + t * ld + col0;
+  double2* out = Up + t * r;
   for (int c = k; c < r; ++c) out[c] = make_double2(0.0, 0.0);
   for (int i = 0; i < k; ++i) out[s_perm[i]] = a[i];
 }
 
-// Vcat rows of the columns of block g: t in sib(g) = [sa[g], sb[g]): Vcat[t, col0 + i] = A[I_i, t]
+// Vcat rows of the columns of block g: t in sib(g) = [sa[g], sb[g]): Vp[t r + i] = A[I_i, t]
 __global__ void hodlr_basis_v_kernel(const int32_t* __restrict__ tiles, const int64_t* __restrict__ sa,
                                      const int64_t* __restrict__ sb, const int32_t* __restrict__ ck,
                                      const int32_t* __restrict__ po, const int32_t* __restrict__ bI, AEntries A,
-                                     double2* __restrict__ Vcat, int ld, int col0, int r) {
+                                     double2* __restrict__ Vp, int r) {
   __shared__ PolyTable T;
   load_poly_table(T);
   const int g = tiles[2 * blockIdx.x], t0 = tiles[2 * blockIdx.x + 1];
@@ -223,23 +235,74 @@ __global__ void hodlr_basis_v_kernel(const int32_t* __restrict__ tiles, const in
   if (t >= sb[g]) return;
   const int k = ck[g];
   const int32_t* I = bI + po[g];
-  double2* out = Vcat + t * ld + col0;
+  double2* out = Vp + t * r;
   for (int i = 0; i < r; ++i) out[i] = i < k ? A(I[i], t, T) : make_double2(0.0, 0.0);
 }
 
 // ---- per depth: Y partials over parts (part = child id, t0, t1) ----
-// partial[(p r + i) nc + c] = sum_{t in part p} Vcat[t, vcol + i] X[t, xc0 + c]
-__global__ void hodlr_segdot_kernel(const int32_t* __restrict__ parts, const double2* __restrict__ Vcat, int ld,
-                                    int vcol, int r, const double2* __restrict__ X, int64_t ldx, int xc0, int nc,
-                                    double2* __restrict__ partial) {
+// partial[(p r + i) nc + c] = sum_{t in part p} Vp[t r + i] X(t, xc0 + c)   (factorisation)
+__global__ void hodlr_segdot_kernel(const int32_t* __restrict__ parts, const double2* __restrict__ Vp, int r, XA X,
+                                    int xc0, int nc, double2* __restrict__ partial) {
   const int p = blockIdx.x;
   const int tc = max(1, (int)blockDim.x / r);
   const int i = threadIdx.x / tc, c = blockIdx.y * tc + threadIdx.x % tc;
   if (i >= r || c >= nc) return;
   const int64_t t0 = parts[3 * p + 1], t1 = parts[3 * p + 2];
   double2 acc = make_double2(0.0, 0.0);
-  for (int64_t t = t0; t < t1; ++t) cfma2(acc, Vcat[t * ld + vcol + i], X[t * ldx + xc0 + c]);
+  for (int64_t t = t0; t < t1; ++t) cfma2(acc, Vp[t * r + i], X.at(t, xc0 + c));
   partial[((int64_t)p * r + i) * nc + c] = acc;
+}
+
+// apply (one vector): partial[p r + i] = sum_{t in part p} Vp[t r + i] x[t]; the CTA's threads
+// are (row slot, i) with rp = r rounded up to a power of two lanes per row, so each row's r
+// values are one contiguous read; the slots are summed in a fixed order.
+__global__ void __launch_bounds__(256) hodlr_segdot_vec_kernel(const int32_t* __restrict__ parts,
+                                                               const double2* __restrict__ Vp, int r, int rp,
+                                                               const double2* __restrict__ x,
+                                                               double2* __restrict__ partial) {
+  __shared__ double2 red[256];
+  const int p = blockIdx.x;
+  const int slot = threadIdx.x / rp, i = threadIdx.x % rp, nslot = blockDim.x / rp;
+  const int64_t t0 = parts[3 * p + 1], t1 = parts[3 * p + 2];
+  double2 acc = make_double2(0.0, 0.0);
+  if (i < r)
+    for (int64_t t = t0 + slot; t < t1; t += nslot) cfma2(acc, Vp[t * r + i], x[t]);
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < r) {
+    double2 sm = make_double2(0.0, 0.0);
+    for (int q = 0; q < nslot; ++q) {
+      sm.x += red[q * rp + threadIdx.x].x;
+      sm.y += red[q * rp + threadIdx.x].y;
+    }
+    partial[(int64_t)p * r + threadIdx.x] = sm;
+  }
+}
+
+// apply: x[t] -= sum_i Up[t r + i] C[nu][half r + i] over the rows of part p (child 2 nu + half);
+// rp lanes per row, reduced by xor shuffles within the lane group.
+__global__ void __launch_bounds__(256) hodlr_update_vec_kernel(const int32_t* __restrict__ parts,
+                                                               const double2* __restrict__ Up, int r, int rp,
+                                                               const double2* __restrict__ C,
+                                                               double2* __restrict__ x) {
+  const int p = blockIdx.x;
+  const int child = parts[3 * p];
+  const int slot = threadIdx.x / rp, i = threadIdx.x % rp, nslot = blockDim.x / rp;
+  const int64_t t0 = parts[3 * p + 1], t1 = parts[3 * p + 2];
+  const double2 cc = i < r ? C[(int64_t)(child >> 1) * 2 * r + (child & 1) * r + i] : make_double2(0.0, 0.0);
+  for (int64_t base = t0; base < t1; base += nslot) {  // uniform trip count: every lane shuffles
+    const int64_t t = base + slot;
+    double2 v = make_double2(0.0, 0.0);
+    if (t < t1 && i < r) cfma2(v, Up[t * r + i], cc);
+    for (int o = rp >> 1; o > 0; o >>= 1) {
+      v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+      v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    }
+    if (t < t1 && i == 0) {
+      x[t].x -= v.x;
+      x[t].y -= v.y;
+    }
+  }
 }
 
 // Y_gamma[i][c]: the sum of the child's parts, in part order
@@ -315,10 +378,9 @@ __global__ void hodlr_node_kernel(const int32_t* __restrict__ pptr, const double
   }
 }
 
-// X[t, xc0 + c] -= sum_i Ucat[t, ucol + i] C[nu][half(t) r + i][c] for t in split node nu
-__global__ void hodlr_update_kernel(int nnodes, const int64_t* __restrict__ amb, const double2* __restrict__ Ucat,
-                                    int ld, int ucol, int r, const double2* __restrict__ C, int ncs,
-                                    double2* __restrict__ X, int64_t ldx, int xc0, int64_t n) {
+// X(t, xc0 + c) -= sum_i Up[t r + i] C[nu][half(t) r + i][c] for t in split node nu (factorisation)
+__global__ void hodlr_update_kernel(int nnodes, const int64_t* __restrict__ amb, const double2* __restrict__ Up,
+                                    int r, const double2* __restrict__ C, int ncs, XA X, int xc0, int64_t n) {
   const int64_t total = n * ncs;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = e / ncs;
@@ -333,10 +395,10 @@ __global__ void hodlr_update_kernel(int nnodes, const int64_t* __restrict__ amb,
     if (t >= amb[3 * lo + 2]) continue;
     const int half = t >= amb[3 * lo + 1] ? 1 : 0;
     const double2* cc = C + ((int64_t)lo * 2 * r + half * r) * ncs + c;
-    const double2* u = Ucat + t * ld + ucol;
+    const double2* u = Up + t * r;
     double2 acc = make_double2(0.0, 0.0);
     for (int i = 0; i < r; ++i) cfma2(acc, u[i], cc[(int64_t)i * ncs]);
-    double2& x = X[t * ldx + xc0 + c];
+    double2& x = X.at(t, xc0 + c);
     x.x -= acc.x;
     x.y -= acc.y;
   }
@@ -371,28 +433,43 @@ int grid_for(int64_t work, int threads) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, 148 * 16));
 }
 
-// one round of the per-depth kernels on columns [xc0, xc0 + nc) of X (segdot, node, update)
-int depth_round(HodlrPlan& h, int d, double2* X, int64_t ldx, int xc0, int nc, bool factor, cudaStream_t s,
-                std::string& err) {
+// one round of the per-depth kernels on columns [xc0, xc0 + nc) of the U planes (factorisation:
+// segdot, node factor / solve, update)
+int factor_round(HodlrPlan& h, int d, int xc0, int nc, bool gcols, cudaStream_t s, std::string& err) {
   const int r = h.r, nn = (int)h.split_a[d].size();
   if (nn == 0) return DAFMM_OK;
-  const int vcol = d * r;
-  // factor round: the G columns (block d of Ucat) first; otherwise the solve columns
+  const int64_t plane = h.n * (int64_t)r;
+  const XA X{h.Ucat, plane, r, r};
+  const double2* Vp = h.Vcat + d * plane;
+  const double2* Up = h.Ucat + d * plane;
   const int tc = std::max(1, 256 / r);
   const int threads = ((std::min(nc, tc) * r + 31) / 32) * 32;
   dim3 grid(h.nparts[d], (nc + tc - 1) / tc);
-  hodlr_segdot_kernel<<<grid, threads, 0, s>>>(h.part_d[d], h.Vcat, h.ld, vcol, r, X, ldx, xc0, nc, h.partial);
+  hodlr_segdot_kernel<<<grid, threads, 0, s>>>(h.part_d[d], Vp, r, X, xc0, nc, h.partial);
   const size_t smem = (size_t)4 * r * r * sizeof(double2);
-  if (factor) {
+  if (gcols) {  // the G columns (depth d's own U): S_nu = I + Z^H W, factored
     hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, 0, 0, h.S_lu[d], h.S_prow[d], h.C,
-                                         h.status);
-    return ck(cudaGetLastError(), err, "hodlr factor round") ? DAFMM_OK : DAFMM_ECUDA;
+                                            h.status);
+  } else {
+    hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, -1, nc, h.S_lu[d], h.S_prow[d], h.C,
+                                            h.status);
+    hodlr_update_kernel<<<grid_for(h.n * nc, 256), 256, 0, s>>>(nn, h.split_d[d], Up, r, h.C, nc, X, xc0, h.n);
   }
-  hodlr_node_kernel<<<nn, nc == 1 ? 32 : 128, nc == 1 ? 0 : smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, -1, nc, h.S_lu[d],
-                                                      h.S_prow[d], h.C, h.status);
-  hodlr_update_kernel<<<grid_for(h.n * nc, 256), 256, 0, s>>>(nn, h.split_d[d], h.Ucat, h.ld, vcol, r, h.C, nc, X,
-                                                              ldx, xc0, h.n);
-  return ck(cudaGetLastError(), err, "hodlr depth round") ? DAFMM_OK : DAFMM_ECUDA;
+  return ck(cudaGetLastError(), err, "hodlr factor round") ? DAFMM_OK : DAFMM_ECUDA;
+}
+
+// one depth of the apply on the tree-order vector h.xt: b <- b - W S^{-1} Z^H b
+int apply_round(HodlrPlan& h, int d, cudaStream_t s, std::string& err) {
+  const int r = h.r, nn = (int)h.split_a[d].size();
+  if (nn == 0) return DAFMM_OK;
+  int rp = 1;
+  while (rp < r) rp <<= 1;
+  const int64_t plane = h.n * (int64_t)r;
+  hodlr_segdot_vec_kernel<<<h.nparts[d], 256, 0, s>>>(h.part_d[d], h.Vcat + d * plane, r, rp, h.xt, h.partial);
+  hodlr_node_kernel<<<nn, 32, 0, s>>>(h.part_ptr_d[d], h.partial, r, 1, -1, 1, h.S_lu[d], h.S_prow[d], h.C,
+                                      h.status);
+  hodlr_update_vec_kernel<<<h.nparts[d], 256, 0, s>>>(h.part_d[d], h.Ucat + d * plane, r, rp, h.C, h.xt);
+  return ck(cudaGetLastError(), err, "hodlr apply round") ? DAFMM_OK : DAFMM_ECUDA;
 }
 
 bool write_npy_i64(const std::string& path, const std::vector<int64_t>& v, std::vector<int64_t> shape) {
@@ -420,10 +497,13 @@ void hodlr_free(HodlrPlan& h) {
   h.device_bytes = 0;
 }
 
-int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, HodlrPlan& h, std::string& err) {
+int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64_t max_block, HodlrPlan& h,
+                 std::string& err) {
   if (P.opt.kernel_mode != 0) { err = "the HODLR preconditioner needs kernel_mode 0 (Lippmann-Schwinger)"; return DAFMM_EINVAL; }
   if (rank < 1 || rank > kMaxRank) { err = "HODLR rank must be in [1, 32]"; return DAFMM_EINVAL; }
   if (leaf_size < 1 || leaf_size > kMaxLeaf) { err = "HODLR leaf size must be in [1, 64]"; return DAFMM_EINVAL; }
+  if (max_block < 0) { err = "HODLR max_block must be >= 0"; return DAFMM_EINVAL; }
+  h.max_block = max_block;
   const int64_t n = P.n;
   h.n = n;
   h.r = rank;
@@ -501,7 +581,8 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, Hodlr
             const double aq = std::fabs(P.q[P.perm[t]]);
             if (aq > bq) { bq = aq; best = t; }
           }
-          if (best < 0) continue;
+          // HR5 (option): blocks of more than max_block rows are dropped (rank 0)
+          if (best < 0 || (max_block > 0 && rb - ra > max_block)) continue;
           AcaProblem pr{};
           pr.row_off = ra;
           pr.col_off = c0;
@@ -621,10 +702,11 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, Hodlr
       ok = ck(cudaFuncSetAttribute(hodlr_basis_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), err,
               "smem attr");
       if (ok) {
+        const int64_t plane = n * (int64_t)rank;
         hodlr_basis_u_kernel<<<(int)(tu.size() / 2), 128, smem, s>>>(d_tu, d_ca, d_cb, d_ck, d_po, d_I, d_J, A,
-                                                                     h.Ucat, h.ld, dd * rank, rank, h.status);
-        hodlr_basis_v_kernel<<<(int)(tv.size() / 2), 128, 0, s>>>(d_tv, d_sa, d_sb, d_ck, d_po, d_I, A, h.Vcat, h.ld,
-                                                                  dd * rank, rank);
+                                                                     h.Ucat + dd * plane, rank, h.status);
+        hodlr_basis_v_kernel<<<(int)(tv.size() / 2), 128, 0, s>>>(d_tv, d_sa, d_sb, d_ck, d_po, d_I, A,
+                                                                  h.Vcat + dd * plane, rank);
         ok = ck(cudaGetLastError(), err, "hodlr basis") && ck(cudaStreamSynchronize(s), err, "hodlr basis");
       }
     }
@@ -659,13 +741,14 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, Hodlr
   // (deepest split first): factor S from block d (the G columns), apply (I + W Z^H)^{-1} of the
   // depth to the U columns of the coarser depths, chunk by chunk ----
   hodlr_leaf_solve_multi_kernel<<<nleaves, 64, leaf_smem, s>>>(h.leaf_a_d, h.leaf_n_d, h.leaf_lu_off, h.leaf_lu,
-                                                              h.leaf_prow, h.Ucat, h.ld, h.ld);
+                                                              h.leaf_prow, XA{h.Ucat, n * (int64_t)rank, rank, rank},
+                                                              h.ld);
   if (!ck(cudaGetLastError(), err, "hodlr leaf solve")) return DAFMM_ECUDA;
   for (int dd = h.depths - 1; dd >= 0; --dd) {
-    int rc = depth_round(h, dd, h.Ucat, h.ld, dd * rank, rank, true, s, err);
+    int rc = factor_round(h, dd, dd * rank, rank, true, s, err);
     if (rc != DAFMM_OK) return rc;
     for (int c0 = 0; c0 < dd * rank; c0 += kChunk) {
-      rc = depth_round(h, dd, h.Ucat, h.ld, c0, std::min(kChunk, dd * rank - c0), false, s, err);
+      rc = factor_round(h, dd, c0, std::min(kChunk, dd * rank - c0), false, s, err);
       if (rc != DAFMM_OK) return rc;
     }
   }
@@ -686,7 +769,7 @@ int hodlr_apply(HodlrPlan& h, const double2* in, double2* out, cudaStream_t s, s
   hodlr_leaf_solve_vec_kernel<<<(nleaves + 3) / 4, 128, 0, s>>>(nleaves, h.leaf_a_d, h.leaf_n_d, h.leaf_lu_off,
                                                                 h.leaf_lu, h.leaf_prow, h.xt);
   for (int dd = h.depths - 1; dd >= 0; --dd) {
-    int rc = depth_round(h, dd, h.xt, 1, 0, 1, false, s, err);
+    int rc = apply_round(h, dd, s, err);
     if (rc != DAFMM_OK) return rc;
   }
   hodlr_scatter_kernel<<<g, 256, 0, s>>>(n, h.perm, h.xt, out);
@@ -710,7 +793,7 @@ int hodlr_export(const HodlrPlan& h, const Plan& P, const std::string& dir, std:
         ptr.push_back((int64_t)I.size());
       }
     }
-  const std::vector<int64_t> meta = {h.r, h.n0, h.n};
+  const std::vector<int64_t> meta = {h.r, h.n0, h.n, h.max_block};
   bool ok = write_npy_i64(dir + "/hodlr_blocks.npy", blocks, {(int64_t)blocks.size() / 5, 5}) &&
             write_npy_i64(dir + "/hodlr_piv_ptr.npy", ptr, {(int64_t)ptr.size()}) &&
             write_npy_i64(dir + "/hodlr_I.npy", I, {(int64_t)I.size()}) &&

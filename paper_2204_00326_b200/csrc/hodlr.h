@@ -17,6 +17,7 @@ namespace dafmm {
 struct HodlrPlan {
   int64_t n = 0;
   int r = 0, n0 = 0;
+  int64_t max_block = 0;  // HR5: blocks with more rows are dropped (0: none)
   int depths = 0;   // depths with split nodes (0 .. depths - 1); pairs live at depths 1 .. depths
   int ld = 0;       // columns of Ucat / Vcat = depths * r
   cudaStream_t stream = nullptr;  // the owning DAFMM handle's stream at creation / solve
@@ -58,7 +59,8 @@ struct HodlrPlan {
 
 // Build Ã of the plan's operator (kernel_mode 0 only) on the device: pivots by the fixed-rank
 // ACA (HR2, device), bases, leaf LU and the recursive factorisation (HR3).
-int hodlr_create(const Plan& plan, const DevPlan& d, int rank, int leaf_size, HodlrPlan& h, std::string& err);
+int hodlr_create(const Plan& plan, const DevPlan& d, int rank, int leaf_size, int64_t max_block, HodlrPlan& h,
+                 std::string& err);
 // out = Ã^{-1} in (device pointers, caller order), enqueued on `s`; in may equal out.
 int hodlr_apply(HodlrPlan& h, const double2* in, double2* out, cudaStream_t s, std::string& err);
 void hodlr_free(HodlrPlan& h);

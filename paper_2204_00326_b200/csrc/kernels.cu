@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <cstdio>
 #include <cstring>
@@ -155,21 +156,24 @@ __global__ void translate_kernel(int items, const int64_t* __restrict__ dst_off,
   }
 }
 
-// Narrow items (few columns, e.g. directional L2L with 2 parent cones): one warp per item,
-// lanes own rows and walk their contiguous row, 4 columns per step into 4 accumulators.
+// Narrow items (few columns, e.g. directional L2L with 2 parent cones): a group of g = 32 / ipw
+// lanes per item (ipw items per warp, g >= the batch's largest row count when ipw > 1), lanes own
+// rows and walk their contiguous row, 4 columns per step into 4 accumulators.
 __global__ void translate_rows_kernel(int items, const int64_t* __restrict__ dst_off,
                                       const int32_t* __restrict__ dst_rows, const int64_t* __restrict__ item_mat_off,
                                       const int32_t* __restrict__ item_cols, const int32_t* __restrict__ term_ptr,
                                       const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
                                       const double2* __restrict__ ops, const double2* __restrict__ src,
-                                      double2* __restrict__ dst, int accumulate) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= items) return;
-  const int R = dst_rows[warp], C = item_cols[warp];
-  const int tb = term_ptr[warp], te = term_ptr[warp + 1];
-  const int64_t doff = dst_off[warp];
-  for (int r = lane; r < R; r += 32) {
+                                      double2* __restrict__ dst, int accumulate, int ipw) {
+  const int g = 32 / ipw;
+  const int lane = (threadIdx.x & 31) % g;
+  const int item = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * ipw + (threadIdx.x & 31) / g;
+  if (item >= items) return;
+  const int R = dst_rows[item], C = item_cols[item];
+  const int tb = term_ptr[item], te = term_ptr[item + 1];
+  const int64_t doff = dst_off[item];
+  const int warp = item;
+  for (int r = lane; r < R; r += g) {
     const double2* row = ops + item_mat_off[warp] + (int64_t)r * C;
     double ar[4] = {0.0, 0.0, 0.0, 0.0}, ai[4] = {0.0, 0.0, 0.0, 0.0};
     int cs = 0;
@@ -964,6 +968,8 @@ constexpr int kPThreads = kPC + 32;
 constexpr int kPStages = DAFMM_PSTAGES;
 constexpr int kPIdx = kMSCols / kPC;
 constexpr size_t kPDynSmem = sizeof(double2) * kPStages * kMSStageE;
+// named barrier 2 over the pair kernel's kPC consumer threads (barrier 1 counts kMSConsumers)
+__device__ __forceinline__ void pair_consumers_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kPC) : "memory"); }
 static_assert(kMSCols % kPC == 0, "multipole gather: whole indices per thread");
 struct MSPUnit {
   int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
@@ -1119,7 +1125,7 @@ __global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
       ar0 = ai0 = ar1 = ai1 = 0.0;
     }
     cp_async_wait_all();
-    consumers_sync();  // u's multipoles complete; everyone is done with the other buffers
+    pair_consumers_sync();  // u's multipoles complete; everyone is done with the other buffers
     const double2* mv = mb[buf];
     const double2* msf = mself[buf];
     const int nc = u.c1 - u.c0;
@@ -1198,9 +1204,9 @@ __global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
     if (u.flags & 2) {  // reduce the slices of each row, write u_B's own share
       // (in mb[buf], free once every consumer has finished the unit's passes)
       double2* red = mb[buf];
-      consumers_sync();
+      pair_consumers_sync();
       red[j] = make_double2(ar0 + ar1, ai0 + ai1);
-      consumers_sync();
+      pair_consumers_sync();
       if (j < r) {
         double sr = 0.0, si = 0.0;
         for (int q = j; q < P; q += r) {
@@ -1601,6 +1607,10 @@ bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& 
   int64_t cols = 0;
   for (int32_t c : h.item_cols) cols += c;
   b.wide = b.items > 0 && cols >= 48 * (int64_t)b.items;
+  // narrow items: several per warp when their rows fit a lane group (16 or 8 lanes)
+  int maxr = 0;
+  for (int32_t r : h.dst_rows) maxr = std::max(maxr, (int)r);
+  b.ipw = maxr <= 8 ? 4 : maxr <= 16 ? 2 : 1;
   return upload(d, &b.dst_off, h.dst_off, err) && upload(d, &b.dst_rows, h.dst_rows, err) &&
          upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.item_mat_off, h.item_mat_off, err) &&
          upload(d, &b.item_cols, h.item_cols, err) &&
@@ -1616,8 +1626,9 @@ int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, do
     translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
                                                  b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
   else
-    translate_rows_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
-                                                      b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
+    translate_rows_kernel<<<(b.items + 8 * b.ipw - 1) / (8 * b.ipw), threads, 0, st>>>(
+        b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols, b.term_ptr, b.src_off, b.src_cols, d.ops, src,
+        dst, accumulate, b.ipw);
   return 1;
 }
 
@@ -1658,8 +1669,10 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
       const auto& a = pk.opd_jobs[j];
       jobs[j] = OpJob{a.off, a.rows, a.col_start, a.stride, 0, a.src_off, a.src_len, 0};
     }
+    const auto t0 = std::chrono::steady_clock::now();
     const int rc = form_ops_device(plan.pts.data(), plan.n, plan.kappa, pk.opd_piv, groups, jobs, d.ops, err);
     if (rc != DAFMM_OK) return rc;
+    d.t_ops_device = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   }
   d.m2l_targets = (int)pk.m2l_loc_off.size();
   d.m2l_leaf_targets = pk.m2l_leaf_targets;

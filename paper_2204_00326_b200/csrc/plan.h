@@ -64,6 +64,7 @@ struct Plan {
   double W = 0, x0 = 0, y0 = 0;
   int L = 0;                         // deepest level
   bool multi_level_leaves = false;   // leaves on more than one level (adaptive tree)
+  bool level_restricted = true;      // adjacent leaves differ by at most one level
   // input copies (original order)
   std::vector<double> pts, w, q;
   std::vector<zd> D;                 // self terms D_i (original order)
@@ -74,6 +75,7 @@ struct Plan {
   std::vector<std::vector<NodePivots>> piv;  // [level][node]
   // statistics
   double t_tree = 0, t_lists = 0, t_nca = 0, t_ops = 0, t_pack = 0, t_upload = 0;
+  double t_nca_device = 0;  // inside t_nca: the device ACA launches (upload, kernel, download)
   int64_t aca_entries = 0;
 };
 

@@ -434,6 +434,40 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
     leaf_levels += any ? 1 : 0;
   }
   P.multi_level_leaves = leaf_levels > 1;
+  // level restriction (boxes sharing a boundary are at most one level apart) -- a
+  // property of the input tree, reported (dafmm_stats.level_restricted), not required: the
+  // near field folds the U / W / X lists in either way (R18)
+  {
+    std::vector<std::vector<int>> deep(L + 1);  // deepest leaf level in each box's subtree
+    for (int l = L; l >= 0; --l) {
+      const Level& lv = P.levels[l];
+      deep[l].assign(lv.boxes.size(), l);
+      if (l < L) {
+        const Level& ch = P.levels[l + 1];
+        for (size_t b = 0; b < lv.boxes.size(); ++b) {
+          if (lv.boxes[b].leaf) continue;
+          for (int c = 0; c < 4; ++c) {
+            auto it = ch.index.find(pack_key(2 * lv.boxes[b].ix + (c & 1), 2 * lv.boxes[b].iy + (c >> 1)));
+            if (it != ch.index.end()) deep[l][b] = std::max(deep[l][b], deep[l + 1][it->second]);
+          }
+        }
+      }
+    }
+    P.level_restricted = true;
+    for (int l = 0; l <= L && P.level_restricted; ++l) {
+      const Level& lv = P.levels[l];
+      for (const Box& B : lv.boxes) {
+        if (!B.leaf) continue;
+        for (int dx = -1; dx <= 1; ++dx)
+          for (int dy = -1; dy <= 1; ++dy) {
+            if (!dx && !dy) continue;
+            auto it = lv.index.find(pack_key(B.ix + dx, B.iy + dy));
+            if (B.ix + dx >= 0 && B.iy + dy >= 0 && it != lv.index.end() && deep[l][it->second] > l + 1)
+              P.level_restricted = false;
+          }
+      }
+    }
+  }
   P.D.assign(n, zd(0.0, 0.0));
   if (opt.self_term == 1)
     for (int64_t i = 0; i < n; ++i) P.D[i] = self_term_disk(kappa, P.w[i]);
@@ -758,7 +792,9 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
         if (dirs == 2) probs[(size_t)dirs * t + 1] = {set_off(t, 2), set_off(t, 3), set_len(t, 2), set_len(t, 3), 0, 0, 0, 0, 0};
       }
       std::vector<int32_t> prow, pcol, rank;
+      const double td = now_s();
       int rc = dev_aca->run(idx, probs, eps, prow, pcol, rank, level_entries, err);
+      P.t_nca_device += now_s() - td;
       if (rc != DAFMM_OK) return rc;
 #pragma omp parallel for schedule(dynamic, 16)
       for (int t = 0; t < ns; ++t) {

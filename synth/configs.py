@@ -60,10 +60,11 @@ def smoothed_disk_q(pts, radius=0.5, sharpness=200.0):
     return 0.5 * (1.0 + np.tanh(sharpness * (radius - r)))
 
 
-def adaptive_leaves(kappa, max_depth, tol=1e-3, T=16.0, qfun=smoothed_disk_q):
+def adaptive_leaves(kappa, max_depth, tol=1e-3, T=16.0, qfun=smoothed_disk_q, balance=True):
     """Leaves (level, i, j) of the config-5 quadtree on [-1,1]^2: split a box while
     max over its corners |q(corner) - q(centre)| > tol, up to max_depth, and (refinement rule 3,
-    P:204) while it is in the high-frequency regime (kappa b)^2 > T, so every leaf is LFR."""
+    P:204) while it is in the high-frequency regime (kappa b)^2 > T, so every leaf is LFR; then
+    (balance=True, the paper's level-restricted tree) level_restrict."""
     leaves, stack = [], [(0, 0, 0)]
     while stack:
         level, i, j = stack.pop()
@@ -77,7 +78,52 @@ def adaptive_leaves(kappa, max_depth, tol=1e-3, T=16.0, qfun=smoothed_disk_q):
             stack += [(level + 1, 2 * i + di, 2 * j + dj) for dj in (1, 0) for di in (1, 0)]
         else:
             leaves.append((level, i, j))
+    if balance:
+        leaves = level_restrict(leaves)
     return sorted(leaves)
+
+
+def _deepest_leaf(leafset, level, i, j):
+    """Level of the deepest leaf inside box (level, i, j), or of the leaf covering it."""
+    key = (level, i, j)
+    if key in leafset:
+        return level
+    lv, a, b = level, i, j
+    while lv > 0:  # a coarser leaf covers the box
+        lv, a, b = lv - 1, a >> 1, b >> 1
+        if (lv, a, b) in leafset:
+            return lv
+    best, stack = -1, [key]
+    while stack:
+        lv, a, b = stack.pop()
+        for c in ((lv + 1, 2 * a + da, 2 * b + db) for db in (0, 1) for da in (0, 1)):
+            if c in leafset:
+                best = max(best, c[0])
+            elif c[0] < 31:
+                stack.append(c)
+    return best
+
+
+def level_restrict(leaves):
+    """Level-restricted tree ("any two boxes that share a boundary are not more than
+    one level apart"): split every leaf that touches (edge or corner) a leaf more than one level
+    finer, until none does.  Splits only add resolution, so the refinement rules still hold."""
+    leafset = set(leaves)
+    changed = True
+    while changed:
+        changed = False
+        for (level, i, j) in sorted(leafset):
+            if (level, i, j) not in leafset:
+                continue
+            n = 1 << level
+            deep = max((_deepest_leaf(leafset, level, i + di, j + dj)
+                        for di in (-1, 0, 1) for dj in (-1, 0, 1)
+                        if (di or dj) and 0 <= i + di < n and 0 <= j + dj < n), default=-1)
+            if deep > level + 1:
+                leafset.remove((level, i, j))
+                leafset.update((level + 1, 2 * i + di, 2 * j + dj) for dj in (0, 1) for di in (0, 1))
+                changed = True
+    return sorted(leafset)
 
 
 def adaptive_grid(leaves, per_side=8):
@@ -119,17 +165,17 @@ def l_shaped_problem(n=4000, kappa=40.0, seed=7, nca_tol=1e-8):
                 f=plane_wave_rhs(pts, q, kappa), gmres_tol=1e-8, n_grid=None)
 
 
-def make_problem(name, n=None, kappa=None):
+def make_problem(name, n=None, kappa=None, balance=True):
     """Return dict(points, weights, q, kappa, nca_tol, leaf_size, x, f, gmres_tol) for a config.
     `n` / `kappa` override the grid size (the maximum depth for the adaptive config 5) and the
-    wavenumber, for scaled-down variants."""
+    wavenumber, for scaled-down variants; balance=False skips config 5's level restriction."""
     cfg = dict(CONFIGS[name])
     if n is not None:
         cfg["n"] = n
     if kappa is not None:
         cfg["kappa"] = kappa
     if cfg["contrast"] == "smoothed_disk":
-        pts, w = adaptive_grid(adaptive_leaves(cfg["kappa"], cfg["n"]))
+        pts, w = adaptive_grid(adaptive_leaves(cfg["kappa"], cfg["n"], balance=balance))
     else:
         pts, w = grid_points(cfg["n"])
     q = {"gaussian": gaussian_q, "disk": disk_q, "bumps": bumps_q,

@@ -256,3 +256,16 @@ def test_host_width_reading_lists_match_oracle(name, n, kappa, tmp_path):
     piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
     prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
     validate_pivots(NCA(prob, tree, lists, P["nca_tol"], pivots=piv), piv)
+
+
+@pytest.mark.parametrize("balance", [True, False])
+def test_host_level_restricted_flag_matches_oracle(balance):
+    """dafmm_stats.level_restricted against the oracle's brute-force check."""
+    from oracle.tree import level_restricted
+    P = make_problem("c5", n=5, kappa=12.0, balance=balance)
+    prod = _prod()
+    op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], host_only=1)
+    flag = op.stats()["level_restricted"]
+    op.close()
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+    assert flag == int(level_restricted(tree)) == int(balance)

@@ -24,7 +24,7 @@ def _import_pivots(path):
     ptr = np.load(path / "hodlr_piv_ptr.npy")
     I, J = np.load(path / "hodlr_I.npy"), np.load(path / "hodlr_J.npy")
     perm = np.load(path / "hodlr_perm.npy")
-    r, n0, n = np.load(path / "hodlr_meta.npy")
+    r, n0, n = np.load(path / "hodlr_meta.npy")[:3]
     piv = {}
     for k, (_, a, b, c, d) in enumerate(blocks):
         piv[(int(a), int(b), int(c), int(d))] = (I[ptr[k]:ptr[k + 1]], J[ptr[k]:ptr[k + 1]])
@@ -132,3 +132,28 @@ def test_gpu_hodlr_invalid_arguments():
     pc.close()
     op.close()
     op2.close()
+
+
+def test_gpu_hodlr_max_block_matches_oracle(tmp_path):
+    """HR5 (option): with max_block the sibling blocks of more rows are dropped; the product's
+    exported pivots are empty exactly there and the solve matches the oracle's HODLR."""
+    P = make_problem("c1")
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"])
+    pc = _prod().HODLR(op, rank=8, leaf_size=64, max_block=512)
+    assert pc.stats()["max_block"] == 512
+    pc.export(str(tmp_path))
+    piv, perm, r, n0, N, blocks = _import_pivots(tmp_path)
+    for (a, b, c, d), (I, J) in piv.items():
+        assert (len(I) == 0) if b - a > 512 else True
+    assert any(len(I) > 0 for I, _ in piv.values())
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    H = HODLR(prob, perm, n0, r, pivots=piv)
+    H.validate()
+    b = np.random.default_rng(3).standard_normal(N) + 0j
+    xd = torch.empty(N, dtype=torch.complex128, device="cuda")
+    pc.solve(_dev(b), xd)
+    torch.cuda.synchronize()
+    x_ref = H.solve(b)
+    assert np.linalg.norm(xd.cpu().numpy() - x_ref) / np.linalg.norm(x_ref) <= 1e-10
+    pc.close()
+    op.close()

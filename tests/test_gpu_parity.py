@@ -277,3 +277,31 @@ def test_gpu_device_aca_matches_host_aca(name, n, kappa, tmp_path):
     yd, yh = _gpu_matvec(op_d, x), _gpu_matvec(op_h, x)
     assert _rel(yd - x, nca_d.matvec(x) - x) <= 1e-11
     assert _rel(yd - x, yh - x) <= 10 * P["nca_tol"]
+
+
+@pytest.mark.parametrize("opts,name,n,kappa", [(dict(self_term=2), "c1", None, None),
+                                               (dict(w_reading=1), "c2", 128, 40.0)])
+def test_gpu_options_match_oracle(opts, name, n, kappa, tmp_path):
+    """The square-cell self term (R24, self_term = 2) and the width reading of w (R25,
+    w_reading = 1): GPU DAFMM against the oracle built with the same option, <= 1e-11, and
+    against the dense product <= 10 nca_tol."""
+    P = make_problem(name, n=n, kappa=kappa)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], **opts)
+    op.export_plan(tmp_path / "plan")
+    plan = load_plan(tmp_path / "plan")
+    st = "square" if opts.get("self_term") == 2 else "disk"
+    wr = "width" if opts.get("w_reading") == 1 else "circumradius"
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"], self_term=st)
+    tree = Tree(P["points"], P["weights"], P["kappa"], 64, w_reading=wr)
+    lists = Lists(tree)
+    compare_lists(plan, tree, lists)
+    piv = [dict()] + [plan["levels"][l]["pivots"] for l in range(1, tree.L + 1)]
+    nca = NCA(prob, tree, lists, P["nca_tol"], pivots=piv)
+    validate_pivots(nca, piv)
+    x = P["x"]
+    y = _gpu_matvec(op, x)
+    assert _rel(y - x, nca.matvec(x) - x) <= 1e-11
+    rows = np.arange(0, prob.n, 5)
+    yd = oracle.dense_matvec_rows(prob, x, rows)
+    assert _rel(y[rows] - x[rows], yd - x[rows]) <= 10 * P["nca_tol"]
+    op.close()

@@ -113,3 +113,19 @@ def test_right_preconditioner_cuts_gmres_iterations():
     psi = Pinv @ u
     assert conv0 and conv1 and it1 * 10 <= it0
     assert np.linalg.norm(A @ psi - f) / np.linalg.norm(f) <= 1.1e-6
+
+
+def test_max_block_drops_top_blocks():
+    """HR5: with max_block the blocks of more rows are zero in Ã (block diagonal at the top);
+    the rest is the ordinary HODLR."""
+    P, prob, perm = _case("c1", 32, 8.0)
+    H = HODLR(prob, perm, 64, 8, max_block=256)
+    Hd = H.dense()
+    n = perm.size
+    for _, a, b, c, d in sibling_blocks(n, 64):
+        if b - a > 256:
+            assert not np.any(Hd[a:b, c:d])
+    full = HODLR(prob, perm, 64, 8)
+    for key, (I, J) in H.pivots.items():
+        if key[1] - key[0] <= 256:
+            assert np.array_equal(I, full.pivots[key][0]) and np.array_equal(J, full.pivots[key][1])

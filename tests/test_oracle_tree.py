@@ -163,3 +163,17 @@ def test_width_reading_pair_counts_and_geometry():
         for key, nb in lists.N[l].items():
             for a in nb:
                 assert math.hypot(a[0] - key[0], a[1] - key[1]) * b < tree.kappa * b * b
+
+
+def test_level_restricted_config5_trees():
+    """the paper's adaptive tree is level restricted.  The config-5 generator balances
+    its refinement (synth.configs.level_restrict); without it the same refinement rules leave
+    leaves two or more levels apart across the contrast's transition layer."""
+    from oracle.tree import level_restricted
+    for n, kappa in [(5, 12.0), (6, 30.0)]:
+        P = make_problem("c5", n=n, kappa=kappa)
+        tree = Tree(P["points"], P["weights"], P["kappa"], 64)
+        assert level_restricted(tree)
+        P0 = make_problem("c5", n=n, kappa=kappa, balance=False)
+        tree0 = Tree(P0["points"], P0["weights"], P0["kappa"], 64)
+        assert not level_restricted(tree0)

@@ -2,7 +2,7 @@
 right preconditioner of rank r; prints setup times, iterations, true residual, solve time and
 the HODLR apply time (CUDA events).
 
-    python tools/hybrid_probe.py c3 '[[50, 0], [50, 8], [50, 16]]'     # [restart, rank] pairs (rank 0: none)
+    python tools/hybrid_probe.py c3 '[[50, 0], [50, 8], [50, 16, 65536]]'   # [restart, rank(, max_block)] (rank 0: none)
 """
 import json
 import os
@@ -27,11 +27,13 @@ print(json.dumps(dict(config=name, N=int(P["points"].shape[0]), setup_s=round(se
                       setup_breakdown={k: round(st[k], 3) for k in ("setup_tree_s", "setup_lists_s", "setup_nca_s",
                                                                     "setup_ops_s", "setup_upload_s")})), flush=True)
 f = torch.from_numpy(P["f"]).cuda()
-for restart, rank in cases:
+for case in cases:
+    restart, rank = case[0], case[1]
+    max_block = case[2] if len(case) > 2 else 0
     pc, pcs, apply_ms = None, None, None
     if rank > 0:
         t0 = time.perf_counter()
-        pc = prod.HODLR(op, rank=rank, leaf_size=64)
+        pc = prod.HODLR(op, rank=rank, leaf_size=64, max_block=max_block)
         torch.cuda.synchronize()
         pcs = dict(setup_s=round(time.perf_counter() - t0, 3), **pc.stats())
         b = torch.empty_like(f)
@@ -50,7 +52,7 @@ for restart, rank in cases:
     t0 = time.perf_counter()
     rc, it, rr = op.gmres(f, psi, P["gmres_tol"], maxit, restart, prec=pc)
     solve = time.perf_counter() - t0
-    print(json.dumps(dict(config=name, restart=restart, rank=rank, status=rc, iterations=it, true_relres=rr,
+    print(json.dumps(dict(config=name, restart=restart, rank=rank, max_block=max_block, status=rc, iterations=it, true_relres=rr,
                           solve_s=round(solve, 3), ms_per_iteration=round(1e3 * solve / max(it, 1), 3),
                           hodlr=pcs, hodlr_apply_ms=apply_ms)), flush=True)
     if pc is not None:
