@@ -111,9 +111,14 @@ def _hbm_peak():
 
 
 def m2l_stored_bytes(stats):
-    """Algorithmic DRAM bytes of one stored-M2L launch: every block entry once
-    (16 B), every source-stream index (4 B) and gathered multipole (16 B), every output (16 B)."""
-    return 16 * stats["m2l_entries"] + 20 * stats["m2l_stream_len"] + 16 * stats["n_loc"]
+    """Algorithmic DRAM bytes of one stored-M2L launch: every stored block entry
+    once (16 B), every source-stream index (4 B) and gathered multipole (16 B), every output
+    (16 B); pair-stored blocks (m2l_stored = 2, R22) add the column-sum slots, written once and
+    read once by the gather (2 x 16 B per stream position)."""
+    b = 16 * stats["m2l_stored_entries"] + 20 * stats["m2l_stream_len"] + 16 * stats["n_loc"]
+    if stats.get("m2l_stored") == 2:
+        b += 32 * stats["m2l_stream_len"]
+    return b
 
 
 def roofline_entry(pass_ms, matvecs, stats, inputs, ms_per_step=None):
@@ -148,7 +153,8 @@ def roofline_entry(pass_ms, matvecs, stats, inputs, ms_per_step=None):
         hpk, hpk_src = _hbm_peak()
         nbytes = m2l_stored_bytes(stats)
         achieved = nbytes / (ms_m2l * 1e-3) / 1e9 if ms_m2l > 0 else None
-        ki = kin.get("m2l_stored", {})
+        pair = stats.get("m2l_stored") == 2
+        ki = kin.get("m2l_pair" if pair else "m2l_stored", {})
         # the step's bound: fp64 work (P2P + the stored M2L's complex MACs, 8 flops per entry)
         # against fp64 peak, DRAM bytes (stored blocks, translation operators, ~10 vector passes)
         # against HBM peak; the two resources overlap
@@ -171,7 +177,9 @@ def roofline_entry(pass_ms, matvecs, stats, inputs, ms_per_step=None):
             step["entries_view"] = {"t_roof_ms": t_roof, "m2l_fp64_flops_per_entry": fpe_fly,
                                     "p2p_fp64_flops_per_entry": fpe_p2p,
                                     "frac": (t_roof / ms_per_step) if ms_per_step else None}
-        return {"kernel": "m2l_stored_kernel (M2L blocks streamed from HBM by TMA; concurrent with p2p_kernel)",
+        kname = ("m2l_pair_kernel (one M2L block per node pair streamed by TMA, row and column sums; R22)"
+                 if pair else "m2l_stored_kernel (M2L blocks streamed from HBM by TMA; concurrent with p2p_kernel)")
+        return {"kernel": kname,
                 "bound": "hbm", "achieved": achieved, "peak": hpk, "unit": "GB/s",
                 "frac": (achieved / hpk) if achieved else None, "traffic": ki.get("dram_bytes_per_launch"),
                 "algorithmic_bytes_per_launch": nbytes, "launch_ms_concurrent": ms_m2l,

@@ -9,13 +9,16 @@ Readings (HR1-HR4):
   HR1  binary tree over the DAFMM tree order (Morton order of the quadtree): node
        [a, b) has children [a, m), [m, b) with m = (a + b) // 2; nodes with at most n0 points are
        leaves (dense diagonal blocks A[leaf, leaf]).
-  HR2  every off-diagonal sibling block A[alpha, beta] is a cross (skeleton) approximation
-       A[alpha, J] A[I, J]^{-1} A[I, beta] whose pivots I, J come from partially pivoted ACA with
-       the rank capped at r ("apriori fixing the rank"): first row = the first row of
-       alpha with the largest |q| (a row with q = 0 is zero in A's off-diagonal blocks); column =
-       first argmax of the residual row over unused columns; next row = first argmax of the
-       residual column over unused rows; the approximation ends at rank r or when the pivot's
-       residual is at rounding level (<= 1e3 eps of the largest entry of its row / column).
+  HR2  every off-diagonal sibling block A[alpha, beta] is replaced by its rank-k ACA approximant
+       sum_l u_l v_l^T (partially pivoted ACA with the rank capped at r, "apriori fixing the
+       rank"): first row = the first row of alpha with the largest |q| (a row with q = 0
+       is zero in A's off-diagonal blocks); column = first argmax of the residual row over unused
+       columns; next row = first argmax of the residual column over unused rows; it ends at rank
+       r or when the pivot's residual is at rounding level (<= 1e3 eps of the largest entry of
+       its row / column).  In exact arithmetic the approximant is the cross approximation
+       A[alpha, J] A[I, J]^{-1} A[I, beta] of the pivots I, J; the factors u_l, v_l are used
+       instead because a fixed-rank ACA that runs past the block's numerical rank leaves A[I, J]
+       with condition numbers up to 1e15 (measured), where the explicit inverse loses all digits.
   HR3  Ã^{-1} by the recursive Sherman-Morrison-Woodbury factorisation of the HODLR solver the
        paper cites -- exact for Ã up to rounding, so the oracle uses a dense solve.
   HR4  right preconditioning A Ã^{-1} u = f, psi = Ã^{-1} u (the paper writes left preconditioning,
@@ -118,16 +121,44 @@ class HODLR:
                 pivots[(a, b, c, d)] = (a + np.asarray(I, np.int64), c + np.asarray(J, np.int64))
         self.pivots = pivots
 
+    def factors(self, a, b, c, d):
+        """HR2: the ACA factors (u_l, v_l) of block rows [a, b) x columns [c, d) for its pivots, in
+        the order the ACA chose them: v_l = residual row I_l / its entry at J_l, u_l = residual
+        column J_l (the ACA recursion with the pivots given)."""
+        I, J = self.pivots[(a, b, c, d)]
+        perm, prob = self.perm, self.prob
+        us, vs = [], []
+        for i, j in zip(I, J):
+            row = A_block(prob, perm[i:i + 1], perm[c:d])[0]
+            col = A_block(prob, perm[a:b], perm[j:j + 1])[:, 0]
+            for u, v in zip(us, vs):
+                row = row - u[i - a] * v
+                col = col - v[j - c] * u
+            us.append(col)
+            vs.append(row / row[j - c])
+        return us, vs
+
     def validate(self):
-        """Imported pivots: inside their block, distinct, at most r, non-singular cross matrix."""
+        """Imported pivots: inside their block, distinct, at most r, in an order whose residual
+        pivots are nonzero (HR2's rounding-level rule)."""
         for _, a, b, c, d in self.blocks:
             I, J = self.pivots[(a, b, c, d)]
             assert len(I) == len(J) <= self.r
             assert np.all((I >= a) & (I < b)) and np.all((J >= c) & (J < d))
             assert len(np.unique(I)) == len(I) and len(np.unique(J)) == len(J)
-            if len(I):
-                M = A_block(self.prob, self.perm[I], self.perm[J])
-                assert np.linalg.matrix_rank(M) == len(I), "singular HODLR cross matrix"
+            perm, prob = self.perm, self.prob
+            us, vs = [], []
+            for i, j in zip(I, J):
+                row0 = A_block(prob, perm[i:i + 1], perm[c:d])[0]
+                row = row0.copy()
+                for u, v in zip(us, vs):
+                    row = row - u[i - a] * v
+                assert abs(row[j - c]) > ZERO_RTOL * np.abs(row0).max(), "HODLR pivot at rounding level"
+                col = A_block(prob, perm[a:b], perm[j:j + 1])[:, 0]
+                for u, v in zip(us, vs):
+                    col = col - v[j - c] * u
+                us.append(col)
+                vs.append(row / row[j - c])
 
     def dense(self):
         """Ã assembled densely in tree order: leaf diagonal blocks of A, skeletons elsewhere."""
@@ -137,11 +168,9 @@ class HODLR:
             if b - a <= self.n0:
                 H[a:b, a:b] = A_block(prob, perm[a:b], perm[a:b])
         for _, a, b, c, d in self.blocks:
-            I, J = self.pivots[(a, b, c, d)]
-            if len(I):
-                C = A_block(prob, perm[a:b], perm[J])
-                R = A_block(prob, perm[I], perm[c:d])
-                H[a:b, c:d] = C @ np.linalg.solve(A_block(prob, perm[I], perm[J]), R)
+            us, vs = self.factors(a, b, c, d)
+            for u, v in zip(us, vs):
+                H[a:b, c:d] += np.outer(u, v)
         return H
 
     def solve(self, b_caller):

@@ -2,9 +2,12 @@
 //
 // Ã approximates A = I + kappa^2 diag(q) K in the DAFMM tree order (HR1: binary tree of
 // midpoint splits over the tree positions, leaves of at most n0 points).  Every off-diagonal
-// sibling block A[gamma, sib(gamma)] is the cross approximation U_gamma V_gamma^H with
-// U_gamma = A[gamma, J] A[I, J]^{-1} and V_gamma^H = A[I, sib(gamma)], its pivots I, J from the
-// fixed-rank ACA (HR2; device ACA of setup_device.cu, mode 1).  Factorisation (HR3, the
+// sibling block A[gamma, sib(gamma)] is its rank-k ACA approximant U_gamma V_gamma^H = sum_l u_l
+// v_l^T from the fixed-rank ACA (HR2; device ACA of setup_device.cu, mode 1, which writes the
+// balanced factors straight into the planes below) -- in exact arithmetic the cross
+// approximation A[gamma, J] A[I, J]^{-1} A[I, sib(gamma)] of its pivots, but without the
+// inverse of the cross matrix, whose condition number reaches 1e15 once a fixed-rank ACA runs
+// past the block's numerical rank.  Factorisation (HR3, the
 // recursive Sherman-Morrison-Woodbury form of the HODLR direct solver the paper cites):
 //
 //   Ã_nu = diag(Ã_alpha, Ã_beta) (I + W Z^H),  W = diag(W_alpha, W_beta),  W_gamma = Ã_gamma^{-1} U_gamma,
@@ -90,7 +93,25 @@ struct XA {
   }
 };
 
-// ---- leaves: dense A[leaf, leaf] and its LU ----
+// Inverse of the n x n matrix whose LU (P M = L U, column-major, in shared memory) is M, one
+// column per thread: column c solves L U x = P e_c; written column-major to out.  (The leaf blocks
+// and the Woodbury factors are applied as dense inverses: a GEMV per apply instead of a latency
+// chain of 2n dependent substitution steps.)
+__device__ void lu_inverse(const double2* M, const int* perm, int n, double2* __restrict__ out) {
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double2 x[kMaxLeaf];
+    for (int i = 0; i < n; ++i) x[i] = make_double2(perm[i] == c ? 1.0 : 0.0, 0.0);
+    for (int i = 1; i < n; ++i)
+      for (int j = 0; j < i; ++j) cfms2(x[i], M[j * n + i], x[j]);
+    for (int i = n - 1; i >= 0; --i) {
+      for (int j = i + 1; j < n; ++j) cfms2(x[i], M[j * n + i], x[j]);
+      x[i] = cdiv2(x[i], M[i * n + i]);
+    }
+    for (int i = 0; i < n; ++i) out[(int64_t)c * n + i] = x[i];
+  }
+}
+
+// ---- leaves: dense A[leaf, leaf], its LU and inverse ----
 __global__ void hodlr_leaf_lu_kernel(const int64_t* __restrict__ la, const int32_t* __restrict__ ln,
                                      const int64_t* __restrict__ lu_off, AEntries A, double2* __restrict__ lu,
                                      int32_t* __restrict__ prow, int* status) {
@@ -105,138 +126,57 @@ __global__ void hodlr_leaf_lu_kernel(const int64_t* __restrict__ la, const int32
   for (int e = threadIdx.x; e < n * n; e += blockDim.x) M[e] = A(a + e % n, a + e / n, T);
   __syncthreads();
   block_lu(M, n, s_perm, &s_piv, status);
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) lu[lu_off[leaf] + e] = M[e];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) prow[(int64_t)leaf * kMaxLeaf + i] = s_perm[i];
+  lu_inverse(M, s_perm, n, lu + lu_off[leaf]);  // the leaf's A^{-1}, column-major
+  (void)prow;
 }
 
-// X[leaf rows, xc0 .. xc0 + nc) <- A_leaf^{-1} X (factorisation: many columns, one per thread)
+// X[leaf rows, 0 .. nc) <- A_leaf^{-1} X (factorisation: many columns, one per thread)
 __global__ void hodlr_leaf_solve_multi_kernel(const int64_t* __restrict__ la, const int32_t* __restrict__ ln,
-                                              const int64_t* __restrict__ lu_off, const double2* __restrict__ lu,
-                                              const int32_t* __restrict__ prow, XA X, int nc) {
+                                              const int64_t* __restrict__ lu_off, const double2* __restrict__ inv,
+                                              XA X, int nc) {
   extern __shared__ double2 M[];
   const int leaf = blockIdx.x;
   const int64_t a = la[leaf];
   const int n = ln[leaf];
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) M[e] = lu[lu_off[leaf] + e];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) M[e] = inv[lu_off[leaf] + e];
   __syncthreads();
-  const int32_t* pr = prow + (int64_t)leaf * kMaxLeaf;
   for (int c = threadIdx.x; c < nc; c += blockDim.x) {
     double2 v[kMaxLeaf];
-    for (int i = 0; i < n; ++i) v[i] = X.at(a + pr[i], c);
-    for (int i = 1; i < n; ++i)
-      for (int j = 0; j < i; ++j) cfms2(v[i], M[j * n + i], v[j]);
-    for (int i = n - 1; i >= 0; --i) {
-      for (int j = i + 1; j < n; ++j) cfms2(v[i], M[j * n + i], v[j]);
-      v[i] = cdiv2(v[i], M[i * n + i]);
+    for (int i = 0; i < n; ++i) v[i] = X.at(a + i, c);
+    for (int i = 0; i < n; ++i) {
+      double2 acc = make_double2(0.0, 0.0);
+      for (int j = 0; j < n; ++j) cfma2(acc, M[j * n + i], v[j]);
+      X.at(a + i, c) = acc;
     }
-    for (int i = 0; i < n; ++i) X.at(a + i, c) = v[i];
   }
 }
 
-// Column-oriented triangular solves of one vector by one warp: rows lane and lane + 32 in
-// registers; M column-major n x n (n <= 64), v = P b already loaded.
-__device__ __forceinline__ void warp_lu_solve(const double2* __restrict__ M, int n, double2& v0, double2& v1) {
-  const int lane = threadIdx.x & 31;
-  const int i0 = lane, i1 = lane + 32;
-  for (int j = 0; j < n - 1; ++j) {  // L (unit diagonal)
-    const double2 src = j < 32 ? v0 : v1;
-    const double2 xj = make_double2(__shfl_sync(0xffffffffu, src.x, j & 31), __shfl_sync(0xffffffffu, src.y, j & 31));
-    if (i0 > j && i0 < n) cfms2(v0, M[j * n + i0], xj);
-    if (i1 > j && i1 < n) cfms2(v1, M[j * n + i1], xj);
-  }
-  for (int j = n - 1; j >= 0; --j) {  // U
-    if (j < 32) {
-      if (lane == j) v0 = cdiv2(v0, M[j * n + j]);
-    } else if (lane == j - 32) {
-      v1 = cdiv2(v1, M[j * n + j]);
-    }
-    const double2 src = j < 32 ? v0 : v1;
-    const double2 xj = make_double2(__shfl_sync(0xffffffffu, src.x, j & 31), __shfl_sync(0xffffffffu, src.y, j & 31));
-    if (i0 < j) cfms2(v0, M[j * n + i0], xj);
-    if (i1 < j) cfms2(v1, M[j * n + i1], xj);
-  }
-}
-
-// apply: x[leaf] <- A_leaf^{-1} x[leaf], one warp per leaf (LU read from HBM, coalesced columns)
-__global__ void hodlr_leaf_solve_vec_kernel(int nleaves, const int64_t* __restrict__ la,
-                                            const int32_t* __restrict__ ln, const int64_t* __restrict__ lu_off,
-                                            const double2* __restrict__ lu, const int32_t* __restrict__ prow,
-                                            double2* __restrict__ x) {
+// apply: x[leaf] <- A_leaf^{-1} x[leaf], one warp per leaf: lanes own rows lane, lane + 32; the
+// inverse's columns are read coalesced and independent of each other (loads pipeline)
+__global__ void __launch_bounds__(128) hodlr_leaf_solve_vec_kernel(int nleaves, const int64_t* __restrict__ la,
+                                                                   const int32_t* __restrict__ ln,
+                                                                   const int64_t* __restrict__ lu_off,
+                                                                   const double2* __restrict__ inv,
+                                                                   double2* __restrict__ x) {
   const int leaf = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (leaf >= nleaves) return;
   const int lane = threadIdx.x & 31;
   const int64_t a = la[leaf];
   const int n = ln[leaf];
-  const int32_t* pr = prow + (int64_t)leaf * kMaxLeaf;
+  const double2* M = inv + lu_off[leaf];
   double2 v0 = make_double2(0.0, 0.0), v1 = v0;
-  if (lane < n) v0 = x[a + pr[lane]];
-  if (lane + 32 < n) v1 = x[a + pr[lane + 32]];
-  warp_lu_solve(lu + lu_off[leaf], n, v0, v1);
-  __syncwarp();
-  if (lane < n) x[a + lane] = v0;
-  if (lane + 32 < n) x[a + lane + 32] = v1;
-}
-
-// ---- bases of the blocks of one depth: U_gamma rows (tiles of gamma's rows) ----
-// child g: rows [ca[g], cb[g]), rank ck[g], pivots I = blk_I[po[g] ..], J = blk_J[po[g] ..]
-__global__ void hodlr_basis_u_kernel(const int32_t* __restrict__ tiles, const int64_t* __restrict__ ca,
-                                     const int64_t* __restrict__ cb, const int32_t* __restrict__ ck,
-                                     const int32_t* __restrict__ po, const int32_t* __restrict__ bI,
-                                     const int32_t* __restrict__ bJ, AEntries A, double2* __restrict__ Up, int r,
-                                     int* status) {
-  __shared__ PolyTable T;
-  __shared__ double2 C[kMaxRank * kMaxRank];
-  __shared__ int s_perm[kMaxRank];
-  __shared__ int s_piv;
-  extern __shared__ double2 rhs[];  // blockDim x k
-  load_poly_table(T);
-  const int g = tiles[2 * blockIdx.x], t0 = tiles[2 * blockIdx.x + 1];
-  const int64_t rb = cb[g];
-  const int k = ck[g];
-  const int32_t* I = bI + po[g];
-  const int32_t* J = bJ + po[g];
-  const int64_t t = ca[g] + t0 + threadIdx.x;
-  if (k == 0) {
-    if (t < rb)
-      for (int c = 0; c < r; ++c) Up[t * r + c] = make_double2(0.0, 0.0);
-    return;
+  if (lane < n) v0 = x[a + lane];
+  if (lane + 32 < n) v1 = x[a + lane + 32];
+  double2 y0 = make_double2(0.0, 0.0), y1 = y0;
+#pragma unroll 4
+  for (int j = 0; j < n; ++j) {
+    const double2 src = j < 32 ? v0 : v1;
+    const double2 xj = make_double2(__shfl_sync(0xffffffffu, src.x, j & 31), __shfl_sync(0xffffffffu, src.y, j & 31));
+    if (lane < n) cfma2(y0, M[j * n + lane], xj);
+    if (lane + 32 < n) cfma2(y1, M[j * n + lane + 32], xj);
   }
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) C[e] = A(I[e % k], J[e / k], T);
-  __syncthreads();
-  block_lu(C, k, s_perm, &s_piv, status);  // P C = L U
-  if (t >= rb) return;
-  double2* a = rhs + (int64_t)threadIdx.x * k;
-  for (int j = 0; j < k; ++j) a[j] = A(t, J[j], T);
-  // x C = a with C = P^T L U:  w U = a, then y L = w, then x_{perm[i]} = y_i
-  for (int j = 0; j < k; ++j) {
-    double2 s = a[j];
-    for (int i = 0; i < j; ++i) cfms2(s, a[i], C[j * k + i]);
-    a[j] = cdiv2(s, C[j * k + j]);
-  }
-  for (int j = k - 2; j >= 0; --j) {
-    double2 s = a[j];
-    for (int i = j + 1; i < k; ++i) cfms2(s, a[i], C[j * k + i]);
-    a[j] = s;
-  }
-  double2* out = Up + t * r;
-  for (int c = k; c < r; ++c) out[c] = make_double2(0.0, 0.0);
-  for (int i = 0; i < k; ++i) out[s_perm[i]] = a[i];
-}
-
-// Vcat rows of the columns of block g: t in sib(g) = [sa[g], sb[g]): Vp[t r + i] = A[I_i, t]
-__global__ void hodlr_basis_v_kernel(const int32_t* __restrict__ tiles, const int64_t* __restrict__ sa,
-                                     const int64_t* __restrict__ sb, const int32_t* __restrict__ ck,
-                                     const int32_t* __restrict__ po, const int32_t* __restrict__ bI, AEntries A,
-                                     double2* __restrict__ Vp, int r) {
-  __shared__ PolyTable T;
-  load_poly_table(T);
-  const int g = tiles[2 * blockIdx.x], t0 = tiles[2 * blockIdx.x + 1];
-  const int64_t t = sa[g] + t0 + threadIdx.x;
-  if (t >= sb[g]) return;
-  const int k = ck[g];
-  const int32_t* I = bI + po[g];
-  double2* out = Vp + t * r;
-  for (int i = 0; i < r; ++i) out[i] = i < k ? A(I[i], t, T) : make_double2(0.0, 0.0);
+  if (lane < n) x[a + lane] = y0;
+  if (lane + 32 < n) x[a + lane + 32] = y1;
 }
 
 // ---- per depth: Y partials over parts (part = child id, t0, t1) ----
@@ -309,6 +249,7 @@ __global__ void __launch_bounds__(256) hodlr_update_vec_kernel(const int32_t* __
 __device__ __forceinline__ double2 child_sum(const double2* __restrict__ partial, const int32_t* __restrict__ pptr,
                                              int child, int r, int nc, int i, int c) {
   double2 s = make_double2(0.0, 0.0);
+#pragma unroll 4
   for (int p = pptr[child]; p < pptr[child + 1]; ++p) {
     const double2 v = partial[((int64_t)p * r + i) * nc + c];
     s.x += v.x;
@@ -321,7 +262,7 @@ __device__ __forceinline__ double2 child_sum(const double2* __restrict__ partial
 // factor (gcol >= 0): S = [[I, G_beta], [G_alpha, I]] from partial columns gcol .. gcol + r, LU to
 // S_lu / S_prow.  Then (ncs > 0) C[nu][i][c] = (S^{-1} [Y_beta; Y_alpha])_i for columns c < ncs.
 __global__ void hodlr_node_kernel(const int32_t* __restrict__ pptr, const double2* __restrict__ partial, int r,
-                                  int nc, int gcol, int ncs, double2* __restrict__ S_lu,
+                                  int nc, int gcol, int ncs, double2* __restrict__ S_lu, double2* __restrict__ S_inv,
                                   int32_t* __restrict__ S_prow, double2* __restrict__ C, int* status) {
   extern __shared__ double2 S[];  // (2r)^2, column-major (factor and multi-column solves)
   __shared__ int s_perm[2 * kMaxRank];
@@ -329,19 +270,25 @@ __global__ void hodlr_node_kernel(const int32_t* __restrict__ pptr, const double
   const int nu = blockIdx.x, R2 = 2 * r;
   const int ca = 2 * nu, cb = 2 * nu + 1;
   double2* lu = S_lu + (int64_t)nu * R2 * R2;
-  if (gcol < 0 && ncs == 1) {  // apply: one warp, column-oriented substitution on the stored LU
+  if (gcol < 0 && ncs == 1) {  // apply: one warp, C = S^{-1} [Y_beta; Y_alpha] as a GEMV
     const int lane = threadIdx.x;
     if (lane >= 32) return;
-    const int32_t* pr = S_prow + (int64_t)nu * R2;
-    auto rhs = [&](int q) {  // [Y_beta; Y_alpha]
+    const double2* Si = S_inv + (int64_t)nu * R2 * R2;
+    auto rhs = [&](int q) {  // the child's parts summed in part order
       return q < r ? child_sum(partial, pptr, cb, r, nc, q, 0) : child_sum(partial, pptr, ca, r, nc, q - r, 0);
     };
-    double2 v0 = make_double2(0.0, 0.0), v1 = v0;
-    if (lane < R2) v0 = rhs(pr[lane]);
-    if (lane + 32 < R2) v1 = rhs(pr[lane + 32]);
-    warp_lu_solve(lu, R2, v0, v1);
-    if (lane < R2) C[(int64_t)nu * R2 + lane] = v0;
-    if (lane + 32 < R2) C[(int64_t)nu * R2 + lane + 32] = v1;
+    const double2 b0 = lane < R2 ? rhs(lane) : make_double2(0.0, 0.0);
+    const double2 b1 = lane + 32 < R2 ? rhs(lane + 32) : make_double2(0.0, 0.0);
+    double2 y0 = make_double2(0.0, 0.0), y1 = y0;
+#pragma unroll 4
+    for (int q = 0; q < R2; ++q) {
+      const double2 src = q < 32 ? b0 : b1;
+      const double2 bq = make_double2(__shfl_sync(0xffffffffu, src.x, q & 31), __shfl_sync(0xffffffffu, src.y, q & 31));
+      if (lane < R2) cfma2(y0, Si[q * R2 + lane], bq);
+      if (lane + 32 < R2) cfma2(y1, Si[q * R2 + lane + 32], bq);
+    }
+    if (lane < R2) C[(int64_t)nu * R2 + lane] = y0;
+    if (lane + 32 < R2) C[(int64_t)nu * R2 + lane + 32] = y1;
     return;
   }
   if (gcol >= 0) {
@@ -355,6 +302,7 @@ __global__ void hodlr_node_kernel(const int32_t* __restrict__ pptr, const double
     __syncthreads();
     block_lu(S, R2, s_perm, &s_piv, status);
     for (int e = threadIdx.x; e < R2 * R2; e += blockDim.x) lu[e] = S[e];
+    lu_inverse(S, s_perm, R2, S_inv + (int64_t)nu * R2 * R2);  // for the apply
     for (int i = threadIdx.x; i < R2; i += blockDim.x) S_prow[(int64_t)nu * R2 + i] = s_perm[i];
   } else {
     for (int e = threadIdx.x; e < R2 * R2; e += blockDim.x) S[e] = lu[e];
@@ -448,11 +396,11 @@ int factor_round(HodlrPlan& h, int d, int xc0, int nc, bool gcols, cudaStream_t 
   hodlr_segdot_kernel<<<grid, threads, 0, s>>>(h.part_d[d], Vp, r, X, xc0, nc, h.partial);
   const size_t smem = (size_t)4 * r * r * sizeof(double2);
   if (gcols) {  // the G columns (depth d's own U): S_nu = I + Z^H W, factored
-    hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, 0, 0, h.S_lu[d], h.S_prow[d], h.C,
-                                            h.status);
+    hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, 0, 0, h.S_lu[d], h.S_inv[d],
+                                            h.S_prow[d], h.C, h.status);
   } else {
-    hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, -1, nc, h.S_lu[d], h.S_prow[d], h.C,
-                                            h.status);
+    hodlr_node_kernel<<<nn, 128, smem, s>>>(h.part_ptr_d[d], h.partial, r, nc, -1, nc, h.S_lu[d], h.S_inv[d],
+                                            h.S_prow[d], h.C, h.status);
     hodlr_update_kernel<<<grid_for(h.n * nc, 256), 256, 0, s>>>(nn, h.split_d[d], Up, r, h.C, nc, X, xc0, h.n);
   }
   return ck(cudaGetLastError(), err, "hodlr factor round") ? DAFMM_OK : DAFMM_ECUDA;
@@ -466,8 +414,8 @@ int apply_round(HodlrPlan& h, int d, cudaStream_t s, std::string& err) {
   while (rp < r) rp <<= 1;
   const int64_t plane = h.n * (int64_t)r;
   hodlr_segdot_vec_kernel<<<h.nparts[d], 256, 0, s>>>(h.part_d[d], h.Vcat + d * plane, r, rp, h.xt, h.partial);
-  hodlr_node_kernel<<<nn, 32, 0, s>>>(h.part_ptr_d[d], h.partial, r, 1, -1, 1, h.S_lu[d], h.S_prow[d], h.C,
-                                      h.status);
+  hodlr_node_kernel<<<nn, 32, 0, s>>>(h.part_ptr_d[d], h.partial, r, 1, -1, 1, h.S_lu[d], h.S_inv[d], h.S_prow[d],
+                                      h.C, h.status);
   hodlr_update_vec_kernel<<<h.nparts[d], 256, 0, s>>>(h.part_d[d], h.Ucat + d * plane, r, rp, h.C, h.xt);
   return ck(cudaGetLastError(), err, "hodlr apply round") ? DAFMM_OK : DAFMM_ECUDA;
 }
@@ -554,6 +502,19 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
   }
   const int nleaves = (int)h.leaf_a.size();
   AEntries A{d.pts_t, d.w_t, d.qk2_t, d.D_t};
+  // ---- device buffers ----
+  if (!halloc(h, &h.Ucat, (size_t)n * h.ld, err) || !halloc(h, &h.Vcat, (size_t)n * h.ld, err) ||
+      !halloc(h, &h.xt, (size_t)n, err) || !halloc(h, &h.status, 1, err))
+    return DAFMM_ECUDA;
+  if (!ck(cudaMemsetAsync(h.status, 0, sizeof(int), s), err, "memset") ||
+      !ck(cudaMemsetAsync(h.Ucat, 0, sizeof(double2) * (size_t)n * h.ld, s), err, "memset") ||
+      !ck(cudaMemsetAsync(h.Vcat, 0, sizeof(double2) * (size_t)n * h.ld, s), err, "memset") ||
+      !ck(cudaFuncSetAttribute(hodlr_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(4 * kMaxRank * kMaxRank * sizeof(double2))),
+          err, "smem attr") ||
+      // the ACA runs on its own stream and writes into the zeroed planes
+      !ck(cudaStreamSynchronize(s), err, "memset (HODLR)"))
+    return DAFMM_ECUDA;
   // ---- HR2: pivots of every sibling block by the device ACA (mode 1), depth by depth ----
   double t0 = now_s();
   {
@@ -591,6 +552,11 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
           pr.first_row = (int32_t)(best - ra);
           pr.cap = rank;
           pr.mode = 1;
+          // HR2: the block's ACA factors go straight into the depth's planes: U_gamma rows at the
+          // rows' tree positions, V columns at the sibling's
+          pr.u_out = h.Ucat + (int64_t)dd * n * rank;
+          pr.v_out = h.Vcat + (int64_t)dd * n * rank;
+          pr.ldo = rank;
           prob_of[2 * i + side] = (int)probs.size();
           probs.push_back(pr);
         }
@@ -617,17 +583,6 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
   }
   double t1 = now_s();
   h.t_aca = t1 - t0;
-  // ---- device buffers ----
-  if (!halloc(h, &h.Ucat, (size_t)n * h.ld, err) || !halloc(h, &h.Vcat, (size_t)n * h.ld, err) ||
-      !halloc(h, &h.xt, (size_t)n, err) || !halloc(h, &h.status, 1, err))
-    return DAFMM_ECUDA;
-  if (!ck(cudaMemsetAsync(h.status, 0, sizeof(int), s), err, "memset") ||
-      !ck(cudaMemsetAsync(h.Ucat, 0, sizeof(double2) * (size_t)n * h.ld, s), err, "memset") ||
-      !ck(cudaMemsetAsync(h.Vcat, 0, sizeof(double2) * (size_t)n * h.ld, s), err, "memset") ||
-      !ck(cudaFuncSetAttribute(hodlr_node_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(4 * kMaxRank * kMaxRank * sizeof(double2))),
-          err, "smem attr"))
-    return DAFMM_ECUDA;
   // parts per depth: children cut into runs of at most `pl` rows
   const int64_t pl = std::max<int64_t>(256, n / 1024);
   int64_t max_parts = 1;
@@ -637,6 +592,7 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
   h.nparts.resize(h.depths);
   h.split_d.resize(h.depths);
   h.S_lu.resize(h.depths);
+  h.S_inv.resize(h.depths);
   h.S_prow.resize(h.depths);
   int64_t max_nodes = 1;
   for (int dd = 0; dd < h.depths; ++dd) {
@@ -663,6 +619,7 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
     max_nodes = std::max<int64_t>(max_nodes, (int64_t)nn);
     if (!hupload(h, &h.part_d[dd], parts, err) || !hupload(h, &h.part_ptr_d[dd], pp, err) ||
         !hupload(h, &h.split_d[dd], amb, err) || !halloc(h, &h.S_lu[dd], nn * 4 * rank * rank, err) ||
+        !halloc(h, &h.S_inv[dd], nn * 4 * rank * rank, err) ||
         !halloc(h, &h.S_prow[dd], nn * 2 * rank, err))
       return DAFMM_ECUDA;
   }
@@ -670,49 +627,6 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
   h.partial_len = max_parts * rank * maxcols;
   h.C_len = max_nodes * 2 * rank * maxcols;
   if (!halloc(h, &h.partial, (size_t)h.partial_len, err) || !halloc(h, &h.C, (size_t)h.C_len, err)) return DAFMM_ECUDA;
-  // ---- bases: U (rows of each block) and V (its columns), depth by depth ----
-  for (int dd = 0; dd < h.depths; ++dd) {
-    const size_t nn = h.split_a[dd].size();
-    std::vector<int64_t> ca(2 * nn), cb(2 * nn), sa(2 * nn), sb(2 * nn);
-    std::vector<int32_t> ckv(2 * nn), po(2 * nn), tu, tv;
-    for (size_t i = 0; i < nn; ++i) {
-      const int64_t a = h.split_a[dd][i], m = h.split_m[dd][i], b = h.split_b[dd][i];
-      for (int side = 0; side < 2; ++side) {
-        const size_t g = 2 * i + side;
-        ca[g] = side ? m : a;
-        cb[g] = side ? b : m;
-        sa[g] = side ? a : m;
-        sb[g] = side ? m : b;
-        po[g] = h.blk_ptr[dd][g];
-        ckv[g] = h.blk_ptr[dd][g + 1] - h.blk_ptr[dd][g];
-        for (int64_t t = 0; t < cb[g] - ca[g]; t += 128) tu.insert(tu.end(), {(int32_t)g, (int32_t)t});
-        for (int64_t t = 0; t < sb[g] - sa[g]; t += 128) tv.insert(tv.end(), {(int32_t)g, (int32_t)t});
-      }
-    }
-    HodlrPlan tmp;  // scratch uploads of this depth (freed below)
-    int64_t *d_ca, *d_cb, *d_sa, *d_sb;
-    int32_t *d_ck, *d_po, *d_I, *d_J, *d_tu, *d_tv;
-    bool ok = hupload(tmp, &d_ca, ca, err) && hupload(tmp, &d_cb, cb, err) && hupload(tmp, &d_sa, sa, err) &&
-              hupload(tmp, &d_sb, sb, err) && hupload(tmp, &d_ck, ckv, err) && hupload(tmp, &d_po, po, err) &&
-              hupload(tmp, &d_I, h.blk_I[dd], err) && hupload(tmp, &d_J, h.blk_J[dd], err) &&
-              hupload(tmp, &d_tu, tu, err) && hupload(tmp, &d_tv, tv, err);
-    if (ok) {
-      const int max_k = std::max(1, *std::max_element(ckv.begin(), ckv.end()));
-      const size_t smem = (size_t)128 * max_k * sizeof(double2);
-      ok = ck(cudaFuncSetAttribute(hodlr_basis_u_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem), err,
-              "smem attr");
-      if (ok) {
-        const int64_t plane = n * (int64_t)rank;
-        hodlr_basis_u_kernel<<<(int)(tu.size() / 2), 128, smem, s>>>(d_tu, d_ca, d_cb, d_ck, d_po, d_I, d_J, A,
-                                                                     h.Ucat + dd * plane, rank, h.status);
-        hodlr_basis_v_kernel<<<(int)(tv.size() / 2), 128, 0, s>>>(d_tv, d_sa, d_sb, d_ck, d_po, d_I, A,
-                                                                  h.Vcat + dd * plane, rank);
-        ok = ck(cudaGetLastError(), err, "hodlr basis") && ck(cudaStreamSynchronize(s), err, "hodlr basis");
-      }
-    }
-    hodlr_free(tmp);
-    if (!ok) return DAFMM_ECUDA;
-  }
   // ---- leaves: LU of A[leaf, leaf] ----
   std::vector<int64_t> lu_off(nleaves);
   int64_t lu_len = 0;
@@ -741,8 +655,7 @@ int hodlr_create(const Plan& P, const DevPlan& d, int rank, int leaf_size, int64
   // (deepest split first): factor S from block d (the G columns), apply (I + W Z^H)^{-1} of the
   // depth to the U columns of the coarser depths, chunk by chunk ----
   hodlr_leaf_solve_multi_kernel<<<nleaves, 64, leaf_smem, s>>>(h.leaf_a_d, h.leaf_n_d, h.leaf_lu_off, h.leaf_lu,
-                                                              h.leaf_prow, XA{h.Ucat, n * (int64_t)rank, rank, rank},
-                                                              h.ld);
+                                                              XA{h.Ucat, n * (int64_t)rank, rank, rank}, h.ld);
   if (!ck(cudaGetLastError(), err, "hodlr leaf solve")) return DAFMM_ECUDA;
   for (int dd = h.depths - 1; dd >= 0; --dd) {
     int rc = factor_round(h, dd, dd * rank, rank, true, s, err);
@@ -767,7 +680,7 @@ int hodlr_apply(HodlrPlan& h, const double2* in, double2* out, cudaStream_t s, s
   hodlr_gather_kernel<<<g, 256, 0, s>>>(n, h.perm, in, h.xt);
   const int nleaves = (int)h.leaf_a.size();
   hodlr_leaf_solve_vec_kernel<<<(nleaves + 3) / 4, 128, 0, s>>>(nleaves, h.leaf_a_d, h.leaf_n_d, h.leaf_lu_off,
-                                                                h.leaf_lu, h.leaf_prow, h.xt);
+                                                                h.leaf_lu, h.xt);
   for (int dd = h.depths - 1; dd >= 0; --dd) {
     int rc = apply_round(h, dd, s, err);
     if (rc != DAFMM_OK) return rc;

@@ -30,7 +30,7 @@ struct HodlrPlan {
   // device
   double2* Ucat = nullptr;   // n x ld: per point, per depth: W = (processed) U of its node's block
   double2* Vcat = nullptr;   // n x ld: per point, per depth: A[I_sibling, t]
-  double2* leaf_lu = nullptr;  // per leaf: n_l x n_l LU factors, column-major
+  double2* leaf_lu = nullptr;  // per leaf: n_l x n_l inverse of A[leaf, leaf] (by LU), column-major
   int32_t* leaf_prow = nullptr;  // per leaf: row permutation (P b)_i = b[prow[i]]
   int64_t* leaf_a_d = nullptr;
   int32_t* leaf_n_d = nullptr;
@@ -42,6 +42,7 @@ struct HodlrPlan {
   std::vector<int32_t*> part_ptr_d;
   std::vector<double2*> S_lu;      // per depth: per split node (2r)^2 LU, column-major
   std::vector<int32_t*> S_prow;    // per depth: per split node 2r permutation
+  std::vector<double2*> S_inv;     // per depth: per split node S^{-1}, column-major (the apply)
   double2* partial = nullptr;      // parts x r x ncol scratch
   int64_t partial_len = 0;
   double2* C = nullptr;            // per split node 2r x ncol solve buffer

@@ -2,17 +2,22 @@
 //
 // Passes per matvec:
 //   gather      x (caller order) -> x_t, v_t = w o x_t (tree order)                 HBM
-//   p2m / m2m   batched GEMVs over stored row-major operator blocks               HBM
-//   m2l         all levels in one persistent launch.  Default (m2l_store): the kernel-entry
-//               blocks A_{t s} were evaluated once at create and are streamed from HBM by
-//               TMA bulk copies (m2l_stored_kernel)                               HBM
-//               m2l_store = 0: entries evaluated on the fly (m2l_kernel)           fp64 ALU
+//   p2m / m2m   batched GEMVs over row-major operator blocks (formed on the device
+//               at create, setup_device.cu), one launch per level                  HBM
+//   m2l         all levels in one persistent launch.  Default (m2l_store = -1 -> 1):
+//               the kernel-entry blocks A_{t s}, evaluated once at create by
+//               m2l_form_kernel, streamed from HBM by TMA bulk copies
+//               (m2l_stored_kernel); m2l_store = 2: one block per node pair applied
+//               as row and column sums (m2l_pair_kernel, R22); m2l_store = 0: entries
+//               evaluated on the fly every matvec (m2l_kernel)                    HBM / fp64 ALU
 //   l2l         batched GEMVs, coarse to fine                                      HBM
 //   p2p         per leaf: near field with H0 on the fly (side stream, concurrent
 //               with p2m..l2l); symmetric pairs evaluated once (column sums)       fp64 ALU
 //   combine     L2P + near-field slots + self term + y = x + kappa^2 q phi, scattered
 //               back to caller order                                               HBM
 // Every kernel works in H0 units; the (i/4) of G is applied once per target in `combine`.
+// GMRES (run_gmres): CGS2 multi-dot / combine / norm kernels, host Givens, optional right
+// preconditioner (the HODLR of hodlr.cu, reading HR4).
 #include <cuda_runtime.h>
 
 #include <algorithm>

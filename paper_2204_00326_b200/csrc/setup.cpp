@@ -762,6 +762,7 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
       // device ACA (F2): the search sets of every node of the sweep, packed into one index
       // array; one ACA problem per (node, direction), all run by one launch
       const int ns = (int)sweep_nodes.size();
+      const double ts0 = now_s();
       std::vector<std::array<std::vector<int32_t>, 4>> sets(ns);
 #pragma omp parallel for schedule(dynamic, 4)
       for (int t = 0; t < ns; ++t) {
@@ -795,6 +796,9 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
       const double td = now_s();
       int rc = dev_aca->run(idx, probs, eps, prow, pcol, rank, level_entries, err);
       P.t_nca_device += now_s() - td;
+      if (std::getenv("DAFMM_SETUP_TRACE"))
+        std::fprintf(stderr, "nca level %d sweep %d: %d nodes, %zu set indices, sets %.3f s, device %.3f s\n", l,
+                     sweep, ns, idx.size(), td - ts0, now_s() - td);
       if (rc != DAFMM_OK) return rc;
 #pragma omp parallel for schedule(dynamic, 16)
       for (int t = 0; t < ns; ++t) {

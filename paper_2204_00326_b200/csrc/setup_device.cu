@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(const AcaProblem* __re
                                                           int* __restrict__ ticket, const int32_t* __restrict__ idx,
                                                           const double2* __restrict__ pts,
                                                           const double* __restrict__ w,
-                                                          const double* __restrict__ qrow, double eps,
+                                                          const double* __restrict__ qrow, double k4, double eps,
                                                           double2* __restrict__ scratch, int64_t stride,
                                                           int32_t* __restrict__ piv_row, int32_t* __restrict__ piv_col,
                                                           int32_t* __restrict__ rank_out,
@@ -267,6 +269,44 @@ __global__ void __launch_bounds__(kAcaThreads) aca_kernel(const AcaProblem* __re
       i = nx.p;
     }
     if (tid == 0) rank_out[p] = k;
+    if (mode == 1 && P.u_out) {
+      // the ACA factors of A's block (its entries are (i kappa^2 / 4) q_i H0 w_j: the ACA ran on
+      // q_i H0 w_j, so u_l takes the constant i k4, k4 = kappa^2 / 4), balanced: u_l / s_l and
+      // v_l s_l with s_l = sqrt(|u_l| / |v_l|)
+      __syncthreads();
+      for (int l = wid; l < k; l += kAcaWarps) {
+        double su = 0.0, sv = 0.0;
+        for (int t = lane; t < m; t += 32) su += cabs2(U[(int64_t)l * m + t]);
+        for (int j = lane; j < n; j += 32) sv += cabs2(V[(int64_t)l * n + j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          su += __shfl_xor_sync(0xffffffffu, su, o);
+          sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        }
+        if (lane == 0) s_coef[l].x = (su > 0.0 && sv > 0.0) ? sqrt(sqrt(su) / sqrt(sv)) : 1.0;
+      }
+      __syncthreads();
+      const int ldo = P.ldo;
+      for (int64_t e = tid; e < (int64_t)m * ldo; e += kAcaThreads) {
+        const int t = (int)(e / ldo), l = (int)(e % ldo);
+        double2 v = make_double2(0.0, 0.0);
+        if (l < k) {
+          const double2 u = U[(int64_t)l * m + t];
+          const double c = k4 / s_coef[l].x;
+          v = make_double2(-u.y * c, u.x * c);
+        }
+        P.u_out[(P.row_off + t) * ldo + l] = v;
+      }
+      for (int64_t e = tid; e < (int64_t)n * ldo; e += kAcaThreads) {
+        const int j = (int)(e / ldo), l = (int)(e % ldo);
+        double2 v = make_double2(0.0, 0.0);
+        if (l < k) {
+          const double2 w = V[(int64_t)l * n + j];
+          v = make_double2(w.x * s_coef[l].x, w.y * s_coef[l].x);
+        }
+        P.v_out[(P.col_off + j) * ldo + l] = v;
+      }
+    }
     __syncthreads();
   }
   if (tid == 0) atomicAdd(entries, ent);
@@ -356,6 +396,7 @@ DeviceAca::~DeviceAca() {
 }
 
 int DeviceAca::init(const double* pts, const double* w, int64_t n, double kappa, std::string& err, const double* q) {
+  kappa_ = kappa;
   if (!ck(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), err, "cudaStreamCreate (ACA)"))
     return DAFMM_ECUDA;
   std::vector<double2> xy(n);
@@ -421,9 +462,17 @@ int DeviceAca::run(const std::vector<int32_t>& idx, std::vector<AcaProblem>& pro
             ck(cudaMemsetAsync(d_ent, 0, sizeof(unsigned long long), stream_), err, "memset");
   std::vector<int32_t> rk(np), pr(out), pc(out);
   unsigned long long ent = 0;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const bool trace = std::getenv("DAFMM_SETUP_TRACE") != nullptr;
+  if (trace) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, stream_);
+  }
   if (ok) {
-    aca_kernel<<<(int)grid, kAcaThreads, 0, stream_>>>(d_probs, np, d_ticket, d_idx, pts_, w_, q_, eps, d_scratch, stride,
+    aca_kernel<<<(int)grid, kAcaThreads, 0, stream_>>>(d_probs, np, d_ticket, d_idx, pts_, w_, q_, 0.25 * kappa_ * kappa_, eps, d_scratch, stride,
                                                        d_pr, d_pc, d_rank, d_ent);
+    if (trace) cudaEventRecord(e1, stream_);
     ok = ck(cudaGetLastError(), err, "aca_kernel") &&
          ck(cudaMemcpyAsync(rk.data(), d_rank, np * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_), err, "D2H") &&
          (out == 0 || (ck(cudaMemcpyAsync(pr.data(), d_pr, out * sizeof(int32_t), cudaMemcpyDeviceToHost, stream_),
@@ -433,6 +482,16 @@ int DeviceAca::run(const std::vector<int32_t>& idx, std::vector<AcaProblem>& pro
          ck(cudaMemcpyAsync(&ent, d_ent, sizeof(ent), cudaMemcpyDeviceToHost, stream_), err, "D2H") &&
          ck(cudaStreamSynchronize(stream_), err, "aca_kernel");
   }
+  if (trace && ok) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    int64_t mx = 0;
+    for (const AcaProblem& q : probs) mx = std::max<int64_t>(mx, (int64_t)q.m + q.n);
+    std::fprintf(stderr, "  aca: %d problems, grid %lld, slot %.1f MB, largest m+n %lld, kernel %.3f ms\n", np,
+                 (long long)grid, slot / 1e6, (long long)mx, ms);
+  }
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
   for (void* q : {(void*)d_idx, (void*)d_pr, (void*)d_pc, (void*)d_rank, (void*)d_ticket, (void*)d_probs,
                   (void*)d_scratch, (void*)d_ent})
     if (q) cudaFree(q);

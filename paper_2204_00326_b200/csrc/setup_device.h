@@ -18,11 +18,17 @@ namespace dafmm {
 //           zero residual rows skipped, rank cap min(m, n, 200, cap > 0 ? cap : 200)
 //   mode 1: the HODLR preconditioner's fixed-rank ACA (reading HR2) on the rows of A, q_i G w_j:
 //           first row first_row, rank cap `cap`, ends at a zero residual row or column
+//   mode 1 with u_out / v_out: the ACA factors themselves are written out (the rank-k approximant
+//           sum_l u_l v_l^T, balanced so |u_l| = |v_l|): u_out[(row_off + t) ldo + l], v_out[(col_off + j)
+//           ldo + l] for l < ldo (zero for l >= rank)
 struct AcaProblem {
   int64_t row_off, col_off;
   int32_t m, n;
   int64_t out_off;
   int32_t first_row = 0, cap = 0, mode = 0, pad = 0;
+  double2* u_out = nullptr;
+  double2* v_out = nullptr;
+  int32_t ldo = 0, pad2 = 0;
 };
 
 // Translation operators formed on the device (P:427-562 in the G-only form of DESIGN.md §5):
@@ -68,6 +74,7 @@ class DeviceAca {
   double2* pts_ = nullptr;
   double* w_ = nullptr;
   double* q_ = nullptr;
+  double kappa_ = 0.0;
   cudaStream_t stream_ = nullptr;
 };
 

@@ -25,7 +25,9 @@ setup = time.perf_counter() - t0
 st = op.stats()
 print(json.dumps(dict(config=name, N=int(P["points"].shape[0]), setup_s=round(setup, 2),
                       setup_breakdown={k: round(st[k], 3) for k in ("setup_tree_s", "setup_lists_s", "setup_nca_s",
-                                                                    "setup_ops_s", "setup_upload_s")})), flush=True)
+                                                                    "setup_nca_device_s", "setup_ops_s",
+                                                                    "setup_upload_s", "setup_ops_device_s")})),
+      flush=True)
 f = torch.from_numpy(P["f"]).cuda()
 for case in cases:
     restart, rank = case[0], case[1]
@@ -46,6 +48,15 @@ for case in cases:
         e1.record()
         e1.synchronize()
         apply_ms = e0.elapsed_time(e1) / 10
+        # quality: ||A M^{-1} b - b|| / ||b|| for a random b (0 for M = A)
+        g = torch.Generator(device="cpu").manual_seed(3)
+        bb = torch.randn(f.numel(), dtype=torch.complex128, generator=g).cuda()
+        z = torch.empty_like(bb)
+        pc.solve(bb, z)
+        az = torch.empty_like(bb)
+        op.matvec(z, az)
+        torch.cuda.synchronize()
+        pcs["precond_residual"] = (torch.linalg.norm(az - bb) / torch.linalg.norm(bb)).item()
     psi = torch.empty_like(f)
     op.gmres(f, psi, P["gmres_tol"], 2, restart, prec=pc)
     torch.cuda.synchronize()

@@ -12,9 +12,10 @@ B = json.loads(open(bench).read().strip().splitlines()[-1])
 entries = {"p2p_kernel": B["plan"]["p2p_pairs"], "near_kernel": B["plan"]["p2p_pairs"],
            "m2l_kernel": B["plan"]["m2l_entries"], "m2l_stored_kernel": B["plan"]["m2l_entries"]}
 out = {"source": "profiles/%s_ncu_summary.json (ncu --set full, config %s)" % (tag, B["config"]["workload"][:2]),
-       "fp64_tflops_measured": 34.157,
-       "fp64_peak_source": "tools/fp64_peak.cu DFMA chains, 148 SM x 8 CTA x 256 thr, 1965 MHz, "
-                           "profiles/r01_probe_fp64_peak.log",
+       "fp64_tflops_measured": 34.063,
+       "fp64_peak_source": "tools/fp64_peak.cu DFMA chains, 148 SM x 8 CTA x 256 thr: 25 back-to-back launches, "
+                           "4.56 s sustained at a median 1965 MHz SM clock, no throttle reason: 34.06 TFLOP/s "
+                           "(profiles/r2/fp64_peak_sustained.log, profiles/r2/fp64_peak_clocks.csv)",
        "kernels": {}}
 for d in S:
     k = d["kernel"]

@@ -84,6 +84,9 @@ for opts in sets:
         xs = P["x"][idx]
         err = float(np.linalg.norm((yg - xs) - (yd - xs)) / np.linalg.norm(yd - xs))
     print(json.dumps(dict(config=name, lib=lib, opts=opts, setup_s=round(setup, 2), setup_nca_s=round(st["setup_nca_s"], 2),
+                          setup_detail={k: round(st[k], 3) for k in ("setup_tree_s", "setup_lists_s", "setup_nca_s",
+                                                                     "setup_nca_device_s", "setup_ops_s",
+                                                                     "setup_upload_s", "setup_ops_device_s")},
                           ms_median=statistics.median(ts), ms_min=min(ts), far_only_ms=far_only,
                           near_only_ms=near_only,
                           far_only_passes={k: round(v / max(fcnt, 1), 4) for k, v in far_passes.items()
