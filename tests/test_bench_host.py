@@ -72,7 +72,7 @@ def test_roofline_entry_overlap_span():
 def test_roofline_entry_stored_m2l():
     """Stored M2L blocks: the dominant kernel is the HBM stream; achieved = algorithmic bytes
     (16 B per entry + 20 B per source-stream element + 16 B per output) / its launch time."""
-    stats = {"p2p_pairs": 1000, "m2l_entries": 4000, "m2l_stored": 1, "m2l_stream_len": 100, "n_loc": 50,
+    stats = {"p2p_pairs": 1000, "m2l_entries": 4000, "m2l_stored_entries": 4000, "m2l_stored": 1, "m2l_stream_len": 100, "n_loc": 50,
              "operator_bytes": 10000, "n": 64}
     inputs = {"fp64_tflops_measured": 34.0,
               "kernels": {"m2l_stored": {"dram_bytes_per_launch": 70000, "ncu_time_ms": 0.5},
