@@ -12,7 +12,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 P = make_problem(name)
 mode = int(sys.argv[3]) if len(sys.argv) > 3 else -1  # dafmm_options.m2l_store
-op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=mode)
+extra = dict((kv.split("=")[0], int(kv.split("=")[1])) for kv in os.environ.get("DAFMM_OPTS", "").split(",") if kv)
+op = prod.DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, P["nca_tol"], m2l_store=mode, **extra)
 x = torch.from_numpy(P["x"]).cuda()
 y = torch.empty_like(x)
 for _ in range(reps):
