@@ -62,6 +62,7 @@ struct DevPlan {
   int m2l_targets = 0;
   int m2l_leaf_targets = 0;       // the first m2l_leaf_targets targets are at the deepest level
   int m2l_grid = 1;               // persistent CTAs (SMs x resident CTAs per SM)
+  int* m2l_flag = nullptr;        // raised by the M2M stream when the coarser multipoles are complete
   int* m2l_ticket = nullptr;      // work counters (leaf-level part, rest), reset per matvec
   int64_t* m2l_loc_off = nullptr;
   int32_t* m2l_rows = nullptr;
@@ -81,6 +82,9 @@ struct DevPlan {
   int m2l_sym = 0;
   int m2l_pair_grid = 0;
   int64_t* m2l_self_moff = nullptr;
+  int32_t* m2l_src_ptr = nullptr;   // pair mode: per target, its source runs (one per partner node):
+  int64_t* m2l_src_off = nullptr;   //   first multipole slot of the run
+  int32_t* m2l_src_cnt = nullptr;   //   and its length (the partner's outgoing rank)
   double2* m2l_slots = nullptr;
   int m2l_in_nodes = 0;
   int64_t* m2l_in_lo = nullptr;
@@ -132,6 +136,7 @@ struct DevPlan {
   bool prof_pending = false;     // events of the last profiled matvec not yet harvested
   cudaEvent_t prof_ev[EV_COUNT] = {};
   double prof_ms[kNumPasses] = {};
+  bool prof_side_m2m = false;     // the last matvec ran M2M on the side stream (its time is between the LEAF marks)
   int64_t prof_count = 0;        // profiled matvecs harvested
 };
 

@@ -638,6 +638,9 @@ constexpr int kMSThreads = kMSConsumers + 32;  // + one producer warp (one elect
 #ifndef DAFMM_LEAF_SPLIT
 #define DAFMM_LEAF_SPLIT 0  // 1: the deepest level's M2L on its own stream from the end of P2M
 #endif
+#ifndef DAFMM_M2M_SIDE
+#define DAFMM_M2M_SIDE 0  // 1: M2M on a third stream beside the deepest level's stored M2L (flag handshake); measured slower at C4, C5 (profiles/README.md, r2p)
+#endif
 #ifndef DAFMM_NEAR_HIGH
 #define DAFMM_NEAR_HIGH 0  // 1: the near-field stream gets the high priority instead of the far field
 #endif
@@ -680,6 +683,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__global__ void set_flag_kernel(int* flag) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(flag), "r"(1) : "memory");
 }
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kMSConsumers) : "memory"); }
 // TMA 1-D bulk copy global -> shared, completion counted in bytes on barrier b
@@ -740,7 +752,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
     const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
     const int64_t* __restrict__ mat_off, const double2* __restrict__ mat, const double2* __restrict__ mult,
-    double2* __restrict__ loc) {
+    double2* __restrict__ loc, int nfree, const int* __restrict__ upper_ready) {
   extern __shared__ __align__(128) double2 ms_dyn[];  // the TMA ring: kMSStages x kMSStageE entries
   double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
   __shared__ __align__(16) double2 mb[2][kMSCols];
@@ -772,6 +784,7 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
     int64_t sp = 0, lo = 0, moff = 0;
     int ntgt = blockIdx.x, nr = 0;
     int64_t nsp = 0, nsp1 = 0, nlo = 0, nmoff = 0;
+    bool waited = false;
     auto prefetch_node = [&]() {
       if (ntgt < ntargets) {
         nr = rows[ntgt];
@@ -802,6 +815,17 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
         c0 = 0;
         ntgt += gridDim.x;
         prefetch_node();
+        // targets [nfree, ntargets) read multipoles that M2M writes on another stream while this
+        // kernel works through the deepest level's targets: wait for its flag before the first of
+        // them is published (the consumers gather a unit's multipoles only after its descriptor)
+        if (tgt >= nfree && upper_ready != nullptr && !waited) {
+          // (bounded: a flag that never comes is a scheduling bug; trap instead of hanging)
+          for (int64_t spins = 0; ld_acquire_gpu(upper_ready) == 0; ++spins) {
+            __nanosleep(256);
+            if (spins > (int64_t)1 << 24) __trap();
+          }
+          waited = true;
+        }
       }
       const int c1 = min(L, c0 + kMSCols);
       u = MSUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0), r, 0, sp, lo};
@@ -1225,6 +1249,314 @@ __global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
     buf ^= 1;
   }
   cp_async_wait_all();
+}
+
+// ---- pair-stored M2L, warp-pair version (default for m2l_store = 2) ------------------------------
+// Every pair of warps is an independent worker: it owns whole nodes (node g, g + G, ... of the
+// list sorted by decreasing work, G = warp pairs in the grid) and streams their blocks through
+// its own kPWStages-deep ring of stages, with no CTA-level barrier, so the workers of an SM
+// drift apart and one worker's wait is covered by the others' arithmetic.  A stage holds whole
+// columns (at most 32 and at most kPWStageE entries), the multipoles of those columns and, for
+// r <= 32, the owner's own multipole.  The two warps read every stage once each:
+//   row warp     lane = row t:            acc_t  += sum_c M[t, c] m_A[c]   (kept in registers over
+//                the node's stages, written at its last stage)
+//   column warp  lane = (column, part i): slot_c  = sum_t M[t, c] m_B[t]   (rows visited from a
+//                per-column rotation when r would otherwise put the lanes on few banks; parts
+//                xor-shuffle reduced)
+// The row warp also drives the ring: its lane 0 issues the TMA bulk copy of a stage's entries, and
+// one step later (when the stage's column indices have landed in registers) its lanes gather the
+// multipoles with cp.async; both complete on the stage's `full` mbarrier (1 expect_tx arrival + 32
+// cp.async.mbarrier.arrive.noinc arrivals), which both warps wait on.  A slot is refilled when both
+// warps have arrived on its `empty` mbarrier.
+#ifndef DAFMM_PAIR_CTA
+#define DAFMM_PAIR_CTA 0  // 1: the CTA-wide pair kernel (m2l_pair_kernel) instead of the warp-pair one
+#endif
+#ifndef DAFMM_PW_RINGS
+#define DAFMM_PW_RINGS 6  // warp pairs per CTA
+#endif
+#ifndef DAFMM_PW_STAGES
+#define DAFMM_PW_STAGES 3
+#endif
+#ifndef DAFMM_PW_STAGE_E
+#define DAFMM_PW_STAGE_E 512
+#endif
+#ifndef DAFMM_PW_PER_SM
+#define DAFMM_PW_PER_SM 1
+#endif
+#ifndef DAFMM_PW_SPIN
+#define DAFMM_PW_SPIN 0
+#endif
+#ifndef DAFMM_PW_UNROLL4
+#define DAFMM_PW_UNROLL4 0
+#endif
+#ifndef DAFMM_PW_MAXREG
+#define DAFMM_PW_MAXREG 64  // 6 rings x 64 threads x 64 registers: two P2P CTAs fit beside the CTA
+#endif
+constexpr int kPWRings = DAFMM_PW_RINGS;
+constexpr int kPWThreads = 64 * kPWRings;
+constexpr int kPWStages = DAFMM_PW_STAGES;
+constexpr int kPWStageE = DAFMM_PW_STAGE_E;
+static_assert(kPWStageE >= kMaxStoredRows, "a stage holds at least one whole column");
+static_assert(kPWStages >= 2, "ring depth");
+struct PWStage {
+  double2 ent[kPWStageE];  // whole columns of the block, column-major
+  double2 mv[32];          // multipoles of the stage's columns
+  double2 ms[32];          // the owner's own multipole (r <= 32)
+};
+struct PWDesc {
+  int r, ncs, flags, lg;  // flags: 1 first stage of the node, 2 last; r < 0: no more work;
+  int rot, pad;           // column pass: 2^lg lanes per column, row rotation per column
+  int64_t lo, spc, sm;    // output offset, stream offset of the first column, own multipole
+};
+struct alignas(128) PWRing {
+  PWStage st[kPWStages];
+  PWDesc desc[kPWStages];
+  uint64_t full[kPWStages], empty[kPWStages];
+};
+constexpr size_t kPWDynSmem = sizeof(PWRing) * kPWRings;
+// polling wait (test_wait, no suspend): the warp-pair kernel's waits are short and on every warp's
+// critical path
+__device__ __forceinline__ void mbar_wait_poll(uint64_t* b, uint32_t parity) {
+#if DAFMM_PW_SPIN
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+#else
+  mbar_wait(b, parity);
+#endif
+}
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void cmac(double& ar, double& ai, const double2 m, const double2 v) {
+  ar = fma(m.x, v.x, fma(-m.y, v.y, ar));
+  ai = fma(m.x, v.y, fma(m.y, v.x, ai));
+}
+__global__ void __maxnreg__(DAFMM_PW_MAXREG) m2l_pairw_kernel(
+    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
+    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
+    const int64_t* __restrict__ mat_off, const int64_t* __restrict__ self_moff, const int32_t* __restrict__ src_ptr,
+    const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cnt, const double2* __restrict__ mat,
+    const double2* __restrict__ mult, double2* __restrict__ loc, double2* __restrict__ slots) {
+  extern __shared__ __align__(128) unsigned char pw_dyn[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ring = warp >> 1, role = warp & 1;
+  PWRing& W = reinterpret_cast<PWRing*>(pw_dyn)[ring];  // (no pointer arithmetic on integers: keeps LDS)
+  if (role == 0 && lane == 0) {
+    for (int i = 0; i < kPWStages; ++i) {
+      mbar_init(&W.full[i], 1);
+      mbar_init(&W.empty[i], 2);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (role == 1) {  // ---- column warp
+    for (int k = 0;; ++k) {
+      const int slot = k % kPWStages;
+      mbar_wait_poll(&W.full[slot], (uint32_t)(k / kPWStages) & 1u);
+      const PWDesc d = W.desc[slot];
+      if (d.r < 0) break;
+      const int r = d.r, ncs = d.ncs, lg = d.lg, g = 1 << lg, rot = d.rot;
+      const int cl = lane >> lg, i = lane & (g - 1);
+      const double2* R = W.st[slot].ent;
+      double sr = 0.0, si = 0.0, tr = 0.0, ti = 0.0;
+      if (cl < ncs) {
+        const double2* col = R + cl * r;
+        if (r <= 32) {
+          const double2* ms = W.st[slot].ms;
+          if (rot == 0) {
+            int t = i;
+            for (; t + g < r; t += 2 * g) {
+              cmac(sr, si, col[t], ms[t]);
+              cmac(tr, ti, col[t + g], ms[t + g]);
+            }
+            if (t < r) cmac(sr, si, col[t], ms[t]);
+          } else {
+            int t = i + (rot * cl) % r;
+            if (t >= r) t -= r;
+            int v = i;
+            for (; v + g < r; v += 2 * g) {
+              int t1 = t + g;
+              if (t1 >= r) t1 -= r;
+              cmac(sr, si, col[t], ms[t]);
+              cmac(tr, ti, col[t1], ms[t1]);
+              t = t1 + g;
+              if (t >= r) t -= r;
+            }
+            if (v < r) cmac(sr, si, col[t], ms[t]);
+          }
+        } else {  // more than 32 rows: the own multipole from L2
+          for (int t = i; t < r; t += g) cmac(sr, si, col[t], ld2(mult + d.sm + t));
+        }
+        sr += tr;
+        si += ti;
+      }
+      for (int o = g >> 1; o > 0; o >>= 1) {
+        sr += __shfl_xor_sync(0xffffffffu, sr, o);
+        si += __shfl_xor_sync(0xffffffffu, si, o);
+      }
+      if (i == 0 && cl < ncs) slots[d.spc + cl] = make_double2(sr, si);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&W.empty[slot]);
+    }
+    return;
+  }
+  // ---- row warp (drives the ring)
+  const int G = gridDim.x * kPWRings;
+  // The stage cursor (warp-uniform; lane 0 issues): nodes g, g + G, ...; within a node its source
+  // runs (one per partner node A: r_A consecutive multipole slots = r_A columns of the block), cut
+  // into chunks of at most `cps` columns.  The next node's metadata is loaded one node ahead (one
+  // field per lane), the next run's one run ahead.
+  int nn = blockIdx.x * kPWRings + ring;  // next node to enter
+  int64_t nmeta = 0;
+  auto prefetch_node = [&]() {
+    if (nn < ntargets) {
+      if (lane == 0) nmeta = rows[nn];
+      else if (lane == 1) nmeta = stream_ptr[nn];
+      else if (lane == 2) nmeta = src_ptr[nn];
+      else if (lane == 3) nmeta = loc_off[nn];
+      else if (lane == 4) nmeta = mat_off[nn];
+      else if (lane == 5) nmeta = self_moff[nn];
+      else if (lane == 6) nmeta = src_ptr[nn + 1];
+      else if (lane == 7) nmeta = stream_ptr[nn + 1] - stream_ptr[nn];
+    }
+  };
+  prefetch_node();
+  int cr = 0, ccps = 1, crun = 0, cruns = 0;  // current node: rows, columns per stage, run cursor / end
+  int cL = 0, cc = 0;                         // its columns, the next column
+  int rc = 0, rcnt = 0;                       // the current run: columns taken, length
+  int64_t csp = 0, clo = 0, cmoff = 0, csm = 0, roff = 0;
+  int nrcnt = 0;  // the next run (loaded one run ahead)
+  int64_t nroff = 0;
+  bool done = false;
+  auto next_run = [&]() {
+    rc = 0;
+    roff = nroff;
+    rcnt = nrcnt;
+    if (crun < cruns) {  // crun: the run to load ahead
+      nroff = src_off[crun];
+      nrcnt = src_cnt[crun];
+    }
+    ++crun;
+  };
+  // issue(): a stage = the next (at most ccps) columns of the node's stream, whatever runs they
+  // belong to: one TMA for the entries, one per run segment for the multipoles, one for the own
+  // multipole, all completing on the slot's `full` barrier
+  auto issue = [&](int slot) {
+    while (!done && cc >= cL) {  // next node (skipping nodes that own no block)
+      if (nn >= ntargets) {
+        done = true;
+        break;
+      }
+      cr = (int)__shfl_sync(0xffffffffu, nmeta, 0);
+      csp = __shfl_sync(0xffffffffu, nmeta, 1);
+      crun = (int)__shfl_sync(0xffffffffu, nmeta, 2);
+      clo = __shfl_sync(0xffffffffu, nmeta, 3);
+      cmoff = __shfl_sync(0xffffffffu, nmeta, 4);
+      csm = __shfl_sync(0xffffffffu, nmeta, 5);
+      cruns = (int)__shfl_sync(0xffffffffu, nmeta, 6);
+      cL = (int)__shfl_sync(0xffffffffu, nmeta, 7);
+      nn += G;
+      prefetch_node();
+      ccps = min(32, kPWStageE / cr);
+      cc = 0;
+      rc = rcnt = 0;
+      if (crun < cruns) {
+        nroff = src_off[crun];
+        nrcnt = src_cnt[crun];
+      }
+      ++crun;
+      if (cL > 0) next_run();
+    }
+    if (done) {
+      if (lane == 0) {
+        W.desc[slot] = PWDesc{-1, 0, 0, 0, 0, 0, 0, 0, 0};
+        mbar_arrive_tx(&W.full[slot], 0u);
+      }
+      return;
+    }
+    const int ncs = min(ccps, cL - cc);
+    const bool own = cr <= 32;
+    if (lane == 0) {
+      int lg = 0;
+      while ((2 << lg) * ncs <= 32) ++lg;
+      const int g = 1 << lg;
+      const int rot = (g >= 8 || cr % (2 * g) == g) ? 0 : ((g - cr) & 7);
+      W.desc[slot] = PWDesc{cr, ncs, (cc == 0 ? 1 : 0) | (cc + ncs >= cL ? 2 : 0), lg, rot, 0, clo, csp + cc, csm};
+      mbar_arrive_tx(&W.full[slot], (uint32_t)(ncs * cr + ncs + (own ? cr : 0)) * 16u);
+      bulk_load(W.st[slot].ent, mat + cmoff + (int64_t)cc * cr, (uint32_t)(ncs * cr) * 16u, &W.full[slot]);
+      if (own) bulk_load(W.st[slot].ms, mult + csm, (uint32_t)cr * 16u, &W.full[slot]);
+    }
+    for (int c = 0; c < ncs;) {  // the multipoles, run segment by run segment
+      while (rc >= rcnt) next_run();
+      const int seg = min(ncs - c, rcnt - rc);
+      if (lane == 0) bulk_load(W.st[slot].mv + c, mult + roff + rc, (uint32_t)seg * 16u, &W.full[slot]);
+      rc += seg;
+      c += seg;
+    }
+    cc += ncs;
+  };
+  for (int i = 0; i < kPWStages - 1; ++i) issue(i);  // prologue: stages 0 .. kPWStages - 2
+  double ar = 0.0, ai = 0.0;  // the row sums of rows lane (r <= 32), over the node's stages
+  for (int k = 0;; ++k) {
+    const int slot = k % kPWStages;
+    {  // refill the slot of stage k - 1 with stage k + kPWStages - 1
+      const int ps = (slot + kPWStages - 1) % kPWStages;
+      if (k >= 1) mbar_wait_poll(&W.empty[ps], (uint32_t)((k - 1) / kPWStages) & 1u);
+      issue(ps);
+    }
+    mbar_wait_poll(&W.full[slot], (uint32_t)(k / kPWStages) & 1u);
+    const PWDesc d = W.desc[slot];
+    if (d.r < 0) break;
+    const int r = d.r, ncs = d.ncs;
+    const double2* R = W.st[slot].ent;
+    const double2* mv = W.st[slot].mv;
+    if (r <= 32) {
+      if (d.flags & 1) ar = ai = 0.0;
+      if (lane < r) {
+        const double2* p = R + lane;
+        double br = 0.0, bi = 0.0;
+        int c = 0;
+#if DAFMM_PW_UNROLL4
+        for (; c + 4 <= ncs; c += 4, p += 4 * r) {
+          const double2 m0 = p[0], m1 = p[r], m2 = p[2 * r], m3 = p[3 * r];
+          const double2 v0 = mv[c], v1 = mv[c + 1], v2 = mv[c + 2], v3 = mv[c + 3];
+          cmac(ar, ai, m0, v0);
+          cmac(br, bi, m1, v1);
+          cmac(ar, ai, m2, v2);
+          cmac(br, bi, m3, v3);
+        }
+#endif
+        for (; c + 2 <= ncs; c += 2, p += 2 * r) {
+          const double2 m0 = p[0], m1 = p[r];
+          const double2 v0 = mv[c], v1 = mv[c + 1];
+          cmac(ar, ai, m0, v0);
+          cmac(br, bi, m1, v1);
+        }
+        if (c < ncs) cmac(ar, ai, p[0], mv[c]);
+        ar += br;
+        ai += bi;
+        if (d.flags & 2) loc[d.lo + lane] = make_double2(ar, ai);  // the node's last stage
+      }
+    } else {  // more than 32 rows (rare): per stage, the rows' partial sums are added to the node's
+              // output directly (this warp is its only writer; M2L starts from zeroed outputs)
+      for (int t = lane; t < r; t += 32) {
+        double sr = 0.0, si = 0.0;
+        for (int c = 0; c < ncs; ++c) cmac(sr, si, R[c * r + t], mv[c]);
+        double2 o = loc[d.lo + t];
+        o.x += sr;
+        o.y += si;
+        loc[d.lo + t] = o;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&W.empty[slot]);
+  }
 }
 
 // loc[node] += sum of the column-sum slots the owners wrote for it (fixed order: deterministic).
@@ -1739,7 +2071,9 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
     if (pk.m2l_sym) {  // R22: own multipoles, column-sum slots, receiving nodes' slot lists
       d.m2l_sym = 1;
       d.m2l_in_nodes = (int)pk.m2l_in_lo.size();
-      ok = upload(d, &d.m2l_self_moff, pk.m2l_self_moff, err) && upload(d, &d.m2l_in_lo, pk.m2l_in_lo, err) &&
+      ok = upload(d, &d.m2l_self_moff, pk.m2l_self_moff, err) && upload(d, &d.m2l_src_ptr, pk.m2l_src_ptr, err) &&
+           upload(d, &d.m2l_src_off, pk.m2l_src_off, err) && upload(d, &d.m2l_src_cnt, pk.m2l_src_cnt, err) &&
+           upload(d, &d.m2l_in_lo, pk.m2l_in_lo, err) &&
            upload(d, &d.m2l_in_rows, pk.m2l_in_rows, err) && upload(d, &d.m2l_in_ptr, pk.m2l_in_ptr, err) &&
            upload(d, &d.m2l_in_off, pk.m2l_in_off, err) &&
            alloc(d, &d.m2l_slots, pk.m2l_stream_idx.size(), err);
@@ -1753,13 +2087,21 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
          ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
     d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
     d.m2l_store_grid = std::max(1, std::min(d.m2l_targets, DAFMM_MS_PER_SM * sms));
+#if DAFMM_PAIR_CTA
     d.m2l_pair_grid = std::max(1, std::min(d.m2l_targets, sms));
+#else
+    d.m2l_pair_grid = std::max(1, std::min((d.m2l_targets + kPWRings - 1) / kPWRings, DAFMM_PW_PER_SM * sms));
+#endif
     if (d.m2l_mat)
       ok = ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
               err, "stored M2L shared memory") &&
            ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPDynSmem),
               err, "pair M2L shared memory") &&
            ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
+              "carveout") &&
+           ck(cudaFuncSetAttribute(m2l_pairw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPWDynSmem),
+              err, "pair M2L shared memory") &&
+           ck(cudaFuncSetAttribute(m2l_pairw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
               "carveout") &&
            ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
               "carveout") &&
@@ -1780,7 +2122,7 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
        ck(cudaEventCreateWithFlags(&d.ev_fork, cudaEventDisableTiming), err, "fork event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_far, cudaEventDisableTiming), err, "join event") &&
        ck(cudaEventCreateWithFlags(&d.ev_join_near, cudaEventDisableTiming), err, "join event") &&
-       alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 2, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
+       alloc(d, &d.phi, plan.n, err) && alloc(d, &d.m2l_ticket, 2, err) && alloc(d, &d.m2l_flag, 1, err) && alloc(d, &d.x_t, plan.n, err) && alloc(d, &d.v_t, plan.n, err) && alloc(d, &d.mult, pk.n_mult, err) &&
        alloc(d, &d.loc, pk.n_loc, err) && alloc(d, &d.host_stage, 2 * plan.n, err);
   if (!ok) return DAFMM_ECUDA;
   return DAFMM_OK;
@@ -1837,6 +2179,10 @@ int harvest_profile(DevPlan& d, std::string& err) {
     return DAFMM_ECUDA;
   t[7] = std::max(near_end, far_end);
   if (!el(EV_LEAF0, EV_LEAF1, t[8])) return DAFMM_ECUDA;
+  if (d.prof_side_m2m) {  // M2M ran on its own stream between the LEAF marks
+    t[2] = t[8];
+    t[8] = 0.0;
+  }
   for (int p = 0; p < kNumPasses; ++p) d.prof_ms[p] += t[p];
   ++d.prof_count;
   d.prof_pending = false;
@@ -1873,15 +2219,30 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
     cudaMemsetAsync(d.loc, 0, sizeof(double2) * d.n_loc, fs);
     if (d.m2l_targets > 0 && !d.m2l_mat) cudaMemsetAsync(d.m2l_ticket, 0, 2 * sizeof(int), fs);
   }
+  // M2M beside the deepest level's M2L (DAFMM_M2M_SIDE): that level's M2L reads only the leaves'
+  // multipoles, so the one persistent stored-M2L launch starts right after P2M and takes those
+  // targets first (they are packed first) while M2M runs on a third stream and then raises a flag;
+  // the M2L producers wait for the flag before their first coarser target.
+  const bool side_m2m = DAFMM_M2M_SIDE && far && d.s_leaf != nullptr && d.m2l_mat != nullptr && !d.m2l_sym &&
+                        !DAFMM_LEAF_SPLIT && !d.m2m.empty() && d.m2l_leaf_targets > 0 &&
+                        d.m2l_leaf_targets < d.m2l_targets;
+  if (side_m2m) cudaMemsetAsync(d.m2l_flag, 0, sizeof(int), fs);
   mark(EV_P2M, fs);
   if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0, fs);  // P2M
   // M2L over targets [t0, t1) on stream st (ticket slot k for the on-the-fly kernel)
   auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
     if (t1 <= t0) return;
     if (d.m2l_sym) {  // one block per node pair: row sums and column sums (R22)
+#if DAFMM_PAIR_CTA
       m2l_pair_kernel<<<d.m2l_pair_grid, kPThreads, kPDynSmem, st>>>(
           t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
           d.m2l_self_moff + t0, d.m2l_mat, d.mult, d.loc, d.m2l_slots);
+#else
+      m2l_pairw_kernel<<<d.m2l_pair_grid, kPWThreads, kPWDynSmem, st>>>(
+          t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
+          d.m2l_self_moff + t0, d.m2l_src_ptr + t0, d.m2l_src_off, d.m2l_src_cnt, d.m2l_mat, d.mult, d.loc,
+          d.m2l_slots);
+#endif
       if (d.m2l_in_nodes > 0) {
         m2l_slot_gather_kernel<<<(d.m2l_in_nodes + 7) / 8, 256, 0, st>>>(d.m2l_in_nodes, d.m2l_in_lo, d.m2l_in_rows,
                                                                         d.m2l_in_ptr, d.m2l_in_off, d.m2l_slots,
@@ -1891,7 +2252,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
     } else if (d.m2l_mat) {  // from the stored blocks
       m2l_stored_kernel<<<d.m2l_store_grid, kMSThreads, kMSDynSmem, st>>>(
           t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
-          d.m2l_mat, d.mult, d.loc);
+          d.m2l_mat, d.mult, d.loc, side_m2m ? d.m2l_leaf_targets : t1 - t0, side_m2m ? d.m2l_flag : nullptr);
     } else {  // kernel entries on the fly, persistent CTAs
       m2l_kernel<<<d.m2l_grid, kM2LThreads, 0, st>>>(t1 - t0, d.m2l_ticket + k, d.m2l_loc_off + t0, d.m2l_rows + t0,
                                                       d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_item_ptr + t0,
@@ -1913,15 +2274,26 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
     m2l(0, nleaf, 0, d.s_leaf);
     mark(EV_LEAF1, d.s_leaf);
     cudaEventRecord(d.ev_leaf, d.s_leaf);
-  } else {
+  } else if (!side_m2m) {
     mark(EV_LEAF0, fs);
     mark(EV_LEAF1, fs);
   }
   mark(EV_M2M, fs);
-  if (far)
+  if (side_m2m) {
+    cudaEventRecord(d.ev_p2m, fs);
+    cudaStreamWaitEvent(d.s_leaf, d.ev_p2m, 0);
+    mark(EV_LEAF0, d.s_leaf);
+    for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, d.s_leaf);  // M2M
+    set_flag_kernel<<<1, 1, 0, d.s_leaf>>>(d.m2l_flag);
+    ++d.launches;
+    mark(EV_LEAF1, d.s_leaf);
+    cudaEventRecord(d.ev_leaf, d.s_leaf);
+  } else if (far) {
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
+  }
   mark(EV_M2L, fs);
   if (far) m2l(nleaf, d.m2l_targets, 1, fs);  // M2L: all (remaining) levels
+  if (side_m2m) cudaStreamWaitEvent(fs, d.ev_leaf, 0);  // join the M2M stream
   mark(EV_L2L, fs);
   if (far)
     for (size_t i = 0; i < d.l2l.size(); ++i) {  // L2L
@@ -1951,6 +2323,7 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
                                                         d.slot_total);
   ++d.launches;
   mark(EV_END, s);
+  d.prof_side_m2m = side_m2m;
   if (d.prof) d.prof_pending = true;
   return ck(cudaGetLastError(), err, "matvec launch") ? DAFMM_OK : DAFMM_ECUDA;
 }
