@@ -24,6 +24,7 @@ struct DevBatch {
   int items = 0;
   bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
   int ipw = 1;        // translate_rows_kernel: items per warp (lane groups of 32 / ipw)
+  bool colmajor = false;  // column-major items: translate_cm_kernel (lane per row, no reductions)
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;

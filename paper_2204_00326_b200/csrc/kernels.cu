@@ -212,6 +212,80 @@ __global__ void translate_rows_kernel(int items, const int64_t* __restrict__ dst
   }
 }
 
+// Column-major items (the default layout): entry (r, c) of the item at item_mat_off + c R + r.
+// One warp per item, one lane per output row (row blocks of 32 when R > 32): each step reads one
+// column of the operator as one coalesced run of R entries, eight columns in flight per lane, and
+// the lane accumulates its own row, so there is no cross-lane reduction at all.  The sources of
+// up to kTCMCols columns are staged in shared memory per warp and read as broadcasts.
+constexpr int kTCMCols = 128;
+constexpr int kTCMWarps = 8;
+__global__ void __launch_bounds__(32 * kTCMWarps) translate_cm_kernel(
+    int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
+    const int64_t* __restrict__ item_mat_off, const int32_t* __restrict__ item_cols,
+    const int32_t* __restrict__ term_ptr, const int64_t* __restrict__ src_off, const int32_t* __restrict__ src_cols,
+    const double2* __restrict__ ops, const double2* __restrict__ src, double2* __restrict__ dst, int accumulate) {
+  __shared__ __align__(16) double2 xs_all[kTCMWarps][kTCMCols];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kTCMWarps + w;
+  if (item >= items) return;
+  double2* xs = xs_all[w];
+  const int R = dst_rows[item], C = item_cols[item];
+  const int tb = term_ptr[item], te = term_ptr[item + 1];
+  const int64_t doff = dst_off[item];
+  const double2* M = ops + item_mat_off[item];
+  for (int rb = 0; rb < R; rb += 32) {
+    const int t = rb + lane;
+    const bool act = t < R;
+    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+    for (int cb = 0; cb < C; cb += kTCMCols) {
+      __syncwarp();
+      int cs = 0;
+      for (int q = tb; q < te; ++q) {  // stage the sources of columns [cb, cb + kTCMCols)
+        const int ce = cs + src_cols[q];
+        const int c0 = max(cs, cb), c1 = min(ce, cb + kTCMCols);
+        if (c0 < c1) {
+          const double2* sv = src + src_off[q] - cs;
+          for (int c = c0 + lane; c < c1; c += 32) xs[c - cb] = ld2(sv + c);
+        }
+        cs = ce;
+      }
+      __syncwarp();
+      if (act) {
+        const int nc = min(kTCMCols, C - cb);
+        const double2* p = M + (int64_t)cb * R + t;
+        int c = 0;
+        for (; c + 8 <= nc; c += 8, p += 8 * R) {
+          double2 m[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) m[q] = ld2(p + q * R);
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            const double2 v0 = xs[c + q], v1 = xs[c + q + 1];
+            ar = fma(m[q].x, v0.x, fma(-m[q].y, v0.y, ar));
+            ai = fma(m[q].x, v0.y, fma(m[q].y, v0.x, ai));
+            br = fma(m[q + 1].x, v1.x, fma(-m[q + 1].y, v1.y, br));
+            bi = fma(m[q + 1].x, v1.y, fma(m[q + 1].y, v1.x, bi));
+          }
+        }
+        for (; c < nc; ++c, p += R) {
+          const double2 mm = ld2(p), v0 = xs[c];
+          ar = fma(mm.x, v0.x, fma(-mm.y, v0.y, ar));
+          ai = fma(mm.x, v0.y, fma(mm.y, v0.x, ai));
+        }
+      }
+    }
+    if (act) {
+      double2 o = make_double2(ar + br, ai + bi);
+      if (accumulate) {
+        const double2 pv = dst[doff + t];
+        o.x += pv.x;
+        o.y += pv.y;
+      }
+      dst[doff + t] = o;
+    }
+  }
+}
+
 // ---- source streams ----------------------------------------------------------------------------
 // P2P and M2L share one engine: a CTA owns a set of targets (the points of a leaf or the pivots
 // of a node, one per thread "t", with nsl source slices) and a stream of sources given as a CSR
@@ -1935,8 +2009,9 @@ bool alloc(DevPlan& d, T** dst, size_t count, std::string& err) {
   return true;
 }
 
-bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& err) {
+bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& err, bool colmajor) {
   b.items = (int)h.dst_off.size();
+  b.colmajor = colmajor;
   // kernel choice by shape: wide items (mean >= 48 columns) read each row with all 32 lanes
   // and reduce across the warp; narrow ones give each lane a row.  (A TMA-streamed variant on
   // column-major items, the stored-M2L kernel's ring, was measured slower: one gather latency
@@ -1959,7 +2034,11 @@ int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, do
   if (b.items == 0) return 0;
   int threads = 256;
   int blocks = (b.items * 32 + threads - 1) / threads;
-  if (b.wide)
+  if (b.colmajor)
+    translate_cm_kernel<<<(b.items + kTCMWarps - 1) / kTCMWarps, 32 * kTCMWarps, 0, st>>>(
+        b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols, b.term_ptr, b.src_off, b.src_cols, d.ops, src,
+        dst, accumulate);
+  else if (b.wide)
     translate_kernel<<<blocks, threads, 0, st>>>(b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols,
                                                  b.term_ptr, b.src_off, b.src_cols, d.ops, src, dst, accumulate);
   else
@@ -1990,11 +2069,11 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
   bool ok = upload(d, &d.pts_t, pts, err) && upload(d, &d.w_t, pk.w_t, err) && upload(d, &d.qk2_t, pk.qk2_t, err) &&
             upload(d, &d.D_t, D, err) && upload(d, &d.perm, pk.perm, err) && upload(d, &d.so_xy, so, err) &&
             upload(d, &d.ti_xy, ti, err) &&
-            (pk.ops_on_device ? alloc(d, &d.ops, (size_t)pk.ops_len, err) : upload(d, &d.ops, ops, err)) && upload_batch(d, d.p2m, pk.p2m, err);
+            (pk.ops_on_device ? alloc(d, &d.ops, (size_t)pk.ops_len, err) : upload(d, &d.ops, ops, err)) && upload_batch(d, d.p2m, pk.p2m, err, pk.ops_colmajor != 0);
   d.m2m.assign(pk.m2m.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], err);
+  for (size_t i = 0; ok && i < pk.m2m.size(); ++i) ok = upload_batch(d, d.m2m[i], pk.m2m[i], err, pk.ops_colmajor != 0);
   d.l2l.assign(pk.l2l.size(), DevBatch());
-  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err);
+  for (size_t i = 0; ok && i < pk.l2l.size(); ++i) ok = upload_batch(d, d.l2l[i], pk.l2l[i], err, pk.ops_colmajor != 0);
   if (ok && pk.ops_on_device) {  // F2: translation operators formed on the device
     std::vector<OpGroup> groups(pk.opd_groups.size());
     for (size_t g = 0; g < groups.size(); ++g) {

@@ -105,6 +105,7 @@ struct Packed {
   };
   // operators formed on the device (setup_device, every cross matrix of rank <= 64): ops stays
   // empty on the host and upload_plan runs form_ops_device on these descriptors
+  int ops_colmajor = 1;  // translation items column-major (translate_cm_kernel); 0: row-major (env DAFMM_OPS_ROWMAJOR)
   int ops_on_device = 0;
   int64_t ops_len = 0;
   std::vector<int32_t> opd_piv;

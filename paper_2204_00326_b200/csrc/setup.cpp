@@ -894,6 +894,10 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   };
   std::vector<Job> jobs;
   int64_t ops_len = 0;
+  // column-major items (default): the translate kernel gives every output row a lane and reads
+  // one coalesced column per step; DAFMM_OPS_ROWMAJOR=1 keeps the row-major items of the
+  // warp-per-row kernels (A/B only)
+  pk.ops_colmajor = std::getenv("DAFMM_OPS_ROWMAJOR") ? 0 : 1;
   auto add_job = [&](int kind, int l, int nd, int ch, int64_t len) {
     jobs.push_back({kind, l, nd, ch, ops_len, 0, 0, 0});
     ops_len += len;
@@ -917,7 +921,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     bt.term_ptr.push_back((int32_t)bt.src_off.size());
     int cs = 0;
     for (const Term& t : terms) {
-      jobs.push_back({kind, l, t.node, t.child, off, C, cs, rows});
+      jobs.push_back({kind, l, t.node, t.child, off, pk.ops_colmajor ? 0 : C, cs, rows});
       bt.src_off.push_back(t.src_off);
       bt.src_cols.push_back(t.cols);
       cs += t.cols;
@@ -1342,7 +1346,8 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
         for (int a = 0; a < r; ++a) rhs[a] = cx.H(np.to[a], cols[c]);
         lu.solve(rhs.data());
         for (int a = 0; a < r; ++a) {
-          const size_t at = (size_t)a * J.stride + J.col_start + c;
+          const size_t at = J.stride > 0 ? (size_t)a * J.stride + J.col_start + c
+                                         : (size_t)(J.col_start + c) * J.rows + a;
           out[at] = {rhs[a].real(), rhs[a].imag()};
         }
       }
@@ -1372,7 +1377,9 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
         for (int c = 0; c < r; ++c) rhs[c] = cx.H(rows[a], np.si[c]);
         lu.solve(rhs.data());
         for (int c = 0; c < r; ++c) {
-          const size_t at = J.kind == 3 ? (size_t)c * nr + a : (size_t)a * J.stride + J.col_start + c;
+          const size_t at = J.kind == 3      ? (size_t)c * nr + a
+                            : J.stride > 0 ? (size_t)a * J.stride + J.col_start + c
+                                           : (size_t)(J.col_start + c) * J.rows + a;
           out[at] = {rhs[c].real(), rhs[c].imag()};
         }
       }
