@@ -2,13 +2,15 @@
 //
 // Passes per matvec:
 //   gather      x (caller order) -> x_t, v_t = w o x_t (tree order)                 HBM
-//   p2m / m2m   batched GEMVs over row-major operator blocks (formed on the device
-//               at create, setup_device.cu), one launch per level                  HBM
+//   p2m / m2m   batched GEMVs over column-major operator blocks (formed on the device
+//               at create, setup_device.cu), a lane per output row
+//               (translate_cm_kernel), one launch per level                        HBM
 //   m2l         all levels in one persistent launch.  Default (m2l_store = -1 -> 1):
 //               the kernel-entry blocks A_{t s}, evaluated once at create by
 //               m2l_form_kernel, streamed from HBM by TMA bulk copies
 //               (m2l_stored_kernel); m2l_store = 2: one block per node pair applied
-//               as row and column sums (m2l_pair_kernel, R22); m2l_store = 0: entries
+//               as row and column sums by warp pairs (m2l_pairw_kernel, R22);
+//               m2l_store = 0: entries
 //               evaluated on the fly every matvec (m2l_kernel)                    HBM / fp64 ALU
 //   l2l         batched GEMVs, coarse to fine                                      HBM
 //   p2p         per leaf: near field with H0 on the fly (side stream, concurrent
@@ -1049,283 +1051,13 @@ __global__ void __launch_bounds__(kMSThreads, DAFMM_MS_MINB) m2l_stored_kernel(
 // ---- pair-stored M2L (reading R22, dafmm_options.m2l_store = 2) ---------------------------------
 // With one skeleton per node (R19: s^{B,o} = t^{B,i}) the block of (B <- A) is the transpose of
 // the block of (A <- B), G being symmetric, so each unordered interaction-list pair
-// keeps one block, in the stream of its owner B.  The owner's CTA applies it twice per matvec:
+// keeps one block, in the stream of its owner B.  The owner applies it twice per matvec:
 //   row sums     u_B[t] += sum_c M[t, c] m_A[c]         (as m2l_stored_kernel)
 //   column sums  slot[c] = sum_t M[t, c] m_B[t]          (u_A's share; added by m2l_slot_gather)
-// so the HBM stream is half that of m2l_stored_kernel for the same work.  Same warp-specialised
-// TMA ring, but every stage holds whole columns (floor(kMSStageE / r) of them), so the column
-// sums of a stage are complete in shared memory: after the row pass over a stage, the consumers
-// re-read it column-wise (g threads per column, xor-shuffle reduced) -- a second shared-memory
-// read of the stage instead of a second HBM read of the block.
-#ifndef DAFMM_PC
-#define DAFMM_PC 256  // pair-M2L consumer threads (8 warps): one CTA per SM
-#endif
-#ifndef DAFMM_P_MINB
-#define DAFMM_P_MINB 3  // register cap 72: two P2P CTAs fit beside the pair-M2L CTA
-#endif
-#ifndef DAFMM_PSTAGES
-#define DAFMM_PSTAGES 6
-#endif
-constexpr int kPC = DAFMM_PC;
-constexpr int kPThreads = kPC + 32;
-constexpr int kPStages = DAFMM_PSTAGES;
-constexpr int kPIdx = kMSCols / kPC;
-constexpr size_t kPDynSmem = sizeof(double2) * kPStages * kMSStageE;
-// named barrier 2 over the pair kernel's kPC consumer threads (barrier 1 counts kMSConsumers)
-__device__ __forceinline__ void pair_consumers_sync() { asm volatile("bar.sync 2, %0;" ::"n"(kPC) : "memory"); }
-static_assert(kMSCols % kPC == 0, "multipole gather: whole indices per thread");
-struct MSPUnit {
-  int tgt, c0, c1, flags;  // flags: 1 first unit of the node, 2 last; tgt < 0: no more work
-  int r, pad;
-  int64_t sp, lo, self_m;  // stream offset, output offset, own multipole
-};
-__global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
-    int ntargets, const int64_t* __restrict__ loc_off, const int32_t* __restrict__ rows,
-    const int64_t* __restrict__ stream_ptr, const int32_t* __restrict__ stream_idx,
-    const int64_t* __restrict__ mat_off, const int64_t* __restrict__ self_moff, const double2* __restrict__ mat,
-    const double2* __restrict__ mult, double2* __restrict__ loc, double2* __restrict__ slots) {
-  extern __shared__ __align__(128) double2 ms_dyn[];
-  double2(*ring)[kMSStageE] = reinterpret_cast<double2(*)[kMSStageE]>(ms_dyn);
-  __shared__ __align__(16) double2 mb[2][kMSCols];
-  __shared__ __align__(16) double2 mself[2][kMaxStoredRows];
-  static_assert(kPC <= kMSCols, "the row reduction reuses mb[buf]");
-  __shared__ __align__(8) uint64_t full[kPStages], empty[kPStages], ufull[kMSUnits], uempty[kMSUnits];
-  __shared__ MSPUnit units[kMSUnits];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kPStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kPC / 32);
-    }
-    for (int i = 0; i < kMSUnits; ++i) {
-      mbar_init(&ufull[i], 1);
-      mbar_init(&uempty[i], kPC / 32);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (warp == kPC / 32) {  // ---- producer (one lane)
-    if (lane != 0) return;
-    int stage = 0, uslot = 0;
-    uint32_t sphase = 0, uphase = 0;
-    int tgt = -2, L = 0, c0 = 0, r = 0;
-    int64_t sp = 0, lo = 0, moff = 0, sm = 0;
-    int ntgt = blockIdx.x, nr = 0;
-    int64_t nsp = 0, nsp1 = 0, nlo = 0, nmoff = 0, nsm = 0;
-    auto prefetch_node = [&]() {
-      if (ntgt < ntargets) {
-        nr = rows[ntgt];
-        nsp = stream_ptr[ntgt];
-        nsp1 = stream_ptr[ntgt + 1];
-        nlo = loc_off[ntgt];
-        nmoff = mat_off[ntgt];
-        nsm = self_moff[ntgt];
-      }
-    };
-    prefetch_node();
-    auto next_unit = [&](MSPUnit& u) {
-      if (tgt == -1 || ((tgt == -2 || c0 >= L) && ntgt >= ntargets)) {
-        tgt = -1;
-        u = MSPUnit{-1, 0, 0, 0, 0, 0, 0, 0, 0};
-        return;
-      }
-      if (tgt == -2 || c0 >= L) {
-        tgt = ntgt;
-        r = nr;
-        sp = nsp;
-        L = (int)(nsp1 - nsp);
-        lo = nlo;
-        moff = nmoff;
-        sm = nsm;
-        c0 = 0;
-        ntgt += gridDim.x;
-        prefetch_node();
-      }
-      const int c1 = min(L, c0 + kMSCols);
-      u = MSPUnit{tgt, c0, c1, (c0 == 0 ? 1 : 0) | (c1 >= L ? 2 : 0), r, 0, sp, lo, sm};
-      c0 = c1;
-    };
-    auto publish = [&](const MSPUnit& u) {
-      mbar_wait(&uempty[uslot], uphase ^ 1);
-      units[uslot] = u;
-      mbar_arrive(&ufull[uslot]);
-      if (++uslot == kMSUnits) {
-        uslot = 0;
-        uphase ^= 1;
-      }
-    };
-    MSPUnit cur, nxt;
-    next_unit(cur);
-    int64_t cur_moff = moff;
-    publish(cur);
-    while (cur.tgt >= 0) {
-      next_unit(nxt);
-      const int64_t nxt_moff = moff;
-      publish(nxt);
-      const int cps = kMSStageE / cur.r;  // whole columns per stage
-      const double2* src = mat + cur_moff + (int64_t)cur.c0 * cur.r;
-      for (int cc = 0; cc < cur.c1 - cur.c0; cc += cps) {
-        const int cnt = min(cps, cur.c1 - cur.c0 - cc) * cur.r;
-        mbar_wait(&empty[stage], sphase ^ 1);
-        mbar_arrive_tx(&full[stage], (uint32_t)cnt * 16u);
-        bulk_load(ring[stage], src + (int64_t)cc * cur.r, (uint32_t)cnt * 16u, &full[stage]);
-        if (++stage == kPStages) {
-          stage = 0;
-          sphase ^= 1;
-        }
-      }
-      cur = nxt;
-      cur_moff = nxt_moff;
-    }
-    return;
-  }
-  // ---- consumers
-  const int j = threadIdx.x;
-  int stage = 0, uslot = 0;
-  uint32_t sphase = 0, uphase = 0;
-  auto take = [&]() {
-    mbar_wait(&ufull[uslot], uphase);
-    const MSPUnit u = units[uslot];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&uempty[uslot]);
-    if (++uslot == kMSUnits) {
-      uslot = 0;
-      uphase ^= 1;
-    }
-    return u;
-  };
-  auto gather_idx = [&](const MSPUnit& u, int* kidx) {
-    const int64_t sp = u.sp + u.c0;
-#pragma unroll
-    for (int k = 0; k < kPIdx; ++k) {
-      const int c = j + k * kPC;
-      kidx[k] = (u.tgt >= 0 && c < u.c1 - u.c0) ? __ldg(stream_idx + sp + c) : -1;
-    }
-  };
-  auto gather_issue = [&](const int* kidx, const MSPUnit& u, int b) {
-#pragma unroll
-    for (int k = 0; k < kPIdx; ++k)
-      if (kidx[k] >= 0) cp_async16(&mb[b][j + k * kPC], mult + kidx[k]);
-    if (u.tgt >= 0 && j < u.r) cp_async16(&mself[b][j], mult + u.self_m + j);  // own multipole
-    cp_async_commit();
-  };
-  int nsl = 0, P = 1, buf = 0, sl = 0;
-  bool act = false;
-  double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
-  int kidx[kPIdx];
-  MSPUnit u = take();
-  gather_idx(u, kidx);
-  gather_issue(kidx, u, 0);
-  while (u.tgt >= 0) {
-    const MSPUnit un = take();
-    gather_idx(un, kidx);
-    const int r = u.r;
-    if (u.flags & 1) {
-      nsl = kPC / r;
-      P = nsl * r;
-      sl = j / r;
-      act = j < P;
-      ar0 = ai0 = ar1 = ai1 = 0.0;
-    }
-    cp_async_wait_all();
-    pair_consumers_sync();  // u's multipoles complete; everyone is done with the other buffers
-    const double2* mv = mb[buf];
-    const double2* msf = mself[buf];
-    const int nc = u.c1 - u.c0;
-    const int cps = kMSStageE / r;
-    const int nst = (nc + cps - 1) / cps;
-    // column pass geometry: g threads per column (power of 2, <= 32), kPC / g columns
-    // per round
-    for (int st = 0; st < nst; ++st) {
-      const int a = st * cps, b = min(nc, a + cps);
-      mbar_wait(&full[stage], sphase);
-      const double2* R = ring[stage];
-      if (act) {  // row pass: thread (t = j mod r, slice sl) takes columns c = sl (mod nsl)
-        const int t = j - sl * r;
-        int c = a + ((sl - a) % nsl + nsl) % nsl;
-        for (; c + 3 * nsl < b; c += 4 * nsl) {
-          const double2 m0 = R[(c - a) * r + t], v0 = mv[c];
-          const double2 m1 = R[(c + nsl - a) * r + t], v1 = mv[c + nsl];
-          const double2 m2 = R[(c + 2 * nsl - a) * r + t], v2 = mv[c + 2 * nsl];
-          const double2 m3 = R[(c + 3 * nsl - a) * r + t], v3 = mv[c + 3 * nsl];
-          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
-          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
-          ar1 = fma(m1.x, v1.x, fma(-m1.y, v1.y, ar1));
-          ai1 = fma(m1.x, v1.y, fma(m1.y, v1.x, ai1));
-          ar0 = fma(m2.x, v2.x, fma(-m2.y, v2.y, ar0));
-          ai0 = fma(m2.x, v2.y, fma(m2.y, v2.x, ai0));
-          ar1 = fma(m3.x, v3.x, fma(-m3.y, v3.y, ar1));
-          ai1 = fma(m3.x, v3.y, fma(m3.y, v3.x, ai1));
-        }
-        for (; c < b; c += nsl) {
-          const double2 m0 = R[(c - a) * r + t], v0 = mv[c];
-          ar0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, ar0));
-          ai0 = fma(m0.x, v0.y, fma(m0.y, v0.x, ai0));
-        }
-      }
-      {  // column pass: slot[c] = sum_t M[t, c] m_B[t] over the stage's whole columns; items
-         // (column, part i < g), g threads per column (a power of 2: lane-aligned groups)
-        const int ncs = b - a;
-        int g = 1;
-        while (g < 32 && 2 * g * ncs <= kPC) g <<= 1;
-        const int i = j & (g - 1);
-        for (int it = j; it < ((ncs * g + kPC - 1) / kPC) * kPC; it += kPC) {
-          const int cl = it / g;
-          double sr0 = 0.0, si0 = 0.0, sr1 = 0.0, si1 = 0.0;
-          if (cl < ncs) {
-            const double2* col = R + cl * r;
-            int t = i;
-            for (; t + g < r; t += 2 * g) {
-              const double2 m0 = col[t], v0 = msf[t], m1 = col[t + g], v1 = msf[t + g];
-              sr0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, sr0));
-              si0 = fma(m0.x, v0.y, fma(m0.y, v0.x, si0));
-              sr1 = fma(m1.x, v1.x, fma(-m1.y, v1.y, sr1));
-              si1 = fma(m1.x, v1.y, fma(m1.y, v1.x, si1));
-            }
-            if (t < r) {
-              const double2 m0 = col[t], v0 = msf[t];
-              sr0 = fma(m0.x, v0.x, fma(-m0.y, v0.y, sr0));
-              si0 = fma(m0.x, v0.y, fma(m0.y, v0.x, si0));
-            }
-          }
-          double sr = sr0 + sr1, si = si0 + si1;
-          for (int o = g >> 1; o > 0; o >>= 1) {
-            sr += __shfl_xor_sync(0xffffffffu, sr, o);
-            si += __shfl_xor_sync(0xffffffffu, si, o);
-          }
-          if (i == 0 && cl < ncs) slots[u.sp + u.c0 + a + cl] = make_double2(sr, si);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[stage]);
-      if (++stage == kPStages) {
-        stage = 0;
-        sphase ^= 1;
-      }
-      if (st == nst / 2) gather_issue(kidx, un, buf ^ 1);  // next unit's multipoles
-    }
-    if (u.flags & 2) {  // reduce the slices of each row, write u_B's own share
-      // (in mb[buf], free once every consumer has finished the unit's passes)
-      double2* red = mb[buf];
-      pair_consumers_sync();
-      red[j] = make_double2(ar0 + ar1, ai0 + ai1);
-      pair_consumers_sync();
-      if (j < r) {
-        double sr = 0.0, si = 0.0;
-        for (int q = j; q < P; q += r) {
-          sr += red[q].x;
-          si += red[q].y;
-        }
-        loc[u.lo + j] = make_double2(sr, si);
-      }
-    }
-    u = un;
-    buf ^= 1;
-  }
-  cp_async_wait_all();
-}
-
-// ---- pair-stored M2L, warp-pair version (default for m2l_store = 2) ------------------------------
+// so the HBM stream is half that of m2l_stored_kernel for the same work.  (A CTA-wide version --
+// the stored kernel's ring with whole-column stages, 8 consumer warps doing both passes between
+// CTA barriers -- took 3.9 ms at C4 against 2.15 ms for the warp pairs below.)
+// The kernel: warp pairs.
 // Every pair of warps is an independent worker: it owns whole nodes (node g, g + G, ... of the
 // list sorted by decreasing work, G = warp pairs in the grid) and streams their blocks through
 // its own kPWStages-deep ring of stages, with no CTA-level barrier, so the workers of an SM
@@ -1342,9 +1074,6 @@ __global__ void __launch_bounds__(kPThreads, DAFMM_P_MINB) m2l_pair_kernel(
 // multipoles with cp.async; both complete on the stage's `full` mbarrier (1 expect_tx arrival + 32
 // cp.async.mbarrier.arrive.noinc arrivals), which both warps wait on.  A slot is refilled when both
 // warps have arrived on its `empty` mbarrier.
-#ifndef DAFMM_PAIR_CTA
-#define DAFMM_PAIR_CTA 0  // 1: the CTA-wide pair kernel (m2l_pair_kernel) instead of the warp-pair one
-#endif
 #ifndef DAFMM_PW_RINGS
 #define DAFMM_PW_RINGS 6  // warp pairs per CTA
 #endif
@@ -1403,9 +1132,6 @@ __device__ __forceinline__ void mbar_wait_poll(uint64_t* b, uint32_t parity) {
 #else
   mbar_wait(b, parity);
 #endif
-}
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* b) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(b)) : "memory");
 }
 __device__ __forceinline__ void cmac(double& ar, double& ai, const double2 m, const double2 v) {
   ar = fma(m.x, v.x, fma(-m.y, v.y, ar));
@@ -2166,18 +1892,10 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
          ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, m2l_kernel, kM2LThreads, 0), err, "occupancy");
     d.m2l_grid = std::max(1, std::min(d.m2l_targets, std::max(1, per_sm) * sms));
     d.m2l_store_grid = std::max(1, std::min(d.m2l_targets, DAFMM_MS_PER_SM * sms));
-#if DAFMM_PAIR_CTA
-    d.m2l_pair_grid = std::max(1, std::min(d.m2l_targets, sms));
-#else
     d.m2l_pair_grid = std::max(1, std::min((d.m2l_targets + kPWRings - 1) / kPWRings, DAFMM_PW_PER_SM * sms));
-#endif
     if (d.m2l_mat)
       ok = ck(cudaFuncSetAttribute(m2l_stored_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMSDynSmem),
               err, "stored M2L shared memory") &&
-           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPDynSmem),
-              err, "pair M2L shared memory") &&
-           ck(cudaFuncSetAttribute(m2l_pair_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
-              "carveout") &&
            ck(cudaFuncSetAttribute(m2l_pairw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPWDynSmem),
               err, "pair M2L shared memory") &&
            ck(cudaFuncSetAttribute(m2l_pairw_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err,
@@ -2312,16 +2030,10 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
     if (t1 <= t0) return;
     if (d.m2l_sym) {  // one block per node pair: row sums and column sums (R22)
-#if DAFMM_PAIR_CTA
-      m2l_pair_kernel<<<d.m2l_pair_grid, kPThreads, kPDynSmem, st>>>(
-          t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
-          d.m2l_self_moff + t0, d.m2l_mat, d.mult, d.loc, d.m2l_slots);
-#else
       m2l_pairw_kernel<<<d.m2l_pair_grid, kPWThreads, kPWDynSmem, st>>>(
           t1 - t0, d.m2l_loc_off + t0, d.m2l_rows + t0, d.m2l_stream_ptr + t0, d.m2l_stream_idx, d.m2l_mat_off + t0,
           d.m2l_self_moff + t0, d.m2l_src_ptr + t0, d.m2l_src_off, d.m2l_src_cnt, d.m2l_mat, d.mult, d.loc,
           d.m2l_slots);
-#endif
       if (d.m2l_in_nodes > 0) {
         m2l_slot_gather_kernel<<<(d.m2l_in_nodes + 7) / 8, 256, 0, st>>>(d.m2l_in_nodes, d.m2l_in_lo, d.m2l_in_rows,
                                                                         d.m2l_in_ptr, d.m2l_in_off, d.m2l_slots,

@@ -252,6 +252,29 @@ def test_gpu_pair_stored_m2l(name, n, kappa, tmp_path):
     assert _rel(near + far, y) <= 1e-14
 
 
+def test_gpu_pair_stored_m2l_wide_nodes():
+    """m2l_store=2 on nodes with more than 32 pivots (the warp-pair kernel's row-block path: the
+    row warp adds each stage's partial rows to the node's output, the column warp reads the own
+    multipole from global memory): config 1 at nca_tol 1e-12.  Against the on-the-fly M2L and the
+    per-target stored blocks on the same plan (<= 1e-13) and dense (<= 1e-9)."""
+    P = make_problem("c1")
+    tol = 1e-12
+    kw = dict(symmetric_pivots=1)
+    op = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, tol, m2l_store=2, **kw)
+    st = op.stats()
+    assert st["m2l_stored"] == 2 and st["max_rank"] > 32, st["max_rank"]
+    x = P["x"]
+    y = _gpu_matvec(op, x)
+    assert np.array_equal(y, _gpu_matvec(op, x))
+    for mode in (0, 1):
+        op2 = _prod().DAFMM(P["points"], P["weights"], P["q"], P["kappa"], 64, tol, m2l_store=mode, **kw)
+        assert op2.stats()["m2l_stored"] == mode
+        assert _rel(_gpu_matvec(op2, x) - x, y - x) <= 1e-13
+    prob = Problem(P["points"], P["weights"], P["q"], P["kappa"])
+    yd = oracle.dense_matvec(prob, x)
+    assert _rel(y - x, yd - x) <= 1e-9  # (the 10 nca_tol gate is taken at the configs' own tolerances)
+
+
 @pytest.mark.parametrize("name,n,kappa", [("c2", 128, 20.0), ("c5", 5, 12.0), ("c2", 128, 40.0)])
 def test_gpu_device_aca_matches_host_aca(name, n, kappa, tmp_path):
     """F2: the NCA ACAs run on the device (setup_device=1, default) or on the host (0).  Same
