@@ -1263,7 +1263,8 @@ __global__ void __maxnreg__(DAFMM_PW_MAXREG) m2l_pairw_kernel(
       cL = (int)__shfl_sync(0xffffffffu, nmeta, 7);
       nn += G;
       prefetch_node();
-      ccps = min(32, kPWStageE / cr);
+      if (cr <= 0) cL = 0;  // a node without pivots owns no entries (reading R11)
+      ccps = min(32, kPWStageE / max(cr, 1));
       cc = 0;
       rc = rcnt = 0;
       if (crun < cruns) {
