@@ -832,6 +832,15 @@ int build_plan(Plan& P, const double* points, const double* weights, const doubl
 // Packing: node offsets, pivot coordinates, operator blocks (P:427-562 in the G-only form of
 // DESIGN.md §Operators), and the per-pass work lists.
 int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
+  const bool trace = std::getenv("DAFMM_SETUP_TRACE") != nullptr;
+  double tr0 = now_s();
+  auto mark = [&](const char* what) {
+    if (trace) {
+      const double t = now_s();
+      std::fprintf(stderr, "pack: %-28s %.3f s\n", what, t - tr0);
+      tr0 = t;
+    }
+  };
   double t0 = now_s();
   const int L = P.L;
   const int64_t n = P.n;
@@ -881,9 +890,10 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       }
     }
   // ---- operator block descriptors; blocks are filled in parallel afterwards ----
-  // Translation items (P2M, M2M, L2L) store one row-major block per item: the terms' blocks side
-  // by side (row stride = the item's total column count), so the translate kernel reads each
-  // row as one contiguous run.  U (L2P) stays column-major (one point per thread in combine).
+  // Translation items (P2M, M2M, L2L) store one block per item.  Column-major (default): entry
+  // (row, col) at col * rows + row, the terms' blocks one after another, read one column per step
+  // by translate_cm_kernel.  Row-major (DAFMM_OPS_ROWMAJOR): the terms' blocks side by side (row
+  // stride = the item's total column count).  U (L2P) is column-major (one point per thread in combine).
   struct Job {
     int kind;  // 0: V (P2M), 1: T (M2M), 2: C (L2L), 3: U (L2P)
     int level, node, child;  // node at `level`, child node at level + 1
@@ -994,6 +1004,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     bt.term_ptr.push_back((int32_t)bt.src_off.size());
     pk.l2l.push_back(std::move(bt));
   }
+  mark("offsets, translation items");
   // M2L targets (all levels, one launch).  Each target's source nodes are
   // classified by the exact z-range of their pivot-point pairs and grouped into band-uniform
   // segments.
@@ -1063,6 +1074,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       tg.swap(keep);
     }
   }
+  mark("M2L target lists");
   std::vector<std::vector<int>> codes(tg.size());
 #pragma omp parallel for schedule(dynamic, 16)
   for (size_t i = 0; i < tg.size(); ++i) {
@@ -1082,6 +1094,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       codes[i][e] = choose_band(P.kappa * std::sqrt(lo), P.kappa * std::sqrt(hi), false);
     }
   }
+  mark("M2L band classification");
   // targets in order of decreasing work (the persistent M2L kernel takes them in this order)
   std::vector<int64_t> tcost(tg.size(), 0);
   for (size_t i = 0; i < tg.size(); ++i) {
@@ -1105,13 +1118,14 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
   pk.m2l_stream_ptr.push_back(0);
   // R22: per level, (receiving node, slot of its first pivot in the owner's stream)
   std::vector<std::vector<std::pair<int, int64_t>>> in_lists((size_t)L + 1);
+  int64_t stream_len = 0;
   for (size_t i : torder) {
     const int l = tg[i].level;
     const int ri = (int)P.piv[l][tg[i].node].ti.size();
     std::vector<int> order(tg[i].src.size());
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return codes[i][a] < codes[i][b]; });
-    const int64_t stream0 = (int64_t)pk.m2l_stream_idx.size();
+    const int64_t stream0 = stream_len;
     int prev = -1;
     int32_t cum = 0;  // offset in the target's source-pivot stream
     for (int e : order) {
@@ -1127,7 +1141,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       pk.m2l_src_off.push_back(moff[l][sn]);
       pk.m2l_src_cnt.push_back(ro);
       if (pk.m2l_sym) in_lists[(size_t)l].push_back({sn, stream0 + cum});
-      for (int k = 0; k < ro; ++k) pk.m2l_stream_idx.push_back((int32_t)(moff[l][sn] + k));
+      stream_len += ro;  // (the run's slots are written in parallel after the loop)
       cum += ro;
       const int64_t uses = pk.m2l_sym ? 2 : 1;  // a pair block serves both directions
       pk.m2l_entries += uses * (int64_t)ri * ro;
@@ -1141,7 +1155,17 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     pk.m2l_self_moff.push_back(moff[l][tg[i].node]);
     pk.m2l_rows.push_back(ri);
     pk.m2l_src_ptr.push_back((int32_t)pk.m2l_src_off.size());
-    pk.m2l_stream_ptr.push_back((int64_t)pk.m2l_stream_idx.size());
+    pk.m2l_stream_ptr.push_back(stream_len);
+  }
+  {  // the source streams: every run is the consecutive multipole slots of its source node
+    pk.m2l_stream_idx.resize((size_t)stream_len);
+    const size_t ntg = pk.m2l_rows.size();
+#pragma omp parallel for schedule(dynamic, 64)
+    for (size_t t = 0; t < ntg; ++t) {
+      int64_t pos = pk.m2l_stream_ptr[t];
+      for (int32_t e = pk.m2l_src_ptr[t]; e < pk.m2l_src_ptr[t + 1]; ++e)
+        for (int32_t k = 0; k < pk.m2l_src_cnt[e]; ++k) pk.m2l_stream_idx[(size_t)pos++] = (int32_t)(pk.m2l_src_off[e] + k);
+    }
   }
   if (pk.m2l_sym) {  // R22: the slot lists of every receiving node, level by level, by node id
     pk.m2l_in_ptr.assign(1, 0);
@@ -1158,6 +1182,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
       }
     }
   }
+  mark("M2L streams and slot lists");
   // leaves (every level, coarse first): near field and L2P.  The near field of a leaf B at
   // level l is every source leaf C whose ancestor at level min(l, l_C) neighbours B's (P:750-755,
   // R6; the adaptive U, W and X lists folded into the direct near field):
@@ -1258,6 +1283,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     }
   }
   pk.ops_len = ops_len;
+  mark("near lists, L2P");
   // ---- operator blocks on the device (F2): one group per (node, V~ or U~) sharing its cross
   // matrix; every job lists the caller indices of its columns (V~) or rows (U~) ----
   bool dev_ops = P.opt.setup_device && !P.opt.host_only;
@@ -1308,6 +1334,7 @@ int pack_plan(const Plan& P, Packed& pk, std::string& err, size_t device_free) {
     pk.ops_on_device = 1;
     return DAFMM_OK;
   }
+  mark("device operator jobs");
   // ---- operator blocks (column-major), in parallel ----
   try {
     pk.ops.assign((size_t)ops_len, cplx{0.0, 0.0});
