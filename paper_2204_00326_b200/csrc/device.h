@@ -25,6 +25,7 @@ struct DevBatch {
   bool wide = false;  // translate_kernel (warp per row) vs translate_rows_kernel (lane per row)
   int ipw = 1;        // translate_rows_kernel: items per warp (lane groups of 32 / ipw)
   bool colmajor = false;  // column-major items: translate_cm_kernel (lane per row, no reductions)
+  bool grouped = false;   // mean rows <= 16: translate_cm_kernel<true> (lane groups share a row block)
   int64_t* dst_off = nullptr;
   int32_t* dst_rows = nullptr;
   int32_t* term_ptr = nullptr;

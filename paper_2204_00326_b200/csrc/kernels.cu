@@ -221,6 +221,12 @@ __global__ void translate_rows_kernel(int items, const int64_t* __restrict__ dst
 // up to kTCMCols columns are staged in shared memory per warp and read as broadcasts.
 constexpr int kTCMCols = 128;
 constexpr int kTCMWarps = 8;
+// GROUPS (batches whose items have at most 16 rows, i.e. the directional levels): the warp splits
+// into G = 32 / P2 lane groups (P2 = the power of two >= R), group j takes the columns c = j (mod G)
+// and the groups' partial rows are added at the end (one xor-shuffle tree per item, fixed order),
+// so the small nodes still keep 32 lanes' worth of loads in flight.  Without GROUPS (48 registers
+// instead of 64) every lane owns a row; measured per batch shape in profiles/README.md (r2w).
+template <bool GROUPS>
 __global__ void __launch_bounds__(32 * kTCMWarps) translate_cm_kernel(
     int items, const int64_t* __restrict__ dst_off, const int32_t* __restrict__ dst_rows,
     const int64_t* __restrict__ item_mat_off, const int32_t* __restrict__ item_cols,
@@ -235,8 +241,14 @@ __global__ void __launch_bounds__(32 * kTCMWarps) translate_cm_kernel(
   const int tb = term_ptr[item], te = term_ptr[item + 1];
   const int64_t doff = dst_off[item];
   const double2* M = ops + item_mat_off[item];
-  for (int rb = 0; rb < R; rb += 32) {
-    const int t = rb + lane;
+  int lg = 5;
+  if (GROUPS) {
+    lg = 0;
+    while ((1 << lg) < min(R, 32)) ++lg;
+  }
+  const int P2 = 1 << lg, G = 32 >> lg, tl = lane & (P2 - 1), j = lane >> lg;
+  for (int rb = 0; rb < R; rb += P2) {
+    const int t = rb + tl;
     const bool act = t < R;
     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
     for (int cb = 0; cb < C; cb += kTCMCols) {
@@ -254,30 +266,38 @@ __global__ void __launch_bounds__(32 * kTCMWarps) translate_cm_kernel(
       __syncwarp();
       if (act) {
         const int nc = min(kTCMCols, C - cb);
-        const double2* p = M + (int64_t)cb * R + t;
-        int c = 0;
-        for (; c + 8 <= nc; c += 8, p += 8 * R) {
+        const int64_t step = (int64_t)G * R;
+        const double2* p = M + (int64_t)(cb + j) * R + t;
+        int c = j;
+        for (; c + 7 * G < nc; c += 8 * G, p += 8 * step) {
           double2 m[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) m[q] = ld2(p + q * R);
+          for (int q = 0; q < 8; ++q) m[q] = ld2(p + q * step);
 #pragma unroll
           for (int q = 0; q < 8; q += 2) {
-            const double2 v0 = xs[c + q], v1 = xs[c + q + 1];
+            const double2 v0 = xs[c + q * G], v1 = xs[c + (q + 1) * G];
             ar = fma(m[q].x, v0.x, fma(-m[q].y, v0.y, ar));
             ai = fma(m[q].x, v0.y, fma(m[q].y, v0.x, ai));
             br = fma(m[q + 1].x, v1.x, fma(-m[q + 1].y, v1.y, br));
             bi = fma(m[q + 1].x, v1.y, fma(m[q + 1].y, v1.x, bi));
           }
         }
-        for (; c < nc; ++c, p += R) {
+        for (; c < nc; c += G, p += step) {
           const double2 mm = ld2(p), v0 = xs[c];
           ar = fma(mm.x, v0.x, fma(-mm.y, v0.y, ar));
           ai = fma(mm.x, v0.y, fma(mm.y, v0.x, ai));
         }
       }
     }
-    if (act) {
-      double2 o = make_double2(ar + br, ai + bi);
+    ar += br;
+    ai += bi;
+    if (GROUPS)
+      for (int o = P2; o < 32; o <<= 1) {  // add the groups' partial rows
+        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+      }
+    if (act && j == 0) {
+      double2 o = make_double2(ar, ai);
       if (accumulate) {
         const double2 pv = dst[doff + t];
         o.x += pv.x;
@@ -1750,6 +1770,9 @@ bool upload_batch(DevPlan& d, DevBatch& b, const Packed::Batch& h, std::string& 
   int maxr = 0;
   for (int32_t r : h.dst_rows) maxr = std::max(maxr, (int)r);
   b.ipw = maxr <= 8 ? 4 : maxr <= 16 ? 2 : 1;
+  int64_t rows_sum = 0;
+  for (int32_t r : h.dst_rows) rows_sum += r;
+  b.grouped = b.items > 0 && rows_sum <= 16 * (int64_t)b.items;
   return upload(d, &b.dst_off, h.dst_off, err) && upload(d, &b.dst_rows, h.dst_rows, err) &&
          upload(d, &b.term_ptr, h.term_ptr, err) && upload(d, &b.item_mat_off, h.item_mat_off, err) &&
          upload(d, &b.item_cols, h.item_cols, err) &&
@@ -1761,8 +1784,12 @@ int launch_translate(const DevPlan& d, const DevBatch& b, const double2* src, do
   if (b.items == 0) return 0;
   int threads = 256;
   int blocks = (b.items * 32 + threads - 1) / threads;
-  if (b.colmajor)
-    translate_cm_kernel<<<(b.items + kTCMWarps - 1) / kTCMWarps, 32 * kTCMWarps, 0, st>>>(
+  if (b.colmajor && b.grouped)  // small nodes (mean rows <= 16): lane groups
+    translate_cm_kernel<true><<<(b.items + kTCMWarps - 1) / kTCMWarps, 32 * kTCMWarps, 0, st>>>(
+        b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols, b.term_ptr, b.src_off, b.src_cols, d.ops, src,
+        dst, accumulate);
+  else if (b.colmajor)
+    translate_cm_kernel<false><<<(b.items + kTCMWarps - 1) / kTCMWarps, 32 * kTCMWarps, 0, st>>>(
         b.items, b.dst_off, b.dst_rows, b.item_mat_off, b.item_cols, b.term_ptr, b.src_off, b.src_cols, d.ops, src,
         dst, accumulate);
   else if (b.wide)

@@ -1,5 +1,5 @@
 #!/bin/bash
-# r2w: translate_cm_kernel with lane groups for small-R items: C4/C3/C5 probe, ncu of the 7 launches, parity
+# r2w: translate_cm_kernel with lane groups for small-R batches: C4/C3/C5 probe, ncu of the 7 launches, parity
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 rm -f gpurun_out/r2w_probe.log
