@@ -64,6 +64,7 @@ struct DevPlan {
   int m2l_targets = 0;
   int m2l_leaf_targets = 0;       // the first m2l_leaf_targets targets are at the deepest level
   int m2l_grid = 1;               // persistent CTAs (SMs x resident CTAs per SM)
+  int near_after = 0;             // 2: the P2P starts when M2M has finished (far chain critical), 0: at the fork
   int* m2l_flag = nullptr;        // raised by the M2M stream when the coarser multipoles are complete
   int* m2l_ticket = nullptr;      // work counters (leaf-level part, rest), reset per matvec
   int64_t* m2l_loc_off = nullptr;

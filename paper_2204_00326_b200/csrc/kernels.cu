@@ -737,6 +737,9 @@ constexpr int kMSThreads = kMSConsumers + 32;  // + one producer warp (one elect
 #ifndef DAFMM_M2M_SIDE
 #define DAFMM_M2M_SIDE 0  // 1: M2M on a third stream beside the deepest level's stored M2L (flag handshake); measured slower at C4, C5 (profiles/README.md, r2p)
 #endif
+#ifndef DAFMM_NEAR_AFTER
+#define DAFMM_NEAR_AFTER -1  // P2P held back until P2M (1) / M2M (2) has finished, never (0), or per plan (-1)
+#endif
 #ifndef DAFMM_NEAR_HIGH
 #define DAFMM_NEAR_HIGH 0  // 1: the near-field stream gets the high priority instead of the far field
 #endif
@@ -1934,6 +1937,13 @@ int upload_plan(const Packed& pk, const Plan& plan, DevPlan& d, std::string& err
            // room for the stored-M2L CTA beside them
            ck(cudaFuncSetAttribute(p2p_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100), err, "carveout");
   }
+  {  // which chain is the critical path: the near field at its rate alone (4.2e11 point pairs / s)
+     // against the far field's bytes (stored M2L blocks + translation operators) at 6 TB/s; the
+     // on-the-fly M2L shares the fp64 pipe with the P2P, so nothing is held back then
+    const double t_near = (double)pk.p2p_pairs / 4.2e11;
+    const double t_far = d.m2l_mat ? (16.0 * (double)pk.m2l_stored_entries + 16.0 * (double)pk.ops_len) / 6.0e12 : 0.0;
+    d.near_after = t_far > 1.15 * t_near ? 2 : 0;
+  }
   int prio_lo = 0, prio_hi = 0;
   ok = ok && ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), err, "stream priorities") &&
        ck(cudaStreamCreateWithPriority(&d.s_far, cudaStreamNonBlocking, DAFMM_NEAR_HIGH ? prio_lo : prio_hi), err,
@@ -2054,6 +2064,15 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
   if (side_m2m) cudaMemsetAsync(d.m2l_flag, 0, sizeof(int), fs);
   mark(EV_P2M, fs);
   if (far) d.launches += launch_translate(d, d.p2m, d.v_t, d.mult, 0, fs);  // P2M
+  // The P2P can be held back until P2M (1) or M2M (2) has finished, so that the short translation
+  // kernels at the head of the far chain do not queue behind resident P2P CTAs.  It pays when the
+  // far chain is the critical path (d.near_after, chosen per plan in upload_plan: C4 3.24 -> 3.08 ms,
+  // C3 0.95 -> 0.90 ms) and not when the P2P is (C5: 8.81 -> 8.90 ms); profiles/README.md, r2aa.
+  const int near_after = DAFMM_NEAR_AFTER >= 0 ? DAFMM_NEAR_AFTER : d.near_after;
+  if (near_after == 1 && fork && !side_m2m && !DAFMM_LEAF_SPLIT) {
+    cudaEventRecord(d.ev_p2m, fs);
+    cudaStreamWaitEvent(ns, d.ev_p2m, 0);
+  }
   // M2L over targets [t0, t1) on stream st (ticket slot k for the on-the-fly kernel)
   auto m2l = [&](int t0, int t1, int k, cudaStream_t st) {
     if (t1 <= t0) return;
@@ -2109,6 +2128,10 @@ int run_matvec(DevPlan& d, const double2* x, double2* y, unsigned mask, std::str
     cudaEventRecord(d.ev_leaf, d.s_leaf);
   } else if (far) {
     for (auto& b : d.m2m) d.launches += launch_translate(d, b, d.mult, d.mult, 0, fs);  // M2M
+  }
+  if (near_after == 2 && fork && !side_m2m && !DAFMM_LEAF_SPLIT) {
+    cudaEventRecord(d.ev_p2m, fs);
+    cudaStreamWaitEvent(ns, d.ev_p2m, 0);
   }
   mark(EV_M2L, fs);
   if (far) m2l(nleaf, d.m2l_targets, 1, fs);  // M2L: all (remaining) levels
